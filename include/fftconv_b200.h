@@ -1,0 +1,149 @@
+/*
+ * fftconv_b200 -- C ABI of the B200 (sm_100a) FFT-convolution hot path.
+ *
+ * Drop-in replacement for the reference fftconv::ConvWorkspace<float>
+ * operator interface (/root/reference/proj/include/fftconv/conv_fft.hpp).
+ * Plain pointers and sizes only; no C++ or torch types cross this boundary.
+ * Each entry point names the reference interface it replaces.
+ *
+ * Tensor layouts are the reference's (tensor.hpp:13-15, :63-64):
+ *   x, gx  [S][f][n][n]      fp32 row-major
+ *   y, gy  [S][f'][n'][n']   n' = n - k + 1
+ *   w, gw  [f'][f][k][k]
+ *
+ * Status codes mirror the reference exception classes (errors.hpp:7-41);
+ * validation happens before any work, in the reference's order
+ * (conv_fft.hpp:76-83, :117-122, :156-164): shape/size checks, then the
+ * layer config (config_error), then the workspace capacity.
+ *
+ * Threading: a workspace serves one invocation at a time (conv_fft.hpp:37-38);
+ * calls on one workspace are not reentrant.  Device entry points enqueue on
+ * the caller's stream and return without synchronising.
+ */
+#ifndef FFTCONV_B200_H_
+#define FFTCONV_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes -- fftconv::error subclasses (errors.hpp). */
+enum fftconv_b200_status {
+  FFTCONV_B200_OK = 0,
+  FFTCONV_B200_SIZE_ERROR = 1,     /* fftconv::size_error     */
+  FFTCONV_B200_SHAPE_ERROR = 2,    /* fftconv::shape_error    */
+  FFTCONV_B200_CONFIG_ERROR = 3,   /* fftconv::config_error   */
+  FFTCONV_B200_CAPACITY_ERROR = 4, /* fftconv::capacity_error */
+  FFTCONV_B200_PLAN_ERROR = 5,     /* fftconv::plan_error     */
+  FFTCONV_B200_CUDA_ERROR = 6,     /* CUDA runtime/driver failure */
+  FFTCONV_B200_NCCL_ERROR = 7,     /* reserved: collective failure */
+  FFTCONV_B200_INVALID_ARGUMENT = 8
+};
+
+/* fftconv::LayerConfig (layer_config.hpp:22-40): {k, n, f, f', S}. */
+typedef struct fftconv_b200_layer {
+  size_t kernel;   /* k  */
+  size_t image;    /* n  */
+  size_t in_maps;  /* f  */
+  size_t out_maps; /* f' */
+  size_t batch;    /* S  */
+} fftconv_b200_layer;
+
+typedef struct fftconv_b200_ws fftconv_b200_ws;
+
+/* ConvWorkspace<T>::ConvWorkspace(configs)  conv_fft.hpp:43-58
+ * Capacities are the per-role maxima over `configs` exactly as the
+ * reference computes them; device buffers are allocated once here.
+ * Empty list or invalid config -> FFTCONV_B200_CONFIG_ERROR. */
+int fftconv_b200_ws_create(const fftconv_b200_layer* configs, size_t count, int device,
+                           fftconv_b200_ws** out);
+void fftconv_b200_ws_destroy(fftconv_b200_ws* ws);
+
+/* Thread-local message of the last failure on this thread, or of the
+ * workspace (when non-NULL). */
+const char* fftconv_b200_last_error(const fftconv_b200_ws* ws);
+
+/* ConvWorkspace::max_fft_size/capacity_x/capacity_w/capacity_y/
+ * frequency_bytes  conv_fft.hpp:60-69.
+ * out[0..4] = max_fft_size, cap_x, cap_w, cap_y, frequency_bytes (the
+ * reference's accounting); out[5] = device bytes actually held. */
+int fftconv_b200_ws_info(const fftconv_b200_ws* ws, uint64_t out[6]);
+
+/* ConvWorkspace::counters / reset_counters  conv_fft.hpp:71-72 (OpCounters
+ * :22-28): out = forward_transforms, inverse_transforms, complex_macs. */
+int fftconv_b200_counters(const fftconv_b200_ws* ws, uint64_t out[3]);
+int fftconv_b200_reset_counters(fftconv_b200_ws* ws);
+
+/* ---- Device-pointer operators (inputs/outputs resident in HBM) ---------- */
+
+/* ConvWorkspace<float>::forward(x, w)  conv_fft.hpp:74-113.
+ * x: [S][f][x_rows][x_cols]; w: [w_out][w_in][k][k]; y: [S][w_out][n'][n'].
+ * `stream` is a cudaStream_t (NULL = legacy default stream). */
+int fftconv_b200_forward(fftconv_b200_ws* ws, const float* x, size_t S, size_t f, size_t x_rows,
+                         size_t x_cols, const float* w, size_t w_out, size_t w_in, size_t k,
+                         float* y, void* stream);
+
+/* ConvWorkspace<float>::grad_input(gy, w)  conv_fft.hpp:115-152.
+ * gy: [S][fo][gy_rows][gy_cols]; gx: [S][w_in][n][n], n = gy_rows + k - 1. */
+int fftconv_b200_grad_input(fftconv_b200_ws* ws, const float* gy, size_t S, size_t fo,
+                            size_t gy_rows, size_t gy_cols, const float* w, size_t w_out,
+                            size_t w_in, size_t k, float* gx, void* stream);
+
+/* ConvWorkspace<float>::grad_weight(gy, x)  conv_fft.hpp:154-206.
+ * gw: [fo][f][k][k], k = x_rows - gy_rows + 1. */
+int fftconv_b200_grad_weight(fftconv_b200_ws* ws, const float* gy, size_t S_gy, size_t fo,
+                             size_t gy_rows, size_t gy_cols, const float* x, size_t S_x,
+                             size_t f, size_t x_rows, size_t x_cols, float* gw, void* stream);
+
+/* ---- Host-pointer operators (the drop-in: Tensor4/Weights4 storage) ------
+ * Same contracts; inputs are copied host->device, the result device->host,
+ * and the call returns after the result is in `y`/`gx`/`gw`.  `threads`
+ * is accepted for interface parity (conv_fft.hpp:75) and ignored. */
+int fftconv_b200_forward_host(fftconv_b200_ws* ws, const float* x, size_t S, size_t f,
+                              size_t x_rows, size_t x_cols, const float* w, size_t w_out,
+                              size_t w_in, size_t k, float* y, unsigned threads);
+int fftconv_b200_grad_input_host(fftconv_b200_ws* ws, const float* gy, size_t S, size_t fo,
+                                 size_t gy_rows, size_t gy_cols, const float* w, size_t w_out,
+                                 size_t w_in, size_t k, float* gx, unsigned threads);
+int fftconv_b200_grad_weight_host(fftconv_b200_ws* ws, const float* gy, size_t S_gy, size_t fo,
+                                  size_t gy_rows, size_t gy_cols, const float* x, size_t S_x,
+                                  size_t f, size_t x_rows, size_t x_cols, float* gw,
+                                  unsigned threads);
+
+/* ---- Instrumentation ----------------------------------------------------
+ * When enabled, each operator records CUDA events between its stages on
+ * the launching stream; fftconv_b200_stage_ms returns the last call's
+ * per-stage device times (ms): [0] r2c of operand A, [1] r2c of operand B,
+ * [2] per-bin complex GEMM, [3] c2r + crop.  Blocks until they are known. */
+int fftconv_b200_set_stage_timing(fftconv_b200_ws* ws, int enable);
+int fftconv_b200_stage_ms(fftconv_b200_ws* ws, float out[4]);
+
+/* Number of kernel launches the last operator call enqueued. */
+int fftconv_b200_last_launch_count(const fftconv_b200_ws* ws);
+
+/* ---- Unit-level test hooks (K1 / K4 / K3 in isolation) ------------------ */
+
+/* Forward 2-D real transforms of `planes` square src x src planes
+ * (zero-padded to m x m, m = next_pow2 >= src) into the half spectrum
+ * out[p][u][v] (u in [0, m/2], v in [0, m)), complex interleaved.  This is
+ * the transpose of the reference HalfSpectrum packing (fft.hpp:105-152):
+ * reference packed_bin(u, v) for v <= m/2 equals out[v][u] here. */
+int fftconv_b200_debug_r2c(const float* in, size_t planes, size_t src, size_t m, float* out,
+                           void* stream);
+/* Inverse of the above with top-left crop x crop, scaled by 1/m^2. */
+int fftconv_b200_debug_c2r(const float* in, size_t planes, size_t m, size_t crop, float* out,
+                           void* stream);
+/* Batched complex GEMM per bin, mode 0 fprop (A.conj(B)^T), 1 bprop
+ * (A.B^T), 2 accGrad (conj(A).B^T): a [bins][M][K], b [bins][N][K],
+ * out [bins][N][M], all complex interleaved fp32. */
+int fftconv_b200_debug_cgemm(const float* a, const float* b, float* out, size_t bins, size_t M,
+                             size_t N, size_t K, int mode, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FFTCONV_B200_H_ */

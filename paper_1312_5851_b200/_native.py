@@ -1,0 +1,69 @@
+"""ctypes binding of the C ABI in include/fftconv_b200.h.
+
+The CUDA library is built in-tree (``paper_1312_5851_b200/lib``) by
+``build.py``.  There is no fallback of any kind: if the library is missing or
+cannot be loaded, every operator raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from functools import lru_cache
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libfftconv_b200.so")
+
+_sz = C.c_size_t
+_p = C.c_void_p
+_i = C.c_int
+
+# Every symbol the header declares: (name, restype, argtypes).
+SIGNATURES = [
+    ("fftconv_b200_ws_create", _i, [_p, _sz, _i, C.POINTER(_p)]),
+    ("fftconv_b200_ws_destroy", None, [_p]),
+    ("fftconv_b200_last_error", C.c_char_p, [_p]),
+    ("fftconv_b200_ws_info", _i, [_p, _p]),
+    ("fftconv_b200_counters", _i, [_p, _p]),
+    ("fftconv_b200_reset_counters", _i, [_p]),
+    ("fftconv_b200_forward", _i, [_p, _p, _sz, _sz, _sz, _sz, _p, _sz, _sz, _sz, _p, _p]),
+    ("fftconv_b200_grad_input", _i, [_p, _p, _sz, _sz, _sz, _sz, _p, _sz, _sz, _sz, _p, _p]),
+    ("fftconv_b200_grad_weight", _i, [_p, _p, _sz, _sz, _sz, _sz, _p, _sz, _sz, _sz, _sz, _p, _p]),
+    ("fftconv_b200_forward_host", _i, [_p, _p, _sz, _sz, _sz, _sz, _p, _sz, _sz, _sz, _p, C.c_uint]),
+    ("fftconv_b200_grad_input_host", _i, [_p, _p, _sz, _sz, _sz, _sz, _p, _sz, _sz, _sz, _p, C.c_uint]),
+    ("fftconv_b200_grad_weight_host", _i, [_p, _p, _sz, _sz, _sz, _sz, _p, _sz, _sz, _sz, _sz, _p, C.c_uint]),
+    ("fftconv_b200_set_stage_timing", _i, [_p, _i]),
+    ("fftconv_b200_stage_ms", _i, [_p, _p]),
+    ("fftconv_b200_last_launch_count", _i, [_p]),
+    ("fftconv_b200_debug_r2c", _i, [_p, _sz, _sz, _sz, _p, _p]),
+    ("fftconv_b200_debug_c2r", _i, [_p, _sz, _sz, _sz, _p, _p]),
+    ("fftconv_b200_debug_cgemm", _i, [_p, _p, _p, _sz, _sz, _sz, _sz, _i, _p]),
+]
+
+
+class Layer(C.Structure):
+    """fftconv_b200_layer == fftconv::LayerConfig {k, n, f, f', S}."""
+
+    _fields_ = [("kernel", _sz), ("image", _sz), ("in_maps", _sz), ("out_maps", _sz), ("batch", _sz)]
+
+
+class NativeLibraryMissing(ImportError):
+    pass
+
+
+@lru_cache(maxsize=None)
+def lib() -> C.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise NativeLibraryMissing(
+            f"{LIB_PATH} not found: build the CUDA library with `python build.py` "
+            "(there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    for name, res, args in SIGNATURES:
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    return L
+
+
+def last_error(ws=None) -> str:
+    msg = lib().fftconv_b200_last_error(ws)
+    return msg.decode() if msg else ""

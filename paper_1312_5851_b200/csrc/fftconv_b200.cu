@@ -1,0 +1,746 @@
+// fftconv_b200: B200-native FFT convolution layer (fprop / bprop / accGrad)
+// behind the reference ConvWorkspace operator interface.
+//
+// Host side of the C ABI declared in include/fftconv_b200.h.  Each operator
+// is four launches on the caller's stream:
+//   K1 r2c(operand A) -> K1 r2c(operand B) -> K3 per-bin complex GEMM
+//   (tcgen05, 3xTF32) -> K4 c2r + crop.
+// Reference call stacks this replaces: SURVEY.md section 3 (A)-(C);
+// ConvWorkspace<T>::forward/grad_input/grad_weight at conv_fft.hpp:74-206.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/fftconv_b200.h"
+#include "cgemm_tcgen05.cuh"
+#include "fft_planes.cuh"
+
+namespace fcb {
+
+// ------------------------------------------------------------ errors
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+static thread_local std::string g_last_error;
+
+#define FCB_CUDA(call)                                                                     \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      throw Error(FFTCONV_B200_CUDA_ERROR,                                                 \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                     \
+  } while (0)
+
+// ------------------------------------------------------------ layer maths
+static size_t next_pow2(size_t n) {
+  size_t m = 1;
+  while (m < n) m <<= 1;
+  return m;
+}
+static size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// LayerConfig::validate (layer_config.hpp:32-39)
+static void validate_cfg(const fftconv_b200_layer& c) {
+  if (c.kernel == 0 || c.image == 0 || c.in_maps == 0 || c.out_maps == 0 || c.batch == 0)
+    throw Error(FFTCONV_B200_CONFIG_ERROR, "layer config: all parameters must be >= 1");
+  if (c.kernel > c.image)
+    throw Error(FFTCONV_B200_CONFIG_ERROR, "layer config: kernel " + std::to_string(c.kernel) +
+                                               " exceeds image " + std::to_string(c.image));
+}
+
+enum Pass { kFprop = 0, kBprop = 1, kAccGrad = 2 };
+
+// Device bytes (floats) each pass needs in the three frequency buffers.
+struct PassNeed {
+  size_t a, b, d;
+};
+static PassNeed pass_need(Pass pass, size_t S, size_t f, size_t fo, size_t m) {
+  const size_t bins = m * (m / 2 + 1);
+  switch (pass) {
+    case kFprop:
+      return {bins * S * 2 * round_up(f, 16), bins * fo * 2 * round_up(f, 16), bins * fo * 2 * S};
+    case kBprop:
+      return {bins * S * 2 * round_up(fo, 16), bins * f * 2 * round_up(fo, 16), bins * f * 2 * S};
+    default:
+      return {bins * fo * 2 * round_up(S, 16), bins * f * 2 * round_up(S, 16), bins * f * 2 * fo};
+  }
+}
+
+// ------------------------------------------------------------ driver API
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  if (!fn) throw Error(FFTCONV_B200_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// 3-D fp32 map over F[t][rows][2*kpad]; box {32 floats, box_rows, 1}, SW128.
+static CUtensorMap make_operand_map(const float* base, size_t kpad, size_t rows, size_t bins,
+                                    uint32_t box_rows) {
+  CUtensorMap m;
+  const cuuint64_t dims[3] = {2 * kpad, rows, bins};
+  const cuuint64_t strides[2] = {2 * kpad * sizeof(float), rows * 2 * kpad * sizeof(float)};
+  const cuuint32_t box[3] = {32, box_rows, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw Error(FFTCONV_B200_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return m;
+}
+
+// ------------------------------------------------------------ launchers
+struct DevInfo {
+  int sms = 148;
+  int max_smem_optin = 232448;
+};
+static DevInfo dev_info(int device) {
+  DevInfo d;
+  cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, device);
+  cudaDeviceGetAttribute(&d.max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  return d;
+}
+
+template <int M>
+struct R2CTraits {
+  static constexpr int PC = M / 2 + 1;
+  static constexpr int UC = (M == 64) ? 11 : PC;
+  static constexpr int SPLIT = (M == 64) ? 2 : 1;
+};
+
+template <int M>
+static void launch_r2c_m(const R2CParams& p, cudaStream_t st) {
+  using Tr = R2CTraits<M>;
+  auto kern = r2c_planes_kernel<M, Tr::UC, Tr::SPLIT>;
+  const size_t smem = (size_t)kPlaneGroup * Tr::UC * p.cpad * sizeof(float2);
+  if (smem > 48 * 1024)
+    FCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid(p.kpad / kPlaneGroup, p.R, (Tr::PC + Tr::UC - 1) / Tr::UC);
+  kern<<<grid, 256, smem, st>>>(p);
+  FCB_CUDA(cudaGetLastError());
+}
+
+static void launch_r2c(size_t m, const R2CParams& p, cudaStream_t st) {
+  switch (m) {
+    case 1: return launch_r2c_m<1>(p, st);
+    case 2: return launch_r2c_m<2>(p, st);
+    case 4: return launch_r2c_m<4>(p, st);
+    case 8: return launch_r2c_m<8>(p, st);
+    case 16: return launch_r2c_m<16>(p, st);
+    case 32: return launch_r2c_m<32>(p, st);
+    case 64: return launch_r2c_m<64>(p, st);
+    default:
+      throw Error(FFTCONV_B200_SIZE_ERROR,
+                  "fft size " + std::to_string(m) + " not supported by the B200 kernels (max 64)");
+  }
+}
+
+template <int M>
+static void launch_c2r_m(C2RParams p, cudaStream_t st) {
+  constexpr int PC = M / 2 + 1;
+  constexpr int SPLIT = (M == 64) ? 2 : 1;
+  constexpr int CCMAX = (M == 64) ? 22 : 32;
+  const int nchunks = (p.crop + CCMAX - 1) / CCMAX;
+  p.cc = (p.crop + nchunks - 1) / nchunks;
+  p.ccpad = (p.cc % 2) ? p.cc : p.cc + 1;
+  auto kern = c2r_planes_kernel<M, SPLIT>;
+  const size_t smem = (size_t)kPlaneGroup * PC * p.ccpad * sizeof(float2);
+  if (smem > 48 * 1024)
+    FCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid((p.J + kPlaneGroup - 1) / kPlaneGroup, p.R, nchunks);
+  kern<<<grid, 256, smem, st>>>(p);
+  FCB_CUDA(cudaGetLastError());
+}
+
+static void launch_c2r(size_t m, const C2RParams& p, cudaStream_t st) {
+  switch (m) {
+    case 1: return launch_c2r_m<1>(p, st);
+    case 2: return launch_c2r_m<2>(p, st);
+    case 4: return launch_c2r_m<4>(p, st);
+    case 8: return launch_c2r_m<8>(p, st);
+    case 16: return launch_c2r_m<16>(p, st);
+    case 32: return launch_c2r_m<32>(p, st);
+    case 64: return launch_c2r_m<64>(p, st);
+    default:
+      throw Error(FFTCONV_B200_SIZE_ERROR,
+                  "fft size " + std::to_string(m) + " not supported by the B200 kernels (max 64)");
+  }
+}
+
+struct GemmGeom {
+  int nc, n_tiles, m_tiles, stages;
+  size_t smem;
+};
+static GemmGeom gemm_geom(size_t M, size_t N, const DevInfo& di) {
+  GemmGeom g;
+  const size_t n16 = round_up(N, 16);
+  g.n_tiles = (int)((n16 + 127) / 128);
+  g.nc = (int)round_up((n16 + g.n_tiles - 1) / g.n_tiles, 16);
+  g.m_tiles = (int)((M + kTileM - 1) / kTileM);
+  const int sb = gemm_stage_bytes(g.nc);
+  const int budget = di.max_smem_optin - 1024 - 256;
+  g.stages = std::min(4, budget / sb);
+  if (g.stages < 2) throw Error(FFTCONV_B200_CUDA_ERROR, "gemm tile does not fit shared memory");
+  g.smem = (size_t)g.stages * sb + 1024 + 256;
+  return g;
+}
+
+static void launch_gemm(const float* A, const float* B, float* out, size_t bins, size_t M,
+                        size_t N, size_t kpad, int mode, const DevInfo& di, cudaStream_t st) {
+  const GemmGeom g = gemm_geom(M, N, di);
+  CUtensorMap ta = make_operand_map(A, kpad, M, bins, kTileM);
+  CUtensorMap tb = make_operand_map(B, kpad, N, bins, (uint32_t)g.nc);
+  GemmParams p;
+  p.out = out;
+  p.bins = (int)bins;
+  p.m_valid = (int)M;
+  p.n_valid = (int)N;
+  p.k_chunks = (int)(kpad / 16);
+  p.m_tiles = g.m_tiles;
+  p.n_tiles = g.n_tiles;
+  p.nc = g.nc;
+  p.stages = g.stages;
+  p.mode = mode;
+  FCB_CUDA(cudaFuncSetAttribute(cgemm_bins_tcgen05, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)g.smem));
+  const long long tiles = (long long)bins * g.m_tiles * g.n_tiles;
+  const int grid = (int)std::min<long long>(tiles, di.sms);
+  cgemm_bins_tcgen05<<<grid, kGemmThreads, g.smem, st>>>(ta, tb, p);
+  FCB_CUDA(cudaGetLastError());
+}
+
+}  // namespace fcb
+
+using namespace fcb;
+
+// ------------------------------------------------------------ workspace
+struct fftconv_b200_ws {
+  int device = 0;
+  DevInfo di;
+  uint64_t cap_x = 0, cap_w = 0, cap_y = 0;
+  size_t max_m = 1;
+  // frequency-domain buffers (floats)
+  float* bufA = nullptr;
+  float* bufB = nullptr;
+  float* bufD = nullptr;
+  size_t nA = 0, nB = 0, nD = 0;
+  // host-API device staging
+  float* st_in0 = nullptr;
+  float* st_in1 = nullptr;
+  float* st_out = nullptr;
+  size_t n_in0 = 0, n_in1 = 0, n_out = 0;
+  cudaStream_t host_stream = nullptr;
+  uint64_t ctr[3] = {0, 0, 0};
+  std::string last_error;
+  bool timing = false;
+  cudaEvent_t ev[5] = {};
+  bool ev_ready = false;
+  int last_launches = 0;
+};
+
+namespace {
+
+template <typename F>
+int guarded(fftconv_b200_ws* ws, F&& f) {
+  try {
+    f();
+    return FFTCONV_B200_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    if (ws) ws->last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    if (ws) ws->last_error = e.what();
+    return FFTCONV_B200_INVALID_ARGUMENT;
+  }
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int d) {
+    cudaGetDevice(&prev);
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+void grow(float*& p, size_t& have, size_t need) {
+  if (need <= have) return;
+  if (p) cudaFree(p);
+  p = nullptr;
+  have = 0;
+  FCB_CUDA(cudaMalloc(&p, need * sizeof(float)));
+  have = need;
+}
+
+// ConvWorkspace::prepare (conv_fft.hpp:211-222): validate -> capacity.
+size_t prepare(fftconv_b200_ws* ws, const fftconv_b200_layer& c) {
+  validate_cfg(c);
+  const size_t m = next_pow2(c.image);
+  const uint64_t bins = m * (m / 2 + 1);
+  if (bins * c.batch * c.in_maps > ws->cap_x || bins * c.out_maps * c.in_maps > ws->cap_w ||
+      bins * c.batch * c.out_maps > ws->cap_y)
+    throw Error(FFTCONV_B200_CAPACITY_ERROR, "workspace too small for this layer");
+  if (m > 64)
+    throw Error(FFTCONV_B200_SIZE_ERROR,
+                "fft size " + std::to_string(m) + " not supported by the B200 kernels (max 64)");
+  return m;
+}
+
+void ensure_freq(fftconv_b200_ws* ws, Pass pass, const fftconv_b200_layer& c, size_t m) {
+  const PassNeed need = pass_need(pass, c.batch, c.in_maps, c.out_maps, m);
+  grow(ws->bufA, ws->nA, need.a);
+  grow(ws->bufB, ws->nB, need.b);
+  grow(ws->bufD, ws->nD, need.d);
+}
+
+void record(fftconv_b200_ws* ws, int i, cudaStream_t st) {
+  if (!ws->timing) return;
+  if (!ws->ev_ready) {
+    for (auto& e : ws->ev) FCB_CUDA(cudaEventCreate(&e));
+    ws->ev_ready = true;
+  }
+  FCB_CUDA(cudaEventRecord(ws->ev[i], st));
+}
+
+void require_nonzero(size_t a, size_t b, size_t c, size_t d, const char* what) {
+  if (!a || !b || !c || !d)
+    throw Error(FFTCONV_B200_SIZE_ERROR, std::string(what) + ": all dimensions must be >= 1");
+}
+
+// ---- the three operators (device pointers) ---------------------------
+
+void run_forward(fftconv_b200_ws* ws, const float* x, size_t S, size_t f, size_t xr, size_t xc,
+                 const float* w, size_t wo, size_t wi, size_t k, float* y, cudaStream_t st) {
+  require_nonzero(S, f, xr, xc, "Tensor4");
+  require_nonzero(wo, wi, k, 1, "Weights4");
+  if (xr != xc) throw Error(FFTCONV_B200_SIZE_ERROR, "forward_fft: planes must be square");
+  if (wi != f) throw Error(FFTCONV_B200_SHAPE_ERROR, "forward_fft: weight in_maps != input maps");
+  if (k > xr) throw Error(FFTCONV_B200_SIZE_ERROR, "forward_fft: kernel larger than image");
+  const size_t n = xr, no = n - k + 1, fo = wo;
+  const fftconv_b200_layer cfg{k, n, f, fo, S};
+  const size_t m = prepare(ws, cfg);
+  const size_t bins = m * (m / 2 + 1);
+  ensure_freq(ws, kFprop, cfg, m);
+  const size_t kp = round_up(f, 16);
+
+  record(ws, 0, st);
+  R2CParams a{x, ws->bufA, (long long)(f * n * n), (long long)(n * n), (int)S, (int)f, (int)kp,
+              (int)n, (int)(n | 1)};
+  launch_r2c(m, a, st);
+  record(ws, 1, st);
+  R2CParams b{w, ws->bufB, (long long)(f * k * k), (long long)(k * k), (int)fo, (int)f, (int)kp,
+              (int)k, (int)(k | 1)};
+  launch_r2c(m, b, st);
+  record(ws, 2, st);
+  launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, S, fo, kp, kModeFprop, ws->di, st);
+  record(ws, 3, st);
+  C2RParams c{ws->bufD, y, (long long)(no * no), (long long)(fo * no * no), (int)fo, (int)S,
+              (int)no, 0, 0, 1.0f / (float)(m * m)};
+  launch_c2r(m, c, st);
+  record(ws, 4, st);
+  ws->last_launches = 4;
+  ws->ctr[0] += S * f + fo * f;
+  ws->ctr[1] += S * fo;
+  ws->ctr[2] += (uint64_t)bins * fo * f * S;
+}
+
+void run_grad_input(fftconv_b200_ws* ws, const float* gy, size_t S, size_t fo, size_t gr,
+                    size_t gc, const float* w, size_t wo, size_t wi, size_t k, float* gx,
+                    cudaStream_t st) {
+  require_nonzero(S, fo, gr, gc, "Tensor4");
+  require_nonzero(wo, wi, k, 1, "Weights4");
+  if (gr != gc) throw Error(FFTCONV_B200_SIZE_ERROR, "grad_input_fft: planes must be square");
+  if (wo != fo)
+    throw Error(FFTCONV_B200_SHAPE_ERROR, "grad_input_fft: weight out_maps != gradient maps");
+  const size_t no = gr, n = no + k - 1, f = wi;
+  const fftconv_b200_layer cfg{k, n, f, fo, S};
+  const size_t m = prepare(ws, cfg);
+  const size_t bins = m * (m / 2 + 1);
+  ensure_freq(ws, kBprop, cfg, m);
+  const size_t kp = round_up(fo, 16);
+
+  record(ws, 0, st);
+  R2CParams a{gy, ws->bufA, (long long)(fo * no * no), (long long)(no * no), (int)S, (int)fo,
+              (int)kp, (int)no, (int)(no | 1)};
+  launch_r2c(m, a, st);
+  record(ws, 1, st);
+  R2CParams b{w, ws->bufB, (long long)(k * k), (long long)(f * k * k), (int)f, (int)fo, (int)kp,
+              (int)k, (int)(k | 1)};
+  launch_r2c(m, b, st);
+  record(ws, 2, st);
+  launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, S, f, kp, kModeBprop, ws->di, st);
+  record(ws, 3, st);
+  C2RParams c{ws->bufD, gx, (long long)(n * n), (long long)(f * n * n), (int)f, (int)S, (int)n,
+              0, 0, 1.0f / (float)(m * m)};
+  launch_c2r(m, c, st);
+  record(ws, 4, st);
+  ws->last_launches = 4;
+  ws->ctr[0] += S * fo + fo * f;
+  ws->ctr[1] += S * f;
+  ws->ctr[2] += (uint64_t)bins * fo * f * S;
+}
+
+void run_grad_weight(fftconv_b200_ws* ws, const float* gy, size_t Sg, size_t fo, size_t gr,
+                     size_t gc, const float* x, size_t Sx, size_t f, size_t xr, size_t xc,
+                     float* gw, cudaStream_t st) {
+  require_nonzero(Sg, fo, gr, gc, "Tensor4");
+  require_nonzero(Sx, f, xr, xc, "Tensor4");
+  if (gr != gc) throw Error(FFTCONV_B200_SIZE_ERROR, "grad_weight_fft: planes must be square");
+  if (xr != xc) throw Error(FFTCONV_B200_SIZE_ERROR, "grad_weight_fft: planes must be square");
+  if (Sg != Sx) throw Error(FFTCONV_B200_SHAPE_ERROR, "grad_weight_fft: batch mismatch");
+  const size_t no = gr, n = xr;
+  if (no > n) throw Error(FFTCONV_B200_SIZE_ERROR, "grad_weight_fft: gradient larger than input");
+  const size_t k = n - no + 1, S = Sx;
+  const fftconv_b200_layer cfg{k, n, f, fo, S};
+  const size_t m = prepare(ws, cfg);
+  const size_t bins = m * (m / 2 + 1);
+  ensure_freq(ws, kAccGrad, cfg, m);
+  const size_t kp = round_up(S, 16);
+
+  record(ws, 0, st);
+  R2CParams a{gy, ws->bufA, (long long)(no * no), (long long)(fo * no * no), (int)fo, (int)S,
+              (int)kp, (int)no, (int)(no | 1)};
+  launch_r2c(m, a, st);
+  record(ws, 1, st);
+  R2CParams b{x, ws->bufB, (long long)(n * n), (long long)(f * n * n), (int)f, (int)S, (int)kp,
+              (int)n, (int)(n | 1)};
+  launch_r2c(m, b, st);
+  record(ws, 2, st);
+  launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, fo, f, kp, kModeAccGrad, ws->di, st);
+  record(ws, 3, st);
+  C2RParams c{ws->bufD, gw, (long long)(k * k), (long long)(f * k * k), (int)f, (int)fo, (int)k,
+              0, 0, 1.0f / (float)(m * m)};
+  launch_c2r(m, c, st);
+  record(ws, 4, st);
+  ws->last_launches = 4;
+  ws->ctr[0] += S * f + S * fo;
+  ws->ctr[1] += fo * f;
+  ws->ctr[2] += (uint64_t)bins * fo * f * S;
+}
+
+// Host-pointer staging helpers.
+void stage_in(fftconv_b200_ws* ws, float*& dst, size_t& have, const float* src, size_t n) {
+  grow(dst, have, n);
+  FCB_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(float), cudaMemcpyHostToDevice, ws->host_stream));
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ C ABI
+extern "C" {
+
+int fftconv_b200_ws_create(const fftconv_b200_layer* configs, size_t count, int device,
+                           fftconv_b200_ws** out) {
+  return guarded(nullptr, [&] {
+    if (!out) throw Error(FFTCONV_B200_INVALID_ARGUMENT, "out is NULL");
+    *out = nullptr;
+    if (count == 0 || !configs)
+      throw Error(FFTCONV_B200_CONFIG_ERROR, "workspace: at least one layer config required");
+    auto* ws = new fftconv_b200_ws;
+    try {
+      ws->device = device;
+      for (size_t i = 0; i < count; ++i) {
+        const auto& c = configs[i];
+        validate_cfg(c);
+        const uint64_t m = next_pow2(c.image);
+        const uint64_t bins = m * (m / 2 + 1);
+        ws->cap_x = std::max<uint64_t>(ws->cap_x, bins * c.batch * c.in_maps);
+        ws->cap_w = std::max<uint64_t>(ws->cap_w, bins * c.out_maps * c.in_maps);
+        ws->cap_y = std::max<uint64_t>(ws->cap_y, bins * c.batch * c.out_maps);
+        ws->max_m = std::max<size_t>(ws->max_m, m);
+      }
+      DeviceGuard g(device);
+      ws->di = dev_info(device);
+      FCB_CUDA(cudaStreamCreateWithFlags(&ws->host_stream, cudaStreamNonBlocking));
+      // Size the frequency buffers for every registered layer and pass up
+      // front, so timed calls never allocate.
+      size_t na = 0, nb = 0, nd = 0;
+      for (size_t i = 0; i < count; ++i) {
+        const auto& c = configs[i];
+        const size_t m = next_pow2(c.image);
+        for (Pass p : {kFprop, kBprop, kAccGrad}) {
+          const PassNeed need = pass_need(p, c.batch, c.in_maps, c.out_maps, m);
+          na = std::max(na, need.a);
+          nb = std::max(nb, need.b);
+          nd = std::max(nd, need.d);
+        }
+      }
+      grow(ws->bufA, ws->nA, na);
+      grow(ws->bufB, ws->nB, nb);
+      grow(ws->bufD, ws->nD, nd);
+    } catch (...) {
+      fftconv_b200_ws_destroy(ws);
+      throw;
+    }
+    *out = ws;
+  });
+}
+
+void fftconv_b200_ws_destroy(fftconv_b200_ws* ws) {
+  if (!ws) return;
+  {
+    DeviceGuard g(ws->device);
+    for (float* p : {ws->bufA, ws->bufB, ws->bufD, ws->st_in0, ws->st_in1, ws->st_out})
+      if (p) cudaFree(p);
+    if (ws->host_stream) cudaStreamDestroy(ws->host_stream);
+    if (ws->ev_ready)
+      for (auto& e : ws->ev) cudaEventDestroy(e);
+  }
+  delete ws;
+}
+
+const char* fftconv_b200_last_error(const fftconv_b200_ws* ws) {
+  return ws ? ws->last_error.c_str() : g_last_error.c_str();
+}
+
+int fftconv_b200_ws_info(const fftconv_b200_ws* ws, uint64_t out[6]) {
+  if (!ws || !out) return FFTCONV_B200_INVALID_ARGUMENT;
+  out[0] = ws->max_m;
+  out[1] = ws->cap_x;
+  out[2] = ws->cap_w;
+  out[3] = ws->cap_y;
+  out[4] = (ws->cap_x + ws->cap_w + ws->cap_y) * 8;  // sizeof(std::complex<float>)
+  out[5] = (ws->nA + ws->nB + ws->nD + ws->n_in0 + ws->n_in1 + ws->n_out) * sizeof(float);
+  return FFTCONV_B200_OK;
+}
+
+int fftconv_b200_counters(const fftconv_b200_ws* ws, uint64_t out[3]) {
+  if (!ws || !out) return FFTCONV_B200_INVALID_ARGUMENT;
+  for (int i = 0; i < 3; ++i) out[i] = ws->ctr[i];
+  return FFTCONV_B200_OK;
+}
+
+int fftconv_b200_reset_counters(fftconv_b200_ws* ws) {
+  if (!ws) return FFTCONV_B200_INVALID_ARGUMENT;
+  ws->ctr[0] = ws->ctr[1] = ws->ctr[2] = 0;
+  return FFTCONV_B200_OK;
+}
+
+int fftconv_b200_forward(fftconv_b200_ws* ws, const float* x, size_t S, size_t f, size_t x_rows,
+                         size_t x_cols, const float* w, size_t w_out, size_t w_in, size_t k,
+                         float* y, void* stream) {
+  if (!ws) return FFTCONV_B200_INVALID_ARGUMENT;
+  return guarded(ws, [&] {
+    DeviceGuard g(ws->device);
+    run_forward(ws, x, S, f, x_rows, x_cols, w, w_out, w_in, k, y, (cudaStream_t)stream);
+  });
+}
+
+int fftconv_b200_grad_input(fftconv_b200_ws* ws, const float* gy, size_t S, size_t fo,
+                            size_t gy_rows, size_t gy_cols, const float* w, size_t w_out,
+                            size_t w_in, size_t k, float* gx, void* stream) {
+  if (!ws) return FFTCONV_B200_INVALID_ARGUMENT;
+  return guarded(ws, [&] {
+    DeviceGuard g(ws->device);
+    run_grad_input(ws, gy, S, fo, gy_rows, gy_cols, w, w_out, w_in, k, gx, (cudaStream_t)stream);
+  });
+}
+
+int fftconv_b200_grad_weight(fftconv_b200_ws* ws, const float* gy, size_t S_gy, size_t fo,
+                             size_t gy_rows, size_t gy_cols, const float* x, size_t S_x,
+                             size_t f, size_t x_rows, size_t x_cols, float* gw, void* stream) {
+  if (!ws) return FFTCONV_B200_INVALID_ARGUMENT;
+  return guarded(ws, [&] {
+    DeviceGuard g(ws->device);
+    run_grad_weight(ws, gy, S_gy, fo, gy_rows, gy_cols, x, S_x, f, x_rows, x_cols, gw,
+                    (cudaStream_t)stream);
+  });
+}
+
+int fftconv_b200_forward_host(fftconv_b200_ws* ws, const float* x, size_t S, size_t f,
+                              size_t x_rows, size_t x_cols, const float* w, size_t w_out,
+                              size_t w_in, size_t k, float* y, unsigned threads) {
+  (void)threads;
+  if (!ws) return FFTCONV_B200_INVALID_ARGUMENT;
+  return guarded(ws, [&] {
+    DeviceGuard g(ws->device);
+    // Shape checks first so errors never touch the device.
+    require_nonzero(S, f, x_rows, x_cols, "Tensor4");
+    require_nonzero(w_out, w_in, k, 1, "Weights4");
+    const size_t nx = S * f * x_rows * x_cols, nw = w_out * w_in * k * k;
+    const size_t no = (k <= x_rows) ? x_rows - k + 1 : 1;
+    const size_t ny = S * w_out * no * no;
+    if (x_rows == x_cols && w_in == f && k <= x_rows) {
+      prepare(ws, fftconv_b200_layer{k, x_rows, f, w_out, S});
+      stage_in(ws, ws->st_in0, ws->n_in0, x, nx);
+      stage_in(ws, ws->st_in1, ws->n_in1, w, nw);
+      grow(ws->st_out, ws->n_out, ny);
+    }
+    run_forward(ws, ws->st_in0, S, f, x_rows, x_cols, ws->st_in1, w_out, w_in, k, ws->st_out,
+                ws->host_stream);
+    FCB_CUDA(cudaMemcpyAsync(y, ws->st_out, ny * sizeof(float), cudaMemcpyDeviceToHost,
+                             ws->host_stream));
+    FCB_CUDA(cudaStreamSynchronize(ws->host_stream));
+  });
+}
+
+int fftconv_b200_grad_input_host(fftconv_b200_ws* ws, const float* gy, size_t S, size_t fo,
+                                 size_t gy_rows, size_t gy_cols, const float* w, size_t w_out,
+                                 size_t w_in, size_t k, float* gx, unsigned threads) {
+  (void)threads;
+  if (!ws) return FFTCONV_B200_INVALID_ARGUMENT;
+  return guarded(ws, [&] {
+    DeviceGuard g(ws->device);
+    require_nonzero(S, fo, gy_rows, gy_cols, "Tensor4");
+    require_nonzero(w_out, w_in, k, 1, "Weights4");
+    const size_t n = gy_rows + k - 1;
+    const size_t ngy = S * fo * gy_rows * gy_cols, nw = w_out * w_in * k * k;
+    const size_t ngx = S * w_in * n * n;
+    if (gy_rows == gy_cols && w_out == fo) {
+      prepare(ws, fftconv_b200_layer{k, n, w_in, fo, S});
+      stage_in(ws, ws->st_in0, ws->n_in0, gy, ngy);
+      stage_in(ws, ws->st_in1, ws->n_in1, w, nw);
+      grow(ws->st_out, ws->n_out, ngx);
+    }
+    run_grad_input(ws, ws->st_in0, S, fo, gy_rows, gy_cols, ws->st_in1, w_out, w_in, k,
+                   ws->st_out, ws->host_stream);
+    FCB_CUDA(cudaMemcpyAsync(gx, ws->st_out, ngx * sizeof(float), cudaMemcpyDeviceToHost,
+                             ws->host_stream));
+    FCB_CUDA(cudaStreamSynchronize(ws->host_stream));
+  });
+}
+
+int fftconv_b200_grad_weight_host(fftconv_b200_ws* ws, const float* gy, size_t S_gy, size_t fo,
+                                  size_t gy_rows, size_t gy_cols, const float* x, size_t S_x,
+                                  size_t f, size_t x_rows, size_t x_cols, float* gw,
+                                  unsigned threads) {
+  (void)threads;
+  if (!ws) return FFTCONV_B200_INVALID_ARGUMENT;
+  return guarded(ws, [&] {
+    DeviceGuard g(ws->device);
+    require_nonzero(S_gy, fo, gy_rows, gy_cols, "Tensor4");
+    require_nonzero(S_x, f, x_rows, x_cols, "Tensor4");
+    const size_t ngy = S_gy * fo * gy_rows * gy_cols, nx = S_x * f * x_rows * x_cols;
+    const size_t k = (gy_rows <= x_rows) ? x_rows - gy_rows + 1 : 1;
+    const size_t ngw = fo * f * k * k;
+    if (gy_rows == gy_cols && x_rows == x_cols && S_gy == S_x && gy_rows <= x_rows) {
+      prepare(ws, fftconv_b200_layer{k, x_rows, f, fo, S_x});
+      stage_in(ws, ws->st_in0, ws->n_in0, gy, ngy);
+      stage_in(ws, ws->st_in1, ws->n_in1, x, nx);
+      grow(ws->st_out, ws->n_out, ngw);
+    }
+    run_grad_weight(ws, ws->st_in0, S_gy, fo, gy_rows, gy_cols, ws->st_in1, S_x, f, x_rows,
+                    x_cols, ws->st_out, ws->host_stream);
+    FCB_CUDA(cudaMemcpyAsync(gw, ws->st_out, ngw * sizeof(float), cudaMemcpyDeviceToHost,
+                             ws->host_stream));
+    FCB_CUDA(cudaStreamSynchronize(ws->host_stream));
+  });
+}
+
+int fftconv_b200_set_stage_timing(fftconv_b200_ws* ws, int enable) {
+  if (!ws) return FFTCONV_B200_INVALID_ARGUMENT;
+  ws->timing = enable != 0;
+  return FFTCONV_B200_OK;
+}
+
+int fftconv_b200_stage_ms(fftconv_b200_ws* ws, float out[4]) {
+  if (!ws || !out) return FFTCONV_B200_INVALID_ARGUMENT;
+  return guarded(ws, [&] {
+    if (!ws->ev_ready) throw Error(FFTCONV_B200_INVALID_ARGUMENT, "stage timing not enabled");
+    DeviceGuard g(ws->device);
+    FCB_CUDA(cudaEventSynchronize(ws->ev[4]));
+    for (int i = 0; i < 4; ++i) FCB_CUDA(cudaEventElapsedTime(&out[i], ws->ev[i], ws->ev[i + 1]));
+  });
+}
+
+int fftconv_b200_last_launch_count(const fftconv_b200_ws* ws) {
+  return ws ? ws->last_launches : -1;
+}
+
+// ---- unit-level test hooks -------------------------------------------
+
+int fftconv_b200_debug_r2c(const float* in, size_t planes, size_t src, size_t m, float* out,
+                           void* stream) {
+  return guarded(nullptr, [&] {
+    if (next_pow2(src) > m || (m & (m - 1)))
+      throw Error(FFTCONV_B200_PLAN_ERROR, "debug_r2c: bad m");
+    // R = planes rows, J = 1: F[t][p][2*16]; copy out[p][t] with a strided 2-D memcpy.
+    const size_t bins = m * (m / 2 + 1), kp = 16;
+    float* F = nullptr;
+    FCB_CUDA(cudaMalloc(&F, bins * planes * kp * 2 * sizeof(float)));
+    R2CParams p{in, F, (long long)(src * src), 0, (int)planes, 1, (int)kp, (int)src,
+                (int)(src | 1)};
+    launch_r2c(m, p, (cudaStream_t)stream);
+    // F[(t*planes + p)*32 + 0..1] -> out[(p*bins + t)*2]
+    for (size_t pl = 0; pl < planes; ++pl)
+      FCB_CUDA(cudaMemcpy2DAsync(out + pl * bins * 2, 2 * sizeof(float), F + pl * kp * 2,
+                                 planes * kp * 2 * sizeof(float), 2 * sizeof(float), bins,
+                                 cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    FCB_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    cudaFree(F);
+  });
+}
+
+int fftconv_b200_debug_c2r(const float* in, size_t planes, size_t m, size_t crop, float* out,
+                           void* stream) {
+  return guarded(nullptr, [&] {
+    if ((m & (m - 1)) || crop > m) throw Error(FFTCONV_B200_PLAN_ERROR, "debug_c2r: bad m");
+    // in[p][t] -> P[t][0][p] (R = 1, J = planes)
+    const size_t bins = m * (m / 2 + 1);
+    float* P = nullptr;
+    FCB_CUDA(cudaMalloc(&P, bins * planes * 2 * sizeof(float)));
+    for (size_t pl = 0; pl < planes; ++pl)
+      FCB_CUDA(cudaMemcpy2DAsync(P + pl * 2, planes * 2 * sizeof(float), in + pl * bins * 2,
+                                 2 * sizeof(float), 2 * sizeof(float), bins,
+                                 cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    C2RParams p{P, out, 0, (long long)(crop * crop), 1, (int)planes, (int)crop, 0, 0,
+                1.0f / (float)(m * m)};
+    launch_c2r(m, p, (cudaStream_t)stream);
+    FCB_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    cudaFree(P);
+  });
+}
+
+int fftconv_b200_debug_cgemm(const float* a, const float* b, float* out, size_t bins, size_t M,
+                             size_t N, size_t K, int mode, void* stream) {
+  return guarded(nullptr, [&] {
+    if (mode < 0 || mode > 2) throw Error(FFTCONV_B200_INVALID_ARGUMENT, "mode");
+    int dev = 0;
+    FCB_CUDA(cudaGetDevice(&dev));
+    const DevInfo di = dev_info(dev);
+    const size_t kp = round_up(K, 16);
+    float *A = nullptr, *B = nullptr;
+    FCB_CUDA(cudaMalloc(&A, bins * M * kp * 2 * sizeof(float)));
+    FCB_CUDA(cudaMalloc(&B, bins * N * kp * 2 * sizeof(float)));
+    cudaStream_t st = (cudaStream_t)stream;
+    FCB_CUDA(cudaMemsetAsync(A, 0, bins * M * kp * 2 * sizeof(float), st));
+    FCB_CUDA(cudaMemsetAsync(B, 0, bins * N * kp * 2 * sizeof(float), st));
+    FCB_CUDA(cudaMemcpy2DAsync(A, kp * 2 * sizeof(float), a, K * 2 * sizeof(float),
+                               K * 2 * sizeof(float), bins * M, cudaMemcpyDeviceToDevice, st));
+    FCB_CUDA(cudaMemcpy2DAsync(B, kp * 2 * sizeof(float), b, K * 2 * sizeof(float),
+                               K * 2 * sizeof(float), bins * N, cudaMemcpyDeviceToDevice, st));
+    launch_gemm(A, B, out, bins, M, N, kp, mode, di, st);
+    FCB_CUDA(cudaStreamSynchronize(st));
+    cudaFree(A);
+    cudaFree(B);
+  });
+}
+
+}  // extern "C"
