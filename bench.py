@@ -1,0 +1,403 @@
+#!/usr/bin/env python
+"""Benchmark of the FFT convolution layer hot path (BASELINE.json metric).
+
+One step = fprop + bprop + accGrad of one conv layer (the reference's three
+ConvWorkspace operators, conv_fft.hpp:74-206) over the layer's full
+minibatch, every transform recomputed from spatial data.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config paper|wide|small|sweep:n,k]
+                  [--impl ours|reference]
+
+N>1 runs one process per GPU under torchrun: the minibatch S is sharded
+(strong scaling: the layer's S stays fixed), fprop/bprop are local and
+accGrad's weight gradient is summed with an NCCL all-reduce.  Rank 0 prints
+one JSON line.  Timing: CUDA events on the launching stream, L2 flushed
+between steps (256 MiB write), max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+CONFIGS = {
+    # BASELINE.json configs (k, n, f, f', S)
+    "small": (5, 32, 16, 16, 8),
+    "paper": (7, 32, 96, 96, 128),
+    "wide": (11, 64, 256, 256, 128),
+}
+METRIC = "ms per fprop+bprop+accGrad per layer (S=128) + direct-conv-equiv TFLOP/s"
+OPS = ("forward", "grad_input", "grad_weight")
+
+
+def parse_config(name):
+    if name.startswith("sweep:"):
+        n, k = (int(v) for v in name.split(":")[1].split(","))
+        return (k, n, 96, 96, 128), f"kernel/input sweep point S=128 f=f'=96 n={n} k={k}"
+    k, n, f, fo, S = CONFIGS[name]
+    label = {"paper": "paper sweep point", "wide": "wide layer", "small": "small layer"}[name]
+    return CONFIGS[name], f"{label} S={S} f={f} f'={fo} n={n} k={k}"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled in the background."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "50", "-f", self.path], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        with open(self.path) as fh:
+            for line in fh:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 8:
+                    rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        loaded = [r for r in rows if r[7] not in ("0", "[N/A]")] or rows
+        sm = [float(r[0]) for r in loaded if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in loaded for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows), "samples_under_load": len(loaded)}
+
+
+# ---------------------------------------------------------------- reference arm
+def cpu_reference_step_ms(cfg, iters, warmup, threads, seed=1234):
+    """Reference run_op_bench<float> (bench.hpp:80-145), FFT method, per op."""
+    import oracle
+
+    k, n, f, fo, S = cfg
+    out = {}
+    for op_i, op in enumerate(OPS):
+        r = oracle.ref_run_op_bench(k, n, f, fo, S, op_i, 1, iters, warmup, threads, seed)
+        out[op] = r["mean_ms"]
+    return out
+
+
+def cpu_threads():
+    import oracle
+
+    return int(oracle.ref_lib().ref_resolve_threads(0))
+
+
+def run_reference_arm(args, cfg, label):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+
+    if not oracle.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libfftconv_ref.so not built"}))
+        return
+    threads = cpu_threads()
+    k, n, f, fo, S = cfg
+    for _ in range(args.warmup):
+        cpu_reference_step_ms(cfg, 1, 0, threads)
+    steps = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        cpu_reference_step_ms(cfg, 1, 0, threads)
+        steps.append((time.perf_counter() - t0) * 1e3)
+    ms = statistics.mean(steps)
+    E = 2 * S * f * fo * (n - k + 1) ** 2 * k * k
+    line = {
+        "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference fill_uniform, seed 1234)",
+        "config": {"workload": label, "k": k, "n": n, "f": f, "f_prime": fo, "S": S,
+                   "parallelism": "reference CPU (std::thread parallel_for)"},
+        "impl": "reference",
+        "tflops_equiv": 3 * E / (ms * 1e-3) / 1e12,
+        "cpu_baseline": {"value": ms, "unit": "ms", "cores": threads, "kind": "reference",
+                         "sample": f"reference ConvWorkspace<float> fprop+bprop+accGrad on the full layer, "
+                                   f"{args.steps} steps after {args.warmup} warm-up"},
+        "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="paper")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg, label = parse_config(args.config)
+    if args.impl == "reference":
+        return run_reference_arm(args, cfg, label)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1312_5851_b200 import ConvWorkspace, LayerConfig
+    from paper_1312_5851_b200.rng import ROLE_GRAD_OUTPUT, ROLE_INPUT, ROLE_WEIGHTS, fill_uniform
+    from paper_1312_5851_b200.sharded import shard_range
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    k, n, f, fo, S = cfg
+    no = n - k + 1
+    b0, b1 = shard_range(S, world, rank)
+    Sl = b1 - b0
+    lcfg = LayerConfig(k, n, f, fo, Sl)
+    # Inputs: the reference generator (same bytes the CPU path consumes), this
+    # rank's minibatch slice, resident in HBM before timing starts.
+    x = fill_uniform((S, f, n, n), 1234, ROLE_INPUT)[b0:b1]
+    w = fill_uniform((fo, f, k, k), 1234, ROLE_WEIGHTS)
+    gy = fill_uniform((S, fo, no, no), 1234, ROLE_GRAD_OUTPUT)[b0:b1]
+    xd, wd, gyd = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (x, w, gy))
+    ws = ConvWorkspace([lcfg], device=local)
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step():
+        y = ws.forward(xd, wd)
+        gx = ws.grad_input(gyd, wd)
+        gw = ws.grad_weight(gyd, xd)
+        if world > 1:
+            dist.all_reduce(gw)
+        return y, gx, gw
+
+    # warm-up (also brings clocks up)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    t_end = time.time() + 1.0
+    while time.time() < t_end:
+        step()
+        flush.fill_(1.0)
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.15)
+    # keep the GPU busy while the sampler spins up, then the timed steps
+    t_end = time.time() + 0.5
+    while time.time() < t_end:
+        step()
+        flush.fill_(1.0)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(args.steps):
+        flush.fill_(float(len(times)))  # evict L2 between timed steps (untimed)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        times.append((e0, e1))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in times]
+    # hold load a little longer so the sampler sees the clocks under load
+    t_end = time.time() + 0.3
+    while time.time() < t_end:
+        step()
+        flush.fill_(1.0)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    ms = statistics.mean(step_ms)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # ---- per-kernel device times (events between the 4 launches of each op)
+    ws.set_stage_timing(True)
+    stage = {op: [] for op in OPS}
+    for _ in range(5):
+        for op, fn in (("forward", lambda: ws.forward(xd, wd)), ("grad_input", lambda: ws.grad_input(gyd, wd)),
+                       ("grad_weight", lambda: ws.grad_weight(gyd, xd))):
+            flush.fill_(2.0)
+            fn()
+            stage[op].append(ws.stage_ms())
+    ws.set_stage_timing(False)
+    stage_ms = {op: [statistics.mean(v[i] for v in stage[op]) for i in range(4)] for op in OPS}
+
+    hbm_gbs, bf16_tflops, peak_src = load_peaks()
+    tf32x3_tflops = bf16_tflops / 2.0 / 3.0
+    lc = lcfg
+    bins = lc.bins()
+    # algorithmic bytes per launch of each transform kernel, flops of the GEMM
+    Sl_, f_, fo_ = Sl, f, fo
+    alg = {
+        "forward": [4 * Sl_ * f_ * n * n + 8 * bins * Sl_ * f_, 4 * fo_ * f_ * k * k + 8 * bins * fo_ * f_,
+                    8 * bins * Sl_ * f_ * fo_, 8 * bins * Sl_ * fo_ + 4 * Sl_ * fo_ * no * no],
+        "grad_input": [4 * Sl_ * fo_ * no * no + 8 * bins * Sl_ * fo_, 4 * fo_ * f_ * k * k + 8 * bins * fo_ * f_,
+                       8 * bins * Sl_ * f_ * fo_, 8 * bins * Sl_ * f_ + 4 * Sl_ * f_ * n * n],
+        "grad_weight": [4 * Sl_ * fo_ * no * no + 8 * bins * Sl_ * fo_, 4 * Sl_ * f_ * n * n + 8 * bins * Sl_ * f_,
+                        8 * bins * Sl_ * f_ * fo_, 8 * bins * f_ * fo_ + 4 * fo_ * f_ * k * k],
+    }
+    kname = ["r2c_planes_kernel(A)", "r2c_planes_kernel(B)", "cgemm_bins_tcgen05", "c2r_planes_kernel"]
+    stages = []
+    for op in OPS:
+        for i in range(4):
+            t_ms = stage_ms[op][i]
+            if i == 2:
+                ach = alg[op][i] / (t_ms * 1e-3) / 1e12
+                stages.append({"op": op, "kernel": kname[i], "ms": t_ms, "bound": "tensor", "achieved": ach,
+                               "peak": tf32x3_tflops, "unit": "TFLOP/s", "frac": ach / tf32x3_tflops,
+                               "alg_flops": alg[op][i]})
+            else:
+                ach = alg[op][i] / (t_ms * 1e-3) / 1e9
+                stages.append({"op": op, "kernel": kname[i], "ms": t_ms, "bound": "hbm", "achieved": ach,
+                               "peak": hbm_gbs, "unit": "GB/s", "frac": ach / hbm_gbs, "alg_bytes": alg[op][i]})
+    # dominant kernel = largest total time across the step
+    tot = {}
+    for s_ in stages:
+        key = s_["kernel"] if s_["kernel"] != "r2c_planes_kernel(B)" else "r2c_planes_kernel(A)"
+        key = "r2c_planes_kernel" if key.startswith("r2c") else key
+        tot[key] = tot.get(key, 0.0) + s_["ms"]
+    dom = max(tot, key=tot.get)
+    dom_st = [s_ for s_ in stages if s_["kernel"].startswith(dom)]
+    dom_ms = statistics.mean(s_["ms"] for s_ in dom_st)
+    if dom == "cgemm_bins_tcgen05":
+        alg_per_launch = statistics.mean(s_["alg_flops"] for s_ in dom_st)
+        achieved = alg_per_launch / (dom_ms * 1e-3) / 1e12
+        roofline = {"bound": "tensor", "achieved": achieved, "peak": tf32x3_tflops, "unit": "TFLOP/s",
+                    "frac": achieved / tf32x3_tflops,
+                    "peak_basis": f"{peak_src} bf16 {bf16_tflops} TF/s / 2 (TF32 rate) / 3 (3xTF32 passes)"}
+    else:
+        alg_per_launch = statistics.mean(s_["alg_bytes"] for s_ in dom_st)
+        achieved = alg_per_launch / (dom_ms * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_gbs, "unit": "GB/s",
+                    "frac": achieved / hbm_gbs, "peak_basis": peak_src}
+    roofline["kernel"] = dom
+    roofline["share_of_step"] = tot[dom] / sum(tot.values())
+    roofline["traffic"] = ncu_traffic(dom, args.config)
+
+    # ---- end to end through the public API with host (pinned) buffers
+    e2e = None
+    if world == 1:
+        xp = torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()
+        wp = torch.from_numpy(np.ascontiguousarray(w)).pin_memory().numpy()
+        gyp = torch.from_numpy(np.ascontiguousarray(gy)).pin_memory().numpy()
+        for _ in range(2):
+            ws.forward(xp, wp), ws.grad_input(gyp, wp), ws.grad_weight(gyp, xp)
+        e2e_ms = []
+        for _ in range(args.e2e_steps):
+            t0 = time.perf_counter()
+            y_h = ws.forward(xp, wp)
+            gx_h = ws.grad_input(gyp, wp)
+            gw_h = ws.grad_weight(gyp, xp)
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        h2d = 4 * (x.size + w.size + gy.size + w.size + gy.size + x.size)
+        d2h = 4 * (y_h.size + gx_h.size + gw_h.size)
+        e2e = {"value": statistics.mean(e2e_ms), "unit": "ms", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h),
+               "path": "ConvWorkspace.forward/grad_input/grad_weight on pinned numpy -> fftconv_b200_*_host C ABI"}
+
+    # ---- CPU reference beside it (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            import oracle
+
+            if oracle.ref_available():
+                threads = cpu_threads()
+                iters = 1 if args.config == "wide" else 2
+                per_op = cpu_reference_step_ms(cfg, iters, 1, threads)
+                cpu = {"value": sum(per_op.values()), "unit": "ms", "cores": threads, "kind": "reference",
+                       "per_op_ms": per_op,
+                       "sample": f"reference run_op_bench<float> (FFT method) on the full layer, {iters} iters "
+                                 f"after 1 warm-up per op"}
+        except Exception as exc:  # reported, never fatal
+            cpu = {"value": None, "unit": "ms", "cores": None, "kind": "reference", "sample": f"failed: {exc}"}
+
+    E = 2 * S * f * fo * no * no * k * k
+    line = {
+        "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (reference fill_uniform, seed 1234)",
+        "config": {"workload": label, "k": k, "n": n, "f": f, "f_prime": fo, "S": S, "S_per_gpu": Sl,
+                   "parallelism": f"dp{world} (minibatch-sharded, NCCL all-reduce of gw)" if world > 1 else "dp1",
+                   "l2": "flushed between timed steps (256 MiB write)"},
+        "tflops_equiv": 3 * E / (ms * 1e-3) / 1e12,
+        "per_op_ms": {op: sum(stage_ms[op]) for op in OPS},
+        "roofline": roofline,
+        "stages": stages,
+        "gpu_launches": 12 * args.steps,
+        "clocks": clocks,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def ncu_traffic(kernel, config):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full
+    summary (profiles/ncu_summary.json), or None when not captured."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return d.get(config, {}).get(kernel, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+if __name__ == "__main__":
+    main()

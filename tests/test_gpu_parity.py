@@ -308,6 +308,16 @@ def test_paper_point_full_vs_fft_oracle(dev):
     _assert_close(got, ref)
 
 
+def _assert_adjoint(x, w, gy, y, gx, gw, tol):
+    """<y,gy> = <x,gx> = <w,gw>, gaps relative to the Cauchy-Schwarz bound
+    (the dot products themselves cancel heavily at these sizes)."""
+    d = lambda a, b: float(np.dot(a.ravel().astype(np.float64), b.ravel().astype(np.float64)))  # noqa: E731
+    nrm = lambda a: float(np.linalg.norm(a.ravel().astype(np.float64)))  # noqa: E731
+    a, b, c = d(y, gy), d(x, gx), d(w, gw)
+    scale = max(nrm(y) * nrm(gy), nrm(x) * nrm(gx), nrm(w) * nrm(gw))
+    assert abs(a - b) / scale < tol and abs(a - c) / scale < tol, (a, b, c, scale)
+
+
 def _sampled_planes_check(dev, cfg, seed, nplanes=6):
     import torch
 
@@ -329,11 +339,7 @@ def _sampled_planes_check(dev, cfg, seed, nplanes=6):
     for got, ref in ((gy_, ry), (ggx, rgx), (ggw, rgw)):
         assert oracle.rel_l2_error(got, ref) <= L2_TOL
     # adjoint triple over the full tensors (size-independent property)
-    a = float(np.dot(y.ravel().astype(np.float64), gy.ravel()))
-    b = float(np.dot(x.ravel().astype(np.float64), gx.ravel()))
-    c = float(np.dot(w.ravel().astype(np.float64), gw.ravel()))
-    scale = max(abs(a), abs(b), abs(c))
-    assert abs(a - b) / scale < 1e-5 and abs(a - c) / scale < 1e-5
+    _assert_adjoint(x, w, gy, y, gx, gw, 1e-6)
     del torch
 
 
