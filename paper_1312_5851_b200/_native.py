@@ -11,7 +11,8 @@ import os
 from functools import lru_cache
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libfftconv_b200.so")
+# FFTCONV_B200_LIB: alternative in-tree build for A/B kernel experiments.
+LIB_PATH = os.environ.get("FFTCONV_B200_LIB") or os.path.join(HERE, "lib", "libfftconv_b200.so")
 
 _sz = C.c_size_t
 _p = C.c_void_p

@@ -25,12 +25,12 @@
 // Pipeline (one CTA per SM, persistent over tiles (t, m-tile, n-tile)):
 //   warp 0      TMA producer: raw fp32 A (128 x 32) and B (Nc x 32) tiles
 //               per K chunk of 16 complex, 128-B swizzle, OOB zero fill.
-//   warps 4-7   converters: split hi/lo in place, expand B re/im rows,
+//   warps 4-11  converters: split hi/lo in place, expand B re/im rows,
 //               fence.proxy.async, arrive.
 //   warp 1      MMA issuer (one thread): 4 K-steps x 3 UMMA (M=128,
 //               N=2Nc, K=8) per chunk into a double-buffered TMEM
 //               accumulator; tcgen05.commit frees smem / signals epilogue.
-//   warps 8-11  epilogue: tcgen05.ld -> (re, im) float2 stores into the
+//   warps 12-15 epilogue: tcgen05.ld -> (re, im) float2 stores into the
 //               bin-major product spectrum P[t][n][2*M_valid] (lanes =
 //               consecutive M rows -> coalesced 256-B stores).
 //   warp 2      TMEM allocator.
@@ -55,9 +55,12 @@ struct GemmParams {
   int nc;         // complex columns per N tile (multiple of 8, <= 128)
   int stages;
   int mode;
+  int dbg;  // experiment bits (0 in production): 1 skip conversion, 2 hi.hi only,
+            // 4 raw A as hi (relies on tf32 truncation), lo = x - trunc(x)
 };
 
-constexpr int kGemmThreads = 384;
+constexpr int kGemmThreads = 512;
+constexpr int kConvThreads = 256;  // warps 4..11
 constexpr int kTileM = 128;
 constexpr int kChunkBytesA = kTileM * 128;  // 128 rows x 128 B (32 fp32)
 
@@ -92,7 +95,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&conv[s], 128);
+      mbar_init(&conv[s], kConvThreads);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -162,8 +165,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const uint64_t dbh = umma_desc_sw128(b_hi + off);
             const uint64_t dbl = umma_desc_sw128(b_lo + off);
             umma_tf32(d_tmem, dah, dbh, idesc, (kc | kk) ? 1u : 0u);
-            umma_tf32(d_tmem, dah, dbl, idesc, 1u);
-            umma_tf32(d_tmem, dal, dbh, idesc, 1u);
+            if (!(p.dbg & 2)) {
+              umma_tf32(d_tmem, dah, dbl, idesc, 1u);
+              umma_tf32(d_tmem, dal, dbh, idesc, 1u);
+            }
           }
           umma_commit(&empty[s]);
           if (kc == kc_n - 1) umma_commit(&tfull[a]);
@@ -172,9 +177,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (++s == S) { s = 0; ph ^= 1; }
       }
     }
-  } else if (warp >= 4 && warp < 8) {
+  } else if (warp >= 4 && warp < 12) {
     // ------------------------------------------------ converters
-    const int ct = threadIdx.x - 128;  // 0..127
+    const int ct = threadIdx.x - 128;  // 0..255
     float s1 = 1.f, s2 = 1.f, s3 = 1.f;  // re=(p, s1 q)  im=(s2 q, s3 p)
     // fprop: re (p,q) im (-q,p); bprop: re (p,-q) im (q,p); accGrad: re (p,q) im (q,-p)
     bool swap_im = true;
@@ -187,26 +192,46 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
       for (int kc = 0; kc < kc_n; ++kc) {
         mbar_wait(&full[s], ph);
+        if (p.dbg & 1) {
+          fence_proxy_async_smem();
+          mbar_arrive(&conv[s]);
+          if (++s == S) { s = 0; ph ^= 1; }
+          continue;
+        }
         uint8_t* st = smem + s * stageBytes;
         float4* ahi = reinterpret_cast<float4*>(st);
         float4* alo = reinterpret_cast<float4*>(st + kChunkBytesA);
+        if (p.dbg & 4) {
 #pragma unroll 4
-        for (int i = ct; i < kChunkBytesA / 16; i += 128) {
-          const float4 v = ahi[i];
-          float4 h, l;
-          h.x = tf32_round(v.x); l.x = v.x - h.x;
-          h.y = tf32_round(v.y); l.y = v.y - h.y;
-          h.z = tf32_round(v.z); l.z = v.z - h.z;
-          h.w = tf32_round(v.w); l.w = v.w - h.w;
-          ahi[i] = h;
-          alo[i] = l;
+          for (int i = ct; i < kChunkBytesA / 16; i += kConvThreads) {
+            const float4 v = ahi[i];
+            float4 l;
+            l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+            l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+            l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+            l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+            alo[i] = l;
+          }
+        } else {
+#pragma unroll 4
+          for (int i = ct; i < kChunkBytesA / 16; i += kConvThreads) {
+            const float4 v = ahi[i];
+            float4 h, l;
+            h.x = tf32_round(v.x); l.x = v.x - h.x;
+            h.y = tf32_round(v.y); l.y = v.y - h.y;
+            h.z = tf32_round(v.z); l.z = v.z - h.z;
+            h.w = tf32_round(v.w); l.w = v.w - h.w;
+            ahi[i] = h;
+            alo[i] = l;
+          }
         }
         float4* bre_hi = reinterpret_cast<float4*>(st + 2 * kChunkBytesA);
         float4* bim_hi = reinterpret_cast<float4*>(st + 2 * kChunkBytesA + nc * 128);
         float4* bre_lo = reinterpret_cast<float4*>(st + 2 * kChunkBytesA + bBytes);
         float4* bim_lo = reinterpret_cast<float4*>(st + 2 * kChunkBytesA + bBytes + nc * 128);
         const int nb = nc * 8;  // float4 per raw B tile
-        for (int i = ct; i < nb; i += 128) {
+#pragma unroll 2
+        for (int i = ct; i < nb; i += kConvThreads) {
           const float4 v = bre_hi[i];  // (p0, q0, p1, q1)
           const float4 re = make_float4(v.x, s1 * v.y, v.z, s1 * v.w);
           const float4 im = make_float4(s2 * v.y, s3 * v.x, s2 * v.w, s3 * v.z);
@@ -229,7 +254,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (++s == S) { s = 0; ph ^= 1; }
       }
     }
-  } else if (warp >= 8) {
+  } else if (warp >= 12) {
     // ------------------------------------------------ epilogue
     const int q = warp & 3;  // TMEM lane quadrant accessible to this warp
     const int row = q * 32 + lane;

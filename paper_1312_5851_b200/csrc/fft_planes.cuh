@@ -32,7 +32,7 @@
 
 namespace fcb {
 
-constexpr int kPlaneGroup = 16;  // planes (K indices) per CTA: 16 complex = 128 B
+constexpr int kKChunk = 16;  // K padding granule: 16 complex = one 128-B line
 
 __host__ __device__ constexpr int ilog2c(int n) { return n <= 1 ? 0 : 1 + ilog2c(n >> 1); }
 __host__ __device__ constexpr int bitrev_c(int i, int bits) {
@@ -178,6 +178,34 @@ __device__ __forceinline__ void irfft_reg(float2 (&X)[N / 2 + 1], float (&x)[N])
   }
 }
 
+// Threads per CTA: one pass-2 row item per thread (16 planes x (m/2+1)
+// u-rows [x2 split halves for m = 64]) so no pass runs a lightly-filled
+// second round.
+#ifndef FCB_G_SMALL
+#define FCB_G_SMALL 16
+#endif
+template <int M>
+struct PlaneTraits {
+  static constexpr int PC = M / 2 + 1;
+  // Planes (K indices / spectrum columns) per CTA: 16 x 8 B = one 128-B
+  // line per bin and operand row (8 -> 64-B half lines, twice the CTAs).
+  static constexpr int G = (M == 64) ? 16 : FCB_G_SMALL;
+  // r2c: u rows per CTA chunk; c2r / r2c row split for m = 64.
+  static constexpr int UC = (M == 64) ? 11 : PC;
+  static constexpr int SPLIT = (M == 64) ? 2 : 1;
+  // Two real columns per complex FFT (m <= 32: registers allow it).
+  static constexpr bool PAIR = (M >= 4 && M <= 32);
+  // One pass-2 row item per thread: G planes x UC u-rows [x2 halves].
+  static constexpr int THREADS = ((G * SPLIT * UC + 31) / 32) * 32 < 64 ? 64 : ((G * SPLIT * UC + 31) / 32) * 32;
+#ifndef FCB_MINB32
+#define FCB_MINB32 2
+#endif
+#ifndef FCB_MINB64
+#define FCB_MINB64 2
+#endif
+  static constexpr int MIN_CTAS = (M == 64) ? FCB_MINB64 : (M == 32) ? (G == 8 ? 4 : FCB_MINB32) : 4;
+};
+
 // ---------------------------------------------------------------- K1: r2c
 struct R2CParams {
   const float* in;  // real planes, plane (r, j) at in + r*in_sr + j*in_sj
@@ -188,35 +216,75 @@ struct R2CParams {
   int kpad;  // padded K (multiple of 16)
   int src;   // source plane edge (square, src <= M): zero-padded implicitly
   int cpad;  // odd smem column stride >= src
+  int conj;  // 1: store the conjugate spectrum
 };
 
-// grid = (kpad/16, R, ceil((M/2+1)/UC)), block = 256.
-// smem = 16 * UC * cpad * sizeof(float2).
-template <int M, int UC, int SPLIT>
-__global__ void __launch_bounds__(256) r2c_planes_kernel(const R2CParams p) {
-  constexpr int PC = M / 2 + 1;
-  constexpr int G = kPlaneGroup;
+// grid = (kpad/G, R, ceil((M/2+1)/UC)), block = PlaneTraits<M>::THREADS.
+// smem = G * UC * cpad * sizeof(float2).
+template <int M>
+__global__ void __launch_bounds__(PlaneTraits<M>::THREADS, PlaneTraits<M>::MIN_CTAS) r2c_planes_kernel(const R2CParams p) {
+  using Tr = PlaneTraits<M>;
+  constexpr int PC = Tr::PC, UC = Tr::UC, SPLIT = Tr::SPLIT;
+  constexpr int G = Tr::G;
   extern __shared__ float2 s1[];  // [G][UC][cpad]
   const int r = blockIdx.y;
   const int j0 = blockIdx.x * G;
   const int u0 = blockIdx.z * UC;
   const int src = p.src, cpad = p.cpad;
   const int jvalid = min(G, p.J - j0);
+  const float* inbase = p.in + (long long)r * p.in_sr + (long long)j0 * p.in_sj;
 
-  // Pass 1: one thread per (plane, column): zero-padded real column FFT
-  // over the rows (coalesced row loads across lanes), keep u in the chunk.
-  const int items1 = jvalid * src;
-  for (int item = threadIdx.x; item < items1; item += blockDim.x) {
-    const int jl = item / src, c = item - jl * src;
-    const float* col = p.in + (long long)r * p.in_sr + (long long)(j0 + jl) * p.in_sj + c;
-    float x[M];
+  // Pass 1: zero-padded real column FFTs over the plane rows; lanes walk
+  // consecutive columns so every row load is coalesced.
+  if constexpr (Tr::PAIR) {
+    // two adjacent real columns (a, b) packed as a + i b in one complex FFT
+    const int npair = (src + 1) >> 1;
+    const int items1 = jvalid * npair;
+    for (int item = threadIdx.x; item < items1; item += blockDim.x) {
+      const int jl = item / npair, cp = item - jl * npair;
+      const int c = 2 * cp;
+      const float* col = inbase + (long long)jl * p.in_sj + c;
+      const bool has_b = c + 1 < src;
+      float2 z[M];
 #pragma unroll
-    for (int i = 0; i < M; ++i) x[i] = (i < src) ? __ldg(col + (long long)i * src) : 0.f;
-    float2* dst = s1 + (jl * UC) * cpad + c;
-    rfft_emit<M>(x, [&](int u, float2 v) {
-      const int ul = u - u0;
-      if (ul >= 0 && ul < UC) dst[ul * cpad] = v;
-    });
+      for (int i = 0; i < M; ++i) {
+        if (i < src) {
+          z[i].x = __ldg(col + (long long)i * src);
+          z[i].y = has_b ? __ldg(col + (long long)i * src + 1) : 0.f;
+        } else {
+          z[i] = make_float2(0.f, 0.f);
+        }
+      }
+      fft_reg<M, false>(z);
+      float2* dst = s1 + (jl * UC) * cpad + c;
+      static_for<0, PC>([&](auto U) {
+        constexpr int u = decltype(U)::value;
+        const float2 zu = z[u];
+        const float2 zc = cconj(z[(M - u) % M]);
+        const float2 a = make_float2(0.5f * (zu.x + zc.x), 0.5f * (zu.y + zc.y));
+        const float2 d = csub(zu, zc);
+        const float2 b = make_float2(0.5f * d.y, -0.5f * d.x);  // (zu - zc) / (2i)
+        const int ul = u - u0;
+        if (ul >= 0 && ul < UC) {
+          dst[ul * cpad] = a;
+          if (has_b) dst[ul * cpad + 1] = b;
+        }
+      });
+    }
+  } else {
+    const int items1 = jvalid * src;
+    for (int item = threadIdx.x; item < items1; item += blockDim.x) {
+      const int jl = item / src, c = item - jl * src;
+      const float* col = inbase + (long long)jl * p.in_sj + c;
+      float x[M];
+#pragma unroll
+      for (int i = 0; i < M; ++i) x[i] = (i < src) ? __ldg(col + (long long)i * src) : 0.f;
+      float2* dst = s1 + (jl * UC) * cpad + c;
+      rfft_emit<M>(x, [&](int u, float2 v) {
+        const int ul = u - u0;
+        if (ul >= 0 && ul < UC) dst[ul * cpad] = v;
+      });
+    }
   }
   __syncthreads();
 
@@ -224,23 +292,23 @@ __global__ void __launch_bounds__(256) r2c_planes_kernel(const R2CParams p) {
   // columns, written bin-major with 16 planes (128 B) per bin per row.
   const int urows = min(UC, PC - u0);
   const int items2 = G * SPLIT * urows;
-  const long long rstride = (long long)p.R * p.kpad * 2;  // floats per bin
-  float* outbase = p.out + ((long long)r * p.kpad + j0) * 2;
+  const long long bstride = (long long)p.R * p.kpad;  // float2 per bin
+  float2* outbase = reinterpret_cast<float2*>(p.out) + (long long)r * p.kpad + j0;
+  const float csign = p.conj ? -1.f : 1.f;
   for (int item = threadIdx.x; item < items2; item += blockDim.x) {
     const int jl = item % G;
     const int rest = item / G;
     const int h = rest % SPLIT;
     const int ul = rest / SPLIT;
     const int u = u0 + ul;
-    float2* o = reinterpret_cast<float2*>(outbase + 2 * jl);
-    if (jl >= jvalid) {
+    float2* o = outbase + jl + (long long)(u * M + h) * bstride;
+    constexpr int NS = M / SPLIT;
+    if (jl >= jvalid) {  // K padding: exact zeros
 #pragma unroll 4
-      for (int i = 0; i < M / SPLIT; ++i)
-        o[(long long)(u * M + i * SPLIT + h) * (rstride / 2)] = make_float2(0.f, 0.f);
+      for (int i = 0; i < NS; ++i) o[(long long)(i * SPLIT) * bstride] = make_float2(0.f, 0.f);
       continue;
     }
     const float2* row = s1 + (jl * UC + ul) * cpad;
-    constexpr int NS = M / SPLIT;
     float2 z[NS];
     if constexpr (SPLIT == 1) {
 #pragma unroll
@@ -248,17 +316,22 @@ __global__ void __launch_bounds__(256) r2c_planes_kernel(const R2CParams p) {
     } else {
       static_assert(SPLIT == 2, "split");
       // decimation in frequency: outputs v = 2i + h
-#pragma unroll
-      for (int c = 0; c < NS; ++c) {
+      static_for<0, NS>([&](auto Cc) {
+        constexpr int c = decltype(Cc)::value;
         const float2 a = (c < src) ? row[c] : make_float2(0.f, 0.f);
         const float2 b = (c + NS < src) ? row[c + NS] : make_float2(0.f, 0.f);
-        if (h == 0) z[c] = cadd(a, b);
-        else z[c] = (c == 0) ? csub(a, b) : cmul(csub(a, b), tw128<false>(c * (128 / M)));
-      }
+        if (h == 0) {
+          z[c] = cadd(a, b);
+        } else {
+          if constexpr (c == 0) z[c] = csub(a, b);
+          else z[c] = cmul(csub(a, b), tw128<false>(c * (128 / M)));
+        }
+      });
     }
     fft_reg<NS, false>(z);
 #pragma unroll
-    for (int i = 0; i < NS; ++i) o[(long long)(u * M + i * SPLIT + h) * (rstride / 2)] = z[i];
+    for (int i = 0; i < NS; ++i)
+      o[(long long)(i * SPLIT) * bstride] = make_float2(z[i].x, csign * z[i].y);
   }
 }
 
@@ -271,15 +344,16 @@ struct C2RParams {
   int crop;     // output edge (top-left crop)
   int cc;       // output columns per CTA chunk
   int ccpad;    // odd smem stride >= cc
-  float scale;  // 1 / m^2
+  float scale;  // 1 / m^2 (negated to fold a sign flip of the product)
 };
 
-// grid = (ceil(J/16), R, ceil(crop/cc)), block = 256.
-// smem = 16 * (M/2+1) * ccpad * sizeof(float2).
-template <int M, int SPLIT>
-__global__ void __launch_bounds__(256) c2r_planes_kernel(const C2RParams p) {
-  constexpr int PC = M / 2 + 1;
-  constexpr int G = kPlaneGroup;
+// grid = (ceil(J/G), R, ceil(crop/cc)), block = PlaneTraits<M>::THREADS.
+// smem = G * (M/2+1) * ccpad * sizeof(float2).
+template <int M>
+__global__ void __launch_bounds__(PlaneTraits<M>::THREADS, PlaneTraits<M>::MIN_CTAS) c2r_planes_kernel(const C2RParams p) {
+  using Tr = PlaneTraits<M>;
+  constexpr int PC = Tr::PC, SPLIT = Tr::SPLIT;
+  constexpr int G = Tr::G;
   constexpr int NS = M / SPLIT;
   extern __shared__ float2 s1[];  // [G][PC][ccpad]
   const int r = blockIdx.y;
@@ -306,13 +380,17 @@ __global__ void __launch_bounds__(256) c2r_planes_kernel(const C2RParams p) {
 #pragma unroll
       for (int v = 0; v < M; ++v) z[v] = __ldg(src + (long long)v * bstride);
     } else {
-#pragma unroll
-      for (int v = 0; v < NS; ++v) {
+      static_for<0, NS>([&](auto Vv) {
+        constexpr int v = decltype(Vv)::value;
         const float2 a = __ldg(src + (long long)v * bstride);
         const float2 b = __ldg(src + (long long)(v + NS) * bstride);
-        if (h == 0) z[v] = cadd(a, b);
-        else z[v] = (v == 0) ? csub(a, b) : cmul(csub(a, b), tw128<true>(v * (128 / M)));
-      }
+        if (h == 0) {
+          z[v] = cadd(a, b);
+        } else {
+          if constexpr (v == 0) z[v] = csub(a, b);
+          else z[v] = cmul(csub(a, b), tw128<true>(v * (128 / M)));
+        }
+      });
     }
     fft_reg<NS, true>(z);
     float2* dst = s1 + (jl * PC + u) * ccpad;
@@ -324,21 +402,55 @@ __global__ void __launch_bounds__(256) c2r_planes_kernel(const C2RParams p) {
   }
   __syncthreads();
 
-  // Pass 2: per (plane, column) Hermitian c2r over u, write the cropped
-  // rows; lanes = consecutive columns -> contiguous row segments.
-  const int items2 = jvalid * ncols;
-  for (int item = threadIdx.x; item < items2; item += blockDim.x) {
-    const int jl = item / ncols, cl = item - jl * ncols;
-    const float2* colp = s1 + (jl * PC) * ccpad + cl;
-    float2 X[PC];
+  // Pass 2: Hermitian c2r over u per cropped column, write the cropped rows;
+  // lanes = consecutive columns -> contiguous row segments.
+  const float scale = p.scale;
+  if constexpr (Tr::PAIR) {
+    // two columns (a, b) at once: Z = Xa + i Xb over the full u range
+    const int npair = (ncols + 1) >> 1;
+    const int items2 = jvalid * npair;
+    for (int item = threadIdx.x; item < items2; item += blockDim.x) {
+      const int jl = item / npair, cp = item - jl * npair;
+      const int cl = 2 * cp;
+      const bool has_b = cl + 1 < ncols;
+      const float2* colp = s1 + (jl * PC) * ccpad + cl;
+      float2 z[M];
+      static_for<0, PC>([&](auto U) {
+        constexpr int u = decltype(U)::value;
+        float2 a = colp[u * ccpad];
+        float2 b = has_b ? colp[u * ccpad + 1] : make_float2(0.f, 0.f);
+        if constexpr (u == 0 || 2 * u == M) {  // c2r ignores these imaginary parts
+          a.y = 0.f;
+          b.y = 0.f;
+        }
+        z[u] = make_float2(a.x - b.y, a.y + b.x);  // a + i b
+        if constexpr (u != 0 && 2 * u != M) z[M - u] = make_float2(a.x + b.y, b.x - a.y);  // conj(a) + i conj(b)
+      });
+      fft_reg<M, true>(z);
+      float* dst = p.out + (long long)r * p.out_sr + (long long)(j0 + jl) * p.out_sj + c0 + cl;
 #pragma unroll
-    for (int u = 0; u < PC; ++u) X[u] = colp[u * ccpad];
-    float x[M];
-    irfft_reg<M>(X, x);
-    float* dst = p.out + (long long)r * p.out_sr + (long long)(j0 + jl) * p.out_sj + c0 + cl;
+      for (int i = 0; i < M; ++i) {
+        if (i < p.crop) {
+          dst[(long long)i * p.crop] = z[i].x * scale;
+          if (has_b) dst[(long long)i * p.crop + 1] = z[i].y * scale;
+        }
+      }
+    }
+  } else {
+    const int items2 = jvalid * ncols;
+    for (int item = threadIdx.x; item < items2; item += blockDim.x) {
+      const int jl = item / ncols, cl = item - jl * ncols;
+      const float2* colp = s1 + (jl * PC) * ccpad + cl;
+      float2 X[PC];
 #pragma unroll
-    for (int i = 0; i < M; ++i)
-      if (i < p.crop) dst[(long long)i * p.crop] = x[i] * p.scale;
+      for (int u = 0; u < PC; ++u) X[u] = colp[u * ccpad];
+      float x[M];
+      irfft_reg<M>(X, x);
+      float* dst = p.out + (long long)r * p.out_sr + (long long)(j0 + jl) * p.out_sj + c0 + cl;
+#pragma unroll
+      for (int i = 0; i < M; ++i)
+        if (i < p.crop) dst[(long long)i * p.crop] = x[i] * scale;
+    }
   }
 }
 

@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <stdexcept>
@@ -123,21 +124,14 @@ static DevInfo dev_info(int device) {
 }
 
 template <int M>
-struct R2CTraits {
-  static constexpr int PC = M / 2 + 1;
-  static constexpr int UC = (M == 64) ? 11 : PC;
-  static constexpr int SPLIT = (M == 64) ? 2 : 1;
-};
-
-template <int M>
 static void launch_r2c_m(const R2CParams& p, cudaStream_t st) {
-  using Tr = R2CTraits<M>;
-  auto kern = r2c_planes_kernel<M, Tr::UC, Tr::SPLIT>;
-  const size_t smem = (size_t)kPlaneGroup * Tr::UC * p.cpad * sizeof(float2);
+  using Tr = PlaneTraits<M>;
+  auto kern = r2c_planes_kernel<M>;
+  const size_t smem = (size_t)Tr::G * Tr::UC * p.cpad * sizeof(float2);
   if (smem > 48 * 1024)
     FCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 grid(p.kpad / kPlaneGroup, p.R, (Tr::PC + Tr::UC - 1) / Tr::UC);
-  kern<<<grid, 256, smem, st>>>(p);
+  dim3 grid(p.kpad / Tr::G, p.R, (Tr::PC + Tr::UC - 1) / Tr::UC);
+  kern<<<grid, Tr::THREADS, smem, st>>>(p);
   FCB_CUDA(cudaGetLastError());
 }
 
@@ -158,18 +152,17 @@ static void launch_r2c(size_t m, const R2CParams& p, cudaStream_t st) {
 
 template <int M>
 static void launch_c2r_m(C2RParams p, cudaStream_t st) {
-  constexpr int PC = M / 2 + 1;
-  constexpr int SPLIT = (M == 64) ? 2 : 1;
+  using Tr = PlaneTraits<M>;
   constexpr int CCMAX = (M == 64) ? 22 : 32;
   const int nchunks = (p.crop + CCMAX - 1) / CCMAX;
   p.cc = (p.crop + nchunks - 1) / nchunks;
   p.ccpad = (p.cc % 2) ? p.cc : p.cc + 1;
-  auto kern = c2r_planes_kernel<M, SPLIT>;
-  const size_t smem = (size_t)kPlaneGroup * PC * p.ccpad * sizeof(float2);
+  auto kern = c2r_planes_kernel<M>;
+  const size_t smem = (size_t)Tr::G * Tr::PC * p.ccpad * sizeof(float2);
   if (smem > 48 * 1024)
     FCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 grid((p.J + kPlaneGroup - 1) / kPlaneGroup, p.R, nchunks);
-  kern<<<grid, 256, smem, st>>>(p);
+  dim3 grid((p.J + Tr::G - 1) / Tr::G, p.R, nchunks);
+  kern<<<grid, Tr::THREADS, smem, st>>>(p);
   FCB_CUDA(cudaGetLastError());
 }
 
@@ -222,6 +215,11 @@ static void launch_gemm(const float* A, const float* B, float* out, size_t bins,
   p.nc = g.nc;
   p.stages = g.stages;
   p.mode = mode;
+  static const int dbg = [] {
+    const char* e = std::getenv("FFTCONV_B200_GEMM_DEBUG");  // experiments only
+    return e ? std::atoi(e) : 0;
+  }();
+  p.dbg = dbg;
   FCB_CUDA(cudaFuncSetAttribute(cgemm_bins_tcgen05, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)g.smem));
   const long long tiles = (long long)bins * g.m_tiles * g.n_tiles;
