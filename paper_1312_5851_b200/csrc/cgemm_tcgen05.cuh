@@ -4,36 +4,39 @@
 // :171-189 accGrad).
 //
 // Per bin t:  D_t (M x Nc complex) = A_t (M x K complex) . op(B_t)^T
-//   fprop   : A = X[b][f],   B = W[o][f],  D = Y[b][o]   = sum_f X conj(W)
-//   bprop   : A = GY[b][o],  B = W[f][o],  D = GX[b][f]  = sum_o GY W
-//   accGrad : A = GY[o][b],  B = X[f][b],  D = GW[o][f]  = sum_b conj(GY) X
+//   fprop   : A = X[b][f],   B = W[o][f],        D = Y[b][o]  = sum_f X conj(W)
+//   bprop   : A = GY[b][o],  B = conj(W)[f][o],  D = GX[b][f] = sum_o GY W
+//             (K1 stores the conjugate spectrum for this operand)
+//   accGrad : A = GY[o][b],  B = X[f][b],        D = GW[o][f] = sum_b conj(GY) X
+//             (computed as -conj of the fprop form: the epilogue negates Im)
+// so all three share one product: D = A . conj(B)^T.
 //
-// Complex arithmetic is embedded in one real GEMM: operand rows hold
-// interleaved (re, im) pairs along K, so A is M x 2K real.  The B tile is
-// expanded in shared memory into 2*Nc real rows -- Nc "re rows" then Nc
-// "im rows" -- whose pair pattern encodes conjugation and the i factor:
-//   fprop  : re (p, q)   im (-q, p)
-//   bprop  : re (p, -q)  im (q, p)
-//   accGrad: re (p, q)   im (q, -p)
-// so D[:, 0:Nc] = Re, D[:, Nc:2Nc] = Im after a single MMA per K step.
+// Complex arithmetic is embedded in one real GEMM.  Operand rows hold
+// interleaved (re, im) pairs along K, so A is M x 2K real.  In shared memory
+// the B tile becomes 2*Nc real rows: the Nc raw rows (p, q) give Re(D), and
+// Nc derived rows (-q, p) give Im(D).  One MMA per K step (N = 2*Nc) thus
+// writes [Re | Im] into TMEM.
 //
-// 3xTF32: every operand x is split as hi = tf32(x), lo = x - hi in smem
-// (exact in fp32) and D += Ahi.Bhi + Ahi.Blo + Alo.Bhi, accumulated in
-// fp32 TMEM.  This keeps fp32-level accuracy (plain TF32 misses the 1e-4
-// bar, SURVEY.md section 7 hard part 4).
+// 3xTF32: x = hi + lo with hi = x truncated to tf32 (the tensor core's own
+// fp32 -> tf32 conversion, so raw fp32 is the hi operand) and lo = x - hi
+// (exact).  D += Ahi.Bhi + Ahi.Blo + Alo.Bhi in fp32 TMEM keeps fp32-level
+// accuracy (plain TF32 misses the 1e-4 bar, SURVEY.md section 7 part 4).
+//
+// The A operand (128 rows) lives in TMEM: the A converters read the TMA'd
+// raw chunk row-per-thread and tcgen05.st both hi and lo into a TMEM
+// staging buffer, so the MMAs read A from TMEM (".kind::tf32 [d], [a], b")
+// and only B needs hi/lo copies in shared memory.
 //
 // Pipeline (one CTA per SM, persistent over tiles (t, m-tile, n-tile)):
-//   warp 0      TMA producer: raw fp32 A (128 x 32) and B (Nc x 32) tiles
-//               per K chunk of 16 complex, 128-B swizzle, OOB zero fill.
-//   warps 4-11  converters: split hi/lo in place, expand B re/im rows,
-//               fence.proxy.async, arrive.
+//   warp 0      TMA: raw fp32 A (128 x 32) and B (Nc x 32) per K chunk of
+//               16 complex; 128-B swizzle; OOB rows/cols zero-filled
+//   warps 4-7   A converters (thread = row): smem -> regs -> TMEM hi/lo
+//   warps 8-11  B converters: im rows + lo rows in smem, fence.proxy.async
 //   warp 1      MMA issuer (one thread): 4 K-steps x 3 UMMA (M=128,
-//               N=2Nc, K=8) per chunk into a double-buffered TMEM
-//               accumulator; tcgen05.commit frees smem / signals epilogue.
-//   warps 12-15 epilogue: tcgen05.ld -> (re, im) float2 stores into the
-//               bin-major product spectrum P[t][n][2*M_valid] (lanes =
-//               consecutive M rows -> coalesced 256-B stores).
-//   warp 2      TMEM allocator.
+//               N=2Nc, K=8) per chunk, double-buffered TMEM accumulator
+//   warps 12-15 epilogue: tcgen05.ld -> float2 (re, im) stores into the
+//               product spectrum P[t][n][m] (lanes = consecutive m rows)
+//   warp 2      TMEM allocator
 #pragma once
 #include <cuda.h>
 
@@ -43,8 +46,6 @@
 
 namespace fcb {
 
-enum GemmMode : int { kModeFprop = 0, kModeBprop = 1, kModeAccGrad = 2 };
-
 struct GemmParams {
   float* out;     // P[t][n][2*m_valid]
   int bins;
@@ -52,53 +53,54 @@ struct GemmParams {
   int n_valid;    // complex output columns (N)
   int k_chunks;   // kpad / 16
   int m_tiles, n_tiles;
-  int nc;         // complex columns per N tile (multiple of 8, <= 128)
+  int nc;         // complex columns per N tile (multiple of 16, <= 96)
   int stages;
-  int mode;
-  int dbg;  // experiment bits (0 in production): 1 skip conversion, 2 hi.hi only,
-            // 4 raw A as hi (relies on tf32 truncation), lo = x - trunc(x)
+  float im_sign;  // +1 (fprop, bprop) or -1 (accGrad)
 };
 
 constexpr int kGemmThreads = 512;
-constexpr int kConvThreads = 256;  // warps 4..11
 constexpr int kTileM = 128;
 constexpr int kChunkBytesA = kTileM * 128;  // 128 rows x 128 B (32 fp32)
+constexpr int kMaxNc = 96;                  // TMEM: 2 x 2*96 accumulator + 2 x 64 A columns
 
 __host__ __device__ inline int gemm_stage_bytes(int nc) {
-  return 2 * kChunkBytesA + 2 * (2 * nc * 128);
+  return kChunkBytesA + 4 * nc * 128;  // raw A | B hi (re, im rows) | B lo (re, im rows)
 }
 
 __global__ void __launch_bounds__(kGemmThreads, 1)
     cgemm_bins_tcgen05(const __grid_constant__ CUtensorMap tmA,
                        const __grid_constant__ CUtensorMap tmB, const GemmParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // 1024-B alignment for the swizzle atoms.
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   const int nc = p.nc;
   const int S = p.stages;
-  const int bBytes = 2 * nc * 128;  // expanded B (re rows + im rows)
+  const int rowsB = nc * 128;  // bytes of nc rows
   const int stageBytes = gemm_stage_bytes(nc);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * stageBytes);
-  uint64_t* full = bars;            // TMA -> converters
-  uint64_t* conv = bars + S;        // converters -> MMA
-  uint64_t* empty = bars + 2 * S;   // MMA -> TMA
-  uint64_t* tfull = bars + 3 * S;   // MMA -> epilogue [2]
-  uint64_t* tempty = bars + 3 * S + 2;  // epilogue -> MMA [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
+  uint64_t* full = bars;              // TMA -> converters           [S]
+  uint64_t* aready = bars + S;        // A converters -> MMA         [S]
+  uint64_t* bready = bars + 2 * S;    // B converters -> MMA         [S]
+  uint64_t* empty = bars + 3 * S;     // MMA -> TMA                  [S]
+  uint64_t* atfree = bars + 4 * S;    // MMA -> A converters (TMEM)  [2]
+  uint64_t* tfull = bars + 4 * S + 2;   // MMA -> epilogue           [2]
+  uint64_t* tempty = bars + 4 * S + 4;  // epilogue -> MMA           [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 * S + 6);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const uint32_t tmem_cols = (4 * nc <= 32) ? 32 : (4 * nc <= 64) ? 64 : (4 * nc <= 128) ? 128
-                             : (4 * nc <= 256) ? 256 : 512;
+  constexpr uint32_t kTmemCols = 512;
+  const uint32_t a_col0 = 4 * nc;  // A staging: 2 buffers x (32 hi + 32 lo) columns
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&conv[s], kConvThreads);
+      mbar_init(&aready[s], 128);
+      mbar_init(&bready[s], 128);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
+      mbar_init(&atfree[a], 1);
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 128);
     }
@@ -108,7 +110,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
   }
-  if (warp == 2) tmem_alloc(tmem_slot, tmem_cols);
+  if (warp == 2) tmem_alloc(tmem_slot, kTmemCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -123,7 +125,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      const uint32_t tx = kChunkBytesA + nc * 128;
+      const uint32_t tx = kChunkBytesA + rowsB;
       for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
         const int t = tile / tiles_per_bin;
         const int rem = tile - t * tiles_per_bin;
@@ -133,7 +135,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           uint8_t* st = smem + s * stageBytes;
           mbar_arrive_expect_tx(&full[s], tx);
           tma_load_3d(st, &tmA, &full[s], kc * 32, mt * kTileM, t);
-          tma_load_3d(st + 2 * kChunkBytesA, &tmB, &full[s], kc * 32, nt * nc, t);
+          tma_load_3d(st + kChunkBytesA, &tmB, &full[s], kc * 32, nt * nc, t);
           if (++s == S) { s = 0; ph ^= 1; }
         }
       }
@@ -143,129 +145,111 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const uint32_t idesc = umma_idesc_tf32(kTileM, 2 * nc);
     int s = 0;
     uint32_t ph = 0;
+    uint32_t g = 0;  // global chunk counter (TMEM A buffer = g & 1)
     int local = 0;
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++local) {
       const int a = local & 1;
-      const uint32_t aph = (local >> 1) & 1;
-      mbar_wait(&tempty[a], aph ^ 1);
+      mbar_wait(&tempty[a], ((local >> 1) & 1) ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + a * (2 * nc);
-      for (int kc = 0; kc < kc_n; ++kc) {
-        mbar_wait(&conv[s], ph);
+      for (int kc = 0; kc < kc_n; ++kc, ++g) {
+        mbar_wait(&aready[s], ph);
+        mbar_wait(&bready[s], ph);
         tc_fence_after();
         if (lane == 0) {
-          const uint32_t st = smem_u32(smem + s * stageBytes);
-          const uint32_t a_hi = st, a_lo = st + kChunkBytesA;
-          const uint32_t b_hi = st + 2 * kChunkBytesA, b_lo = b_hi + bBytes;
+          const uint32_t a_hi = tmem_base + a_col0 + (g & 1) * 64;
+          const uint32_t a_lo = a_hi + 32;
+          const uint32_t b_hi = smem_u32(smem + s * stageBytes + kChunkBytesA);
+          const uint32_t b_lo = b_hi + 2 * rowsB;
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
-            const uint32_t off = kk * 32;
-            const uint64_t dah = umma_desc_sw128(a_hi + off);
-            const uint64_t dal = umma_desc_sw128(a_lo + off);
-            const uint64_t dbh = umma_desc_sw128(b_hi + off);
-            const uint64_t dbl = umma_desc_sw128(b_lo + off);
-            umma_tf32(d_tmem, dah, dbh, idesc, (kc | kk) ? 1u : 0u);
-            if (!(p.dbg & 2)) {
-              umma_tf32(d_tmem, dah, dbl, idesc, 1u);
-              umma_tf32(d_tmem, dal, dbh, idesc, 1u);
-            }
+            const uint64_t dbh = umma_desc_sw128(b_hi + kk * 32);
+            const uint64_t dbl = umma_desc_sw128(b_lo + kk * 32);
+            umma_tf32_ts(d_tmem, a_hi + kk * 8, dbh, idesc, (kc | kk) ? 1u : 0u);
+            umma_tf32_ts(d_tmem, a_hi + kk * 8, dbl, idesc, 1u);
+            umma_tf32_ts(d_tmem, a_lo + kk * 8, dbh, idesc, 1u);
           }
           umma_commit(&empty[s]);
+          umma_commit(&atfree[g & 1]);
           if (kc == kc_n - 1) umma_commit(&tfull[a]);
         }
         __syncwarp();
         if (++s == S) { s = 0; ph ^= 1; }
       }
     }
-  } else if (warp >= 4 && warp < 12) {
-    // ------------------------------------------------ converters
-    const int ct = threadIdx.x - 128;  // 0..255
-    float s1 = 1.f, s2 = 1.f, s3 = 1.f;  // re=(p, s1 q)  im=(s2 q, s3 p)
-    // fprop: re (p,q) im (-q,p); bprop: re (p,-q) im (q,p); accGrad: re (p,q) im (q,-p)
-    bool swap_im = true;
-    if (p.mode == kModeFprop) { s1 = 1.f; s2 = -1.f; s3 = 1.f; }
-    else if (p.mode == kModeBprop) { s1 = -1.f; s2 = 1.f; s3 = 1.f; }
-    else { s1 = 1.f; s2 = 1.f; s3 = -1.f; }
-    (void)swap_im;
+  } else if (warp >= 4 && warp < 8) {
+    // ------------------------------------------------ A converters: smem -> TMEM hi/lo
+    const int q = warp & 3;        // TMEM lane quadrant of this warp
+    const int m = q * 32 + lane;   // A row
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    int s = 0;
+    uint32_t ph = 0;
+    uint32_t g = 0;
+    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+      for (int kc = 0; kc < kc_n; ++kc, ++g) {
+        mbar_wait(&full[s], ph);
+        const uint8_t* arow = smem + s * stageBytes + (m >> 3) * 1024 + (m & 7) * 128;
+        float x[32], lo[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {  // 16-B chunk c of the row sits at c ^ (m & 7)
+          const float4 v = *reinterpret_cast<const float4*>(arow + ((c ^ (m & 7)) << 4));
+          x[4 * c + 0] = v.x;
+          x[4 * c + 1] = v.y;
+          x[4 * c + 2] = v.z;
+          x[4 * c + 3] = v.w;
+        }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) lo[i] = tf32_lo(x[i]);
+        mbar_wait(&atfree[g & 1], ((g >> 1) & 1) ^ 1);  // MMAs of chunk g-2 done with it
+        tc_fence_after();
+        const uint32_t ta = tmem_base + lane_off + a_col0 + (g & 1) * 64;
+        tmem_st_32x32b_x32(ta, x);
+        tmem_st_32x32b_x32(ta + 32, lo);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&aready[s]);
+        if (++s == S) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp >= 8 && warp < 12) {
+    // ------------------------------------------------ B converters: im rows, lo rows
+    const int ct = threadIdx.x - 256;  // 0..127
+    const int nb = nc * 8;             // float4 per raw B tile
     int s = 0;
     uint32_t ph = 0;
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
       for (int kc = 0; kc < kc_n; ++kc) {
         mbar_wait(&full[s], ph);
-        if (p.dbg & 1) {
-          fence_proxy_async_smem();
-          mbar_arrive(&conv[s]);
-          if (++s == S) { s = 0; ph ^= 1; }
-          continue;
-        }
-        uint8_t* st = smem + s * stageBytes;
-        float4* ahi = reinterpret_cast<float4*>(st);
-        float4* alo = reinterpret_cast<float4*>(st + kChunkBytesA);
-        if (p.dbg & 4) {
-#pragma unroll 4
-          for (int i = ct; i < kChunkBytesA / 16; i += kConvThreads) {
-            const float4 v = ahi[i];
-            float4 l;
-            l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-            l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-            l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-            l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-            alo[i] = l;
-          }
-        } else {
-#pragma unroll 4
-          for (int i = ct; i < kChunkBytesA / 16; i += kConvThreads) {
-            const float4 v = ahi[i];
-            float4 h, l;
-            h.x = tf32_round(v.x); l.x = v.x - h.x;
-            h.y = tf32_round(v.y); l.y = v.y - h.y;
-            h.z = tf32_round(v.z); l.z = v.z - h.z;
-            h.w = tf32_round(v.w); l.w = v.w - h.w;
-            ahi[i] = h;
-            alo[i] = l;
-          }
-        }
-        float4* bre_hi = reinterpret_cast<float4*>(st + 2 * kChunkBytesA);
-        float4* bim_hi = reinterpret_cast<float4*>(st + 2 * kChunkBytesA + nc * 128);
-        float4* bre_lo = reinterpret_cast<float4*>(st + 2 * kChunkBytesA + bBytes);
-        float4* bim_lo = reinterpret_cast<float4*>(st + 2 * kChunkBytesA + bBytes + nc * 128);
-        const int nb = nc * 8;  // float4 per raw B tile
-#pragma unroll 2
-        for (int i = ct; i < nb; i += kConvThreads) {
-          const float4 v = bre_hi[i];  // (p0, q0, p1, q1)
-          const float4 re = make_float4(v.x, s1 * v.y, v.z, s1 * v.w);
-          const float4 im = make_float4(s2 * v.y, s3 * v.x, s2 * v.w, s3 * v.z);
-          float4 h, l;
-          h.x = tf32_round(re.x); l.x = re.x - h.x;
-          h.y = tf32_round(re.y); l.y = re.y - h.y;
-          h.z = tf32_round(re.z); l.z = re.z - h.z;
-          h.w = tf32_round(re.w); l.w = re.w - h.w;
-          bre_hi[i] = h;
-          bre_lo[i] = l;
-          h.x = tf32_round(im.x); l.x = im.x - h.x;
-          h.y = tf32_round(im.y); l.y = im.y - h.y;
-          h.z = tf32_round(im.z); l.z = im.z - h.z;
-          h.w = tf32_round(im.w); l.w = im.w - h.w;
-          bim_hi[i] = h;
-          bim_lo[i] = l;
+        uint8_t* bh = smem + s * stageBytes + kChunkBytesA;
+        const float4* bre = reinterpret_cast<const float4*>(bh);
+        float4* bim = reinterpret_cast<float4*>(bh + rowsB);
+        float4* blr = reinterpret_cast<float4*>(bh + 2 * rowsB);
+        float4* bli = reinterpret_cast<float4*>(bh + 3 * rowsB);
+#pragma unroll 3
+        for (int i = ct; i < nb; i += 128) {
+          const float4 v = bre[i];  // (p0, q0, p1, q1): re rows are the raw rows
+          bim[i] = make_float4(-v.y, v.x, -v.w, v.z);
+          const float4 l = make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
+          blr[i] = l;
+          bli[i] = make_float4(-l.y, l.x, -l.w, l.z);
         }
         fence_proxy_async_smem();
-        mbar_arrive(&conv[s]);
+        mbar_arrive(&bready[s]);
         if (++s == S) { s = 0; ph ^= 1; }
       }
     }
   } else if (warp >= 12) {
     // ------------------------------------------------ epilogue
-    const int q = warp & 3;  // TMEM lane quadrant accessible to this warp
+    const int q = warp & 3;
     const int row = q * 32 + lane;
+    const float im_sign = p.im_sign;
     int local = 0;
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++local) {
       const int t = tile / tiles_per_bin;
       const int rem = tile - t * tiles_per_bin;
       const int mt = rem / p.n_tiles, nt = rem - mt * p.n_tiles;
       const int a = local & 1;
-      const uint32_t aph = (local >> 1) & 1;
-      mbar_wait(&tfull[a], aph);
+      mbar_wait(&tfull[a], (local >> 1) & 1);
       tc_fence_after();
       const int m = mt * kTileM + row;
       const bool mok = m < p.m_valid;
@@ -280,8 +264,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int n = n0 + i;
-          if (mok && nb + i < nc && n < p.n_valid)
-            out[(long long)n * p.m_valid] = make_float2(re[i], im[i]);
+          if (mok && n < p.n_valid)
+            out[(long long)n * p.m_valid] = make_float2(re[i], im_sign * im[i]);
         }
       }
       tc_fence_before();
@@ -292,7 +276,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, tmem_cols);
+    tmem_dealloc(tmem_base, kTmemCols);
   }
 }
 

@@ -188,19 +188,22 @@ struct GemmGeom {
 static GemmGeom gemm_geom(size_t M, size_t N, const DevInfo& di) {
   GemmGeom g;
   const size_t n16 = round_up(N, 16);
-  g.n_tiles = (int)((n16 + 127) / 128);
+  g.n_tiles = (int)((n16 + kMaxNc - 1) / kMaxNc);
   g.nc = (int)round_up((n16 + g.n_tiles - 1) / g.n_tiles, 16);
   g.m_tiles = (int)((M + kTileM - 1) / kTileM);
   const int sb = gemm_stage_bytes(g.nc);
   const int budget = di.max_smem_optin - 1024 - 256;
-  g.stages = std::min(4, budget / sb);
+  g.stages = std::min(6, budget / sb);
   if (g.stages < 2) throw Error(FFTCONV_B200_CUDA_ERROR, "gemm tile does not fit shared memory");
   g.smem = (size_t)g.stages * sb + 1024 + 256;
   return g;
 }
 
+// D[t] = A[t] . conj(B[t])^T per bin; im_sign = -1 returns conj(D) (the
+// accGrad orientation, conj(A) . B).  A: F[t][M][2*kpad], B: F[t][N][2*kpad].
 static void launch_gemm(const float* A, const float* B, float* out, size_t bins, size_t M,
-                        size_t N, size_t kpad, int mode, const DevInfo& di, cudaStream_t st) {
+                        size_t N, size_t kpad, float im_sign, const DevInfo& di,
+                        cudaStream_t st) {
   const GemmGeom g = gemm_geom(M, N, di);
   CUtensorMap ta = make_operand_map(A, kpad, M, bins, kTileM);
   CUtensorMap tb = make_operand_map(B, kpad, N, bins, (uint32_t)g.nc);
@@ -214,18 +217,24 @@ static void launch_gemm(const float* A, const float* B, float* out, size_t bins,
   p.n_tiles = g.n_tiles;
   p.nc = g.nc;
   p.stages = g.stages;
-  p.mode = mode;
-  static const int dbg = [] {
-    const char* e = std::getenv("FFTCONV_B200_GEMM_DEBUG");  // experiments only
-    return e ? std::atoi(e) : 0;
-  }();
-  p.dbg = dbg;
-  FCB_CUDA(cudaFuncSetAttribute(cgemm_bins_tcgen05, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)g.smem));
+  p.im_sign = im_sign;
+  static int smem_set = 0;  // opt-in once per process for the largest size seen
+  if ((int)g.smem > smem_set) {
+    FCB_CUDA(cudaFuncSetAttribute(cgemm_bins_tcgen05, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)g.smem));
+    smem_set = (int)g.smem;
+  }
   const long long tiles = (long long)bins * g.m_tiles * g.n_tiles;
   const int grid = (int)std::min<long long>(tiles, di.sms);
   cgemm_bins_tcgen05<<<grid, kGemmThreads, g.smem, st>>>(ta, tb, p);
   FCB_CUDA(cudaGetLastError());
+}
+
+// Negates every imaginary part of n complex values (debug hook helper).
+__global__ void conj_inplace_kernel(float2* v, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    v[i].y = -v[i].y;
 }
 
 }  // namespace fcb
@@ -357,7 +366,7 @@ void run_forward(fftconv_b200_ws* ws, const float* x, size_t S, size_t f, size_t
               (int)k, (int)(k | 1)};
   launch_r2c(m, b, st);
   record(ws, 2, st);
-  launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, S, fo, kp, kModeFprop, ws->di, st);
+  launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, S, fo, kp, 1.0f, ws->di, st);
   record(ws, 3, st);
   C2RParams c{ws->bufD, y, (long long)(no * no), (long long)(fo * no * no), (int)fo, (int)S,
               (int)no, 0, 0, 1.0f / (float)(m * m)};
@@ -390,10 +399,10 @@ void run_grad_input(fftconv_b200_ws* ws, const float* gy, size_t S, size_t fo, s
   launch_r2c(m, a, st);
   record(ws, 1, st);
   R2CParams b{w, ws->bufB, (long long)(k * k), (long long)(f * k * k), (int)f, (int)fo, (int)kp,
-              (int)k, (int)(k | 1)};
+              (int)k, (int)(k | 1), /*conj=*/1};  // GX = GY . W = GY . conj(conj W)
   launch_r2c(m, b, st);
   record(ws, 2, st);
-  launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, S, f, kp, kModeBprop, ws->di, st);
+  launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, S, f, kp, 1.0f, ws->di, st);
   record(ws, 3, st);
   C2RParams c{ws->bufD, gx, (long long)(n * n), (long long)(f * n * n), (int)f, (int)S, (int)n,
               0, 0, 1.0f / (float)(m * m)};
@@ -431,7 +440,7 @@ void run_grad_weight(fftconv_b200_ws* ws, const float* gy, size_t Sg, size_t fo,
               (int)n, (int)(n | 1)};
   launch_r2c(m, b, st);
   record(ws, 2, st);
-  launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, fo, f, kp, kModeAccGrad, ws->di, st);
+  launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, fo, f, kp, -1.0f, ws->di, st);
   record(ws, 3, st);
   C2RParams c{ws->bufD, gw, (long long)(k * k), (long long)(f * k * k), (int)f, (int)fo, (int)k,
               0, 0, 1.0f / (float)(m * m)};
@@ -734,7 +743,10 @@ int fftconv_b200_debug_cgemm(const float* a, const float* b, float* out, size_t 
                                K * 2 * sizeof(float), bins * M, cudaMemcpyDeviceToDevice, st));
     FCB_CUDA(cudaMemcpy2DAsync(B, kp * 2 * sizeof(float), b, K * 2 * sizeof(float),
                                K * 2 * sizeof(float), bins * N, cudaMemcpyDeviceToDevice, st));
-    launch_gemm(A, B, out, bins, M, N, kp, mode, di, st);
+    if (mode == 1)  // A . B = A . conj(conj(B))
+      conj_inplace_kernel<<<256, 256, 0, st>>>(reinterpret_cast<float2*>(B),
+                                               (long long)(bins * N * kp));
+    launch_gemm(A, B, out, bins, M, N, kp, mode == 2 ? -1.0f : 1.0f, di, st);
     FCB_CUDA(cudaStreamSynchronize(st));
     cudaFree(A);
     cudaFree(B);
