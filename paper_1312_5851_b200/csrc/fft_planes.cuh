@@ -28,6 +28,7 @@
 #include <cstdint>
 #include <type_traits>
 
+#include "ptx.cuh"
 #include "twiddles.cuh"
 
 namespace fcb {
@@ -205,6 +206,32 @@ struct PlaneTraits {
 #endif
   static constexpr int MIN_CTAS = (M == 64) ? FCB_MINB64 : (M == 32) ? (G == 8 ? 4 : FCB_MINB32) : 4;
 };
+
+// Hermitian inverse DFT emitting real outputs through emit(i, x_i) in
+// order, without materialising the output array.
+template <int N, typename Emit>
+__device__ __forceinline__ void irfft_emit(float2 (&X)[N / 2 + 1], Emit&& emit) {
+  static_assert(N >= 4, "irfft_emit");
+  constexpr int H = N / 2;
+  X[0].y = 0.f;
+  X[H].y = 0.f;
+  float2 z[H];
+  static_for<0, H>([&](auto K) {
+    constexpr int k = decltype(K)::value;
+    const float2 xk = X[k];
+    const float2 xc = cconj(X[H - k]);
+    const float2 e = cadd(xk, xc);
+    float2 o = csub(xk, xc);
+    if constexpr (k != 0) o = cmul(o, tw128<true>(k * (128 / N)));
+    z[k] = make_float2(e.x - o.y, e.y + o.x);  // e + i*o
+  });
+  fft_reg<H, true>(z);
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    emit(2 * i, z[i].x);
+    emit(2 * i + 1, z[i].y);
+  }
+}
 
 // ---------------------------------------------------------------- K1: r2c
 struct R2CParams {
@@ -450,6 +477,366 @@ __global__ void __launch_bounds__(PlaneTraits<M>::THREADS, PlaneTraits<M>::MIN_C
 #pragma unroll
       for (int i = 0; i < M; ++i)
         if (i < p.crop) dst[(long long)i * p.crop] = x[i] * scale;
+    }
+  }
+}
+
+// ======================================================================
+// m in {4, 8, 16, 32}: warp-specialised persistent kernels.
+//
+// Each CTA loops over 16-plane groups.  Producer warps run pass 1 of group
+// i+1 (global loads straight into registers, FFT, write the intermediate)
+// while consumer warps run pass 2 of group i (read the intermediate, FFT,
+// stream the result out), through a double-buffered shared-memory
+// intermediate guarded by named barriers (FULL[b]: producers -> consumers,
+// EMPTY[b]: consumers -> producers).  Loads of the next group therefore
+// overlap the FFTs and stores of the current one instead of alternating
+// within a CTA.
+// ======================================================================
+template <int M>
+struct WsR2CTraits {
+  static constexpr int G = 16;
+  static constexpr int PC = M / 2 + 1;
+  static constexpr int NPAIR = M / 2;
+  static constexpr int P1_THREADS = ((G * NPAIR + 31) / 32) * 32;
+  static constexpr int P2_THREADS = ((G * PC + 31) / 32) * 32;
+  static constexpr int THREADS = P1_THREADS + P2_THREADS;
+  static constexpr int CP = M + 1;  // intermediate row stride (float2), odd
+  static constexpr int BUF = G * PC * CP;
+  static constexpr int SMEM = 2 * BUF * 8;
+};
+
+enum : int { kBarFull0 = 1, kBarEmpty0 = 3 };  // named barrier ids (+buffer)
+
+// grid = persistent (<= groups), block = THREADS, smem = SMEM.
+// Groups: g = r * (kpad/16) + jg.
+template <int M>
+__global__ void __launch_bounds__(WsR2CTraits<M>::THREADS, 1) r2c_ws_kernel(const R2CParams p) {
+  using Tr = WsR2CTraits<M>;
+  constexpr int G = Tr::G, PC = Tr::PC, NPAIR = Tr::NPAIR, CP = Tr::CP;
+  constexpr int NT = Tr::THREADS;
+  extern __shared__ __align__(16) float2 ws_s1[];  // [2][G][PC][CP]
+  const int ngj = p.kpad / G;
+  const int ngroups = p.R * ngj;
+  const int src = p.src;
+
+  if (threadIdx.x < Tr::P1_THREADS) {
+    // ---------------- producers: pass 1 (column pairs)
+    const int item = threadIdx.x;
+    const bool act = item < G * NPAIR;
+    const int jl = item / NPAIR, cp = item - (item / NPAIR) * NPAIR;
+    const int c = 2 * cp;
+    int i = 0;
+    for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++i) {
+      const int b = i & 1;
+      const int r = g / ngj, j0 = (g - r * ngj) * G;
+      float2 z[M];
+      const bool ld = act && (j0 + jl) < p.J && c < src;
+      const bool has_b = c + 1 < src;
+      const float* col = p.in + (long long)r * p.in_sr + (long long)(j0 + jl) * p.in_sj + c;
+#pragma unroll
+      for (int row = 0; row < M; ++row) {
+        z[row].x = (ld && row < src) ? __ldg(col + row * src) : 0.f;
+        z[row].y = (ld && has_b && row < src) ? __ldg(col + row * src + 1) : 0.f;
+      }
+      fft_reg<M, false>(z);
+      if (i >= 2) named_bar_sync(kBarEmpty0 + b, NT);
+      if (act) {
+        float2* dst = ws_s1 + b * Tr::BUF + (jl * PC) * CP + c;
+        static_for<0, PC>([&](auto U) {
+          constexpr int u = decltype(U)::value;
+          const float2 zu = z[u];
+          const float2 zc = cconj(z[(M - u) % M]);
+          dst[u * CP] = make_float2(0.5f * (zu.x + zc.x), 0.5f * (zu.y + zc.y));
+          const float2 d = csub(zu, zc);
+          dst[u * CP + 1] = make_float2(0.5f * d.y, -0.5f * d.x);  // (zu - zc) / (2i)
+        });
+      }
+      named_bar_arrive(kBarFull0 + b, NT);
+    }
+    // balance the consumers' final EMPTY arrivals
+    for (int k = (i >= 2 ? i - 2 : 0); k < i; ++k) named_bar_sync(kBarEmpty0 + (k & 1), NT);
+  } else {
+    // ---------------- consumers: pass 2 (rows) + bin-major stores
+    const int item = threadIdx.x - Tr::P1_THREADS;
+    const bool act = item < G * PC;
+    const int jl = item % G, u = item / G;
+    const long long bstride = (long long)p.R * p.kpad;  // float2 per bin
+    const float csign = p.conj ? -1.f : 1.f;
+    int i = 0;
+    for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++i) {
+      const int b = i & 1;
+      const int r = g / ngj, j0 = (g - r * ngj) * G;
+      named_bar_sync(kBarFull0 + b, NT);
+      float2 w[M];
+      if (act) {
+        const float2* row = ws_s1 + b * Tr::BUF + (jl * PC + u) * CP;
+#pragma unroll
+        for (int cc = 0; cc < M; ++cc) w[cc] = row[cc];
+      }
+      named_bar_arrive(kBarEmpty0 + b, NT);
+      if (act) {
+        fft_reg<M, false>(w);
+        float2* o = reinterpret_cast<float2*>(p.out) + (long long)r * p.kpad + j0 + jl +
+                    (long long)(u * M) * bstride;
+#pragma unroll
+        for (int v = 0; v < M; ++v) {
+          *o = make_float2(w[v].x, csign * w[v].y);
+          o += bstride;
+        }
+      }
+    }
+  }
+}
+
+template <int M>
+struct WsC2RTraits {
+  static constexpr int G = 16;
+  static constexpr int PC = M / 2 + 1;
+  static constexpr int P1_THREADS = ((G * PC + 31) / 32) * 32;
+  static constexpr int P2_THREADS = ((G * (M / 2) + 31) / 32) * 32;
+  static constexpr int THREADS = P1_THREADS + P2_THREADS;
+  static constexpr int CP = M + 1;  // odd
+  static constexpr int BUF = G * PC * CP;
+  static constexpr int SMEM = 2 * BUF * 8;
+};
+
+// grid = persistent, groups g = r * ceil(J/16) + jg.  crop <= M.
+template <int M>
+__global__ void __launch_bounds__(WsC2RTraits<M>::THREADS, 1) c2r_ws_kernel(const C2RParams p) {
+  using Tr = WsC2RTraits<M>;
+  constexpr int G = Tr::G, PC = Tr::PC, CP = Tr::CP;
+  constexpr int NT = Tr::THREADS;
+  extern __shared__ __align__(16) float2 ws_s1[];  // [2][G][PC][CP]
+  const int ngj = (p.J + G - 1) / G;
+  const int ngroups = p.R * ngj;
+  const int crop = p.crop;
+  const long long bstride = (long long)p.R * p.J;  // float2 per bin
+
+  if (threadIdx.x < Tr::P1_THREADS) {
+    // ---------------- producers: inverse row FFT over v (lanes = planes)
+    const int item = threadIdx.x;
+    const bool act = item < G * PC;
+    const int jl = item % G, u = item / G;
+    int i = 0;
+    for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++i) {
+      const int b = i & 1;
+      const int r = g / ngj, j0 = (g - r * ngj) * G;
+      const bool ld = act && (j0 + jl) < p.J;
+      float2 z[M];
+      const float2* srcp = reinterpret_cast<const float2*>(p.in) + (long long)r * p.J + j0 + jl +
+                           (long long)(u * M) * bstride;
+#pragma unroll
+      for (int v = 0; v < M; ++v) {
+        z[v] = ld ? __ldg(srcp) : make_float2(0.f, 0.f);
+        srcp += bstride;
+      }
+      fft_reg<M, true>(z);
+      if (i >= 2) named_bar_sync(kBarEmpty0 + b, NT);
+      if (act) {
+        float2* dst = ws_s1 + b * Tr::BUF + (jl * PC + u) * CP;
+#pragma unroll
+        for (int cc = 0; cc < M; ++cc)
+          if (cc < crop) dst[cc] = z[cc];
+      }
+      named_bar_arrive(kBarFull0 + b, NT);
+    }
+    for (int k = (i >= 2 ? i - 2 : 0); k < i; ++k) named_bar_sync(kBarEmpty0 + (k & 1), NT);
+  } else {
+    // ---------------- consumers: Hermitian c2r over u, two columns per FFT
+    const int item = threadIdx.x - Tr::P1_THREADS;
+    const int npair = (crop + 1) >> 1;
+    const bool act = item < G * npair;
+    const int jl = act ? item / npair : 0, cp = act ? item - (item / npair) * npair : 0;
+    const int cl = 2 * cp;
+    const bool has_b = cl + 1 < crop;
+    const float scale = p.scale;
+    int i = 0;
+    for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++i) {
+      const int b = i & 1;
+      const int r = g / ngj, j0 = (g - r * ngj) * G;
+      named_bar_sync(kBarFull0 + b, NT);
+      float2 zz[M];
+      if (act) {
+        const float2* colp = ws_s1 + b * Tr::BUF + (jl * PC) * CP + cl;
+        static_for<0, PC>([&](auto U) {
+          constexpr int uu = decltype(U)::value;
+          float2 a = colp[uu * CP];
+          float2 bb = has_b ? colp[uu * CP + 1] : make_float2(0.f, 0.f);
+          if constexpr (uu == 0 || 2 * uu == M) {  // c2r ignores these imaginary parts
+            a.y = 0.f;
+            bb.y = 0.f;
+          }
+          zz[uu] = make_float2(a.x - bb.y, a.y + bb.x);  // a + i b
+          if constexpr (uu != 0 && 2 * uu != M) zz[M - uu] = make_float2(a.x + bb.y, bb.x - a.y);
+        });
+      }
+      named_bar_arrive(kBarEmpty0 + b, NT);
+      if (act && (j0 + jl) < p.J) {
+        fft_reg<M, true>(zz);
+        float* dst = p.out + (long long)r * p.out_sr + (long long)(j0 + jl) * p.out_sj + cl;
+#pragma unroll
+        for (int row = 0; row < M; ++row) {
+          if (row < crop) {
+            dst[0] = zz[row].x * scale;
+            if (has_b) dst[1] = zz[row].y * scale;
+            dst += crop;
+          }
+        }
+      }
+    }
+  }
+}
+
+// ======================================================================
+// m = 64: warp-specialised persistent kernels, 4 planes per group (a 64x33
+// intermediate per plane; double-buffered that is 137 KB).  Pass-1 columns
+// use the half-length real FFT; 64-point complex row FFTs are split into
+// two 32-point halves by one decimation-in-frequency stage so a thread
+// holds 32 complex values.
+// ======================================================================
+struct Ws64 {
+  static constexpr int M = 64, G = 4, PC = 33, CP = 65;
+  static constexpr int BUF = G * PC * CP;             // float2 per buffer
+  static constexpr int SMEM = 2 * BUF * 8;
+  static constexpr int COLS_THREADS = G * M;          // 256: one column per thread
+  static constexpr int ROWS_THREADS = ((G * PC * 2 + 31) / 32) * 32;  // 264 -> 288
+  static constexpr int THREADS = COLS_THREADS + ROWS_THREADS;
+};
+
+// grid = persistent, groups g = r * (kpad/4) + jg.
+__global__ void __maxnreg__(96) r2c_ws64_kernel(const R2CParams p) {
+  constexpr int M = 64, G = Ws64::G, PC = Ws64::PC, CP = Ws64::CP, NT = Ws64::THREADS;
+  extern __shared__ __align__(16) float2 ws_s1[];  // [2][G][PC][CP]
+  const int ngj = p.kpad / G;
+  const int ngroups = p.R * ngj;
+  const int src = p.src;
+  if (threadIdx.x < Ws64::COLS_THREADS) {
+    // ---------------- producers: one real column per thread
+    const int jl = threadIdx.x / M, c = threadIdx.x % M;
+    int i = 0;
+    for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++i) {
+      const int b = i & 1;
+      const int r = g / ngj, j0 = (g - r * ngj) * G;
+      const bool ld = (j0 + jl) < p.J && c < src;
+      const float* col = p.in + (long long)r * p.in_sr + (long long)(j0 + jl) * p.in_sj + c;
+      float x[M];
+#pragma unroll
+      for (int row = 0; row < M; ++row) x[row] = (ld && row < src) ? __ldg(col + row * src) : 0.f;
+      if (i >= 2) named_bar_sync(kBarEmpty0 + b, NT);
+      float2* dst = ws_s1 + b * Ws64::BUF + (jl * PC) * CP + c;
+      rfft_emit<M>(x, [&](int u, float2 v) { dst[u * CP] = v; });
+      named_bar_arrive(kBarFull0 + b, NT);
+    }
+    for (int k = (i >= 2 ? i - 2 : 0); k < i; ++k) named_bar_sync(kBarEmpty0 + (k & 1), NT);
+  } else {
+    // ---------------- consumers: (plane, u, half) -> 32-point FFT -> v = 2i + h
+    const int item = threadIdx.x - Ws64::COLS_THREADS;
+    const bool act = item < G * PC * 2;
+    const int jl = item % G, h = (item / G) & 1, u = item / (2 * G);
+    const long long bstride = (long long)p.R * p.kpad;  // float2 per bin
+    const float csign = p.conj ? -1.f : 1.f;
+    int i = 0;
+    for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++i) {
+      const int b = i & 1;
+      const int r = g / ngj, j0 = (g - r * ngj) * G;
+      named_bar_sync(kBarFull0 + b, NT);
+      float2 z[32];
+      if (act) {
+        const float2* row = ws_s1 + b * Ws64::BUF + (jl * PC + u) * CP;
+        static_for<0, 32>([&](auto Cc) {
+          constexpr int cc = decltype(Cc)::value;
+          const float2 a0 = row[cc], a1 = row[cc + 32];
+          if (h == 0) {
+            z[cc] = cadd(a0, a1);
+          } else {
+            if constexpr (cc == 0) z[cc] = csub(a0, a1);
+            else z[cc] = cmul(csub(a0, a1), tw128<false>(cc * 2));
+          }
+        });
+      }
+      named_bar_arrive(kBarEmpty0 + b, NT);
+      if (act) {
+        fft_reg<32, false>(z);
+        float2* o = reinterpret_cast<float2*>(p.out) + (long long)r * p.kpad + j0 + jl +
+                    (long long)(u * M + h) * bstride;
+        const long long st2 = 2 * bstride;
+#pragma unroll
+        for (int v = 0; v < 32; ++v) {
+          *o = make_float2(z[v].x, csign * z[v].y);
+          o += st2;
+        }
+      }
+    }
+  }
+}
+
+// grid = persistent, groups g = r * ceil(J/4) + jg.
+__global__ void __maxnreg__(96) c2r_ws64_kernel(const C2RParams p) {
+  constexpr int M = 64, G = Ws64::G, PC = Ws64::PC, CP = Ws64::CP, NT = Ws64::THREADS;
+  extern __shared__ __align__(16) float2 ws_s1[];  // [2][G][PC][CP]
+  const int ngj = (p.J + G - 1) / G;
+  const int ngroups = p.R * ngj;
+  const int crop = p.crop;
+  const long long bstride = (long long)p.R * p.J;  // float2 per bin
+  if (threadIdx.x >= Ws64::COLS_THREADS) {
+    // ---------------- producers: (plane, u, half) inverse 64-point row FFT
+    const int item = threadIdx.x - Ws64::COLS_THREADS;
+    const bool act = item < G * PC * 2;
+    const int jl = item % G, h = (item / G) & 1, u = item / (2 * G);
+    int i = 0;
+    for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++i) {
+      const int b = i & 1;
+      const int r = g / ngj, j0 = (g - r * ngj) * G;
+      const bool ld = act && (j0 + jl) < p.J;
+      const float2* srcp = reinterpret_cast<const float2*>(p.in) + (long long)r * p.J + j0 + jl +
+                           (long long)(u * M) * bstride;
+      float2 z[32];
+      static_for<0, 32>([&](auto Vv) {
+        constexpr int v = decltype(Vv)::value;
+        const float2 a0 = ld ? __ldg(srcp + v * bstride) : make_float2(0.f, 0.f);
+        const float2 a1 = ld ? __ldg(srcp + (v + 32) * bstride) : make_float2(0.f, 0.f);
+        if (h == 0) {
+          z[v] = cadd(a0, a1);
+        } else {
+          if constexpr (v == 0) z[v] = csub(a0, a1);
+          else z[v] = cmul(csub(a0, a1), tw128<true>(v * 2));
+        }
+      });
+      fft_reg<32, true>(z);
+      if (i >= 2) named_bar_sync(kBarEmpty0 + b, NT);
+      if (act) {
+        float2* dst = ws_s1 + b * Ws64::BUF + (jl * PC + u) * CP;
+#pragma unroll
+        for (int k = 0; k < 32; ++k)
+          if (2 * k + h < crop) dst[2 * k + h] = z[k];
+      }
+      named_bar_arrive(kBarFull0 + b, NT);
+    }
+    for (int k = (i >= 2 ? i - 2 : 0); k < i; ++k) named_bar_sync(kBarEmpty0 + (k & 1), NT);
+  } else {
+    // ---------------- consumers: one Hermitian column per thread
+    const int jl = threadIdx.x / M, c = threadIdx.x % M;
+    const bool act = c < crop;
+    const float scale = p.scale;
+    int i = 0;
+    for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++i) {
+      const int b = i & 1;
+      const int r = g / ngj, j0 = (g - r * ngj) * G;
+      named_bar_sync(kBarFull0 + b, NT);
+      float2 X[PC];
+      if (act) {
+        const float2* colp = ws_s1 + b * Ws64::BUF + (jl * PC) * CP + c;
+#pragma unroll
+        for (int uu = 0; uu < PC; ++uu) X[uu] = colp[uu * CP];
+      }
+      named_bar_arrive(kBarEmpty0 + b, NT);
+      if (act && (j0 + jl) < p.J) {
+        float* dst = p.out + (long long)r * p.out_sr + (long long)(j0 + jl) * p.out_sj + c;
+        irfft_emit<M>(X, [&](int row, float v) {
+          if (row < crop) dst[row * crop] = v * scale;
+        });
+      }
     }
   }
 }

@@ -135,7 +135,45 @@ static void launch_r2c_m(const R2CParams& p, cudaStream_t st) {
   FCB_CUDA(cudaGetLastError());
 }
 
-static void launch_r2c(size_t m, const R2CParams& p, cudaStream_t st) {
+template <int M>
+static void launch_r2c_ws(const R2CParams& p, const DevInfo& di, cudaStream_t st) {
+  using Tr = WsR2CTraits<M>;
+  auto kern = r2c_ws_kernel<M>;
+  static bool attr = false;
+  if (!attr) {
+    FCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Tr::SMEM));
+    attr = true;
+  }
+  int per_sm = 1;
+  FCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Tr::THREADS, Tr::SMEM));
+  const int groups = p.R * (p.kpad / Tr::G);
+  const int grid = std::max(1, std::min(groups, di.sms * std::max(per_sm, 1)));
+  kern<<<grid, Tr::THREADS, Tr::SMEM, st>>>(p);
+  FCB_CUDA(cudaGetLastError());
+}
+
+static void launch_r2c(size_t m, const R2CParams& p, cudaStream_t st, const DevInfo& di) {
+  switch (m) {
+    case 4: return launch_r2c_ws<4>(p, di, st);
+    case 8: return launch_r2c_ws<8>(p, di, st);
+    case 16: return launch_r2c_ws<16>(p, di, st);
+    case 32: return launch_r2c_ws<32>(p, di, st);
+    case 64: {
+      if (p.src <= 32) break;  // small planes (kernels): 16-plane groups write full lines
+      static bool attr = false;
+      if (!attr) {
+        FCB_CUDA(cudaFuncSetAttribute(r2c_ws64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      Ws64::SMEM));
+        attr = true;
+      }
+      const int groups = p.R * (p.kpad / Ws64::G);
+      const int grid = std::max(1, std::min(groups, di.sms));
+      r2c_ws64_kernel<<<grid, Ws64::THREADS, Ws64::SMEM, st>>>(p);
+      FCB_CUDA(cudaGetLastError());
+      return;
+    }
+    default: break;
+  }
   switch (m) {
     case 1: return launch_r2c_m<1>(p, st);
     case 2: return launch_r2c_m<2>(p, st);
@@ -166,7 +204,45 @@ static void launch_c2r_m(C2RParams p, cudaStream_t st) {
   FCB_CUDA(cudaGetLastError());
 }
 
-static void launch_c2r(size_t m, const C2RParams& p, cudaStream_t st) {
+template <int M>
+static void launch_c2r_ws(const C2RParams& p, const DevInfo& di, cudaStream_t st) {
+  using Tr = WsC2RTraits<M>;
+  auto kern = c2r_ws_kernel<M>;
+  static bool attr = false;
+  if (!attr) {
+    FCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Tr::SMEM));
+    attr = true;
+  }
+  int per_sm = 1;
+  FCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Tr::THREADS, Tr::SMEM));
+  const int groups = p.R * ((p.J + Tr::G - 1) / Tr::G);
+  const int grid = std::max(1, std::min(groups, di.sms * std::max(per_sm, 1)));
+  kern<<<grid, Tr::THREADS, Tr::SMEM, st>>>(p);
+  FCB_CUDA(cudaGetLastError());
+}
+
+static void launch_c2r(size_t m, const C2RParams& p, cudaStream_t st, const DevInfo& di) {
+  switch (m) {
+    case 4: return launch_c2r_ws<4>(p, di, st);
+    case 8: return launch_c2r_ws<8>(p, di, st);
+    case 16: return launch_c2r_ws<16>(p, di, st);
+    case 32: return launch_c2r_ws<32>(p, di, st);
+    case 64: {
+      if (p.crop <= 32) break;  // small crops (gw): 16-plane groups read full lines
+      static bool attr = false;
+      if (!attr) {
+        FCB_CUDA(cudaFuncSetAttribute(c2r_ws64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      Ws64::SMEM));
+        attr = true;
+      }
+      const int groups = p.R * ((p.J + Ws64::G - 1) / Ws64::G);
+      const int grid = std::max(1, std::min(groups, di.sms));
+      c2r_ws64_kernel<<<grid, Ws64::THREADS, Ws64::SMEM, st>>>(p);
+      FCB_CUDA(cudaGetLastError());
+      return;
+    }
+    default: break;
+  }
   switch (m) {
     case 1: return launch_c2r_m<1>(p, st);
     case 2: return launch_c2r_m<2>(p, st);
@@ -248,6 +324,9 @@ struct fftconv_b200_ws {
   uint64_t cap_x = 0, cap_w = 0, cap_y = 0;
   size_t max_m = 1;
   // frequency-domain buffers (floats)
+  // frequency-domain arena: [A | B | D], one allocation so a single L2
+  // access-policy window can cover the spectra between K1 -> K3 -> K4
+  float* freq = nullptr;
   float* bufA = nullptr;
   float* bufB = nullptr;
   float* bufD = nullptr;
@@ -320,11 +399,26 @@ size_t prepare(fftconv_b200_ws* ws, const fftconv_b200_layer& c) {
   return m;
 }
 
+void set_arena(fftconv_b200_ws* ws, size_t na, size_t nb, size_t nd) {
+  na = round_up(std::max(na, ws->nA), 64);  // keep 256-B alignment of B and D
+  nb = round_up(std::max(nb, ws->nB), 64);
+  nd = round_up(std::max(nd, ws->nD), 64);
+  if (ws->freq && na == ws->nA && nb == ws->nB && nd == ws->nD) return;
+  if (ws->freq) cudaFree(ws->freq);
+  ws->freq = nullptr;
+  ws->nA = ws->nB = ws->nD = 0;
+  FCB_CUDA(cudaMalloc(&ws->freq, (na + nb + nd) * sizeof(float)));
+  ws->bufA = ws->freq;
+  ws->bufB = ws->freq + na;
+  ws->bufD = ws->bufB + nb;
+  ws->nA = na;
+  ws->nB = nb;
+  ws->nD = nd;
+}
+
 void ensure_freq(fftconv_b200_ws* ws, Pass pass, const fftconv_b200_layer& c, size_t m) {
   const PassNeed need = pass_need(pass, c.batch, c.in_maps, c.out_maps, m);
-  grow(ws->bufA, ws->nA, need.a);
-  grow(ws->bufB, ws->nB, need.b);
-  grow(ws->bufD, ws->nD, need.d);
+  if (need.a > ws->nA || need.b > ws->nB || need.d > ws->nD) set_arena(ws, need.a, need.b, need.d);
 }
 
 void record(fftconv_b200_ws* ws, int i, cudaStream_t st) {
@@ -360,17 +454,17 @@ void run_forward(fftconv_b200_ws* ws, const float* x, size_t S, size_t f, size_t
   record(ws, 0, st);
   R2CParams a{x, ws->bufA, (long long)(f * n * n), (long long)(n * n), (int)S, (int)f, (int)kp,
               (int)n, (int)(n | 1)};
-  launch_r2c(m, a, st);
+  launch_r2c(m, a, st, ws->di);
   record(ws, 1, st);
   R2CParams b{w, ws->bufB, (long long)(f * k * k), (long long)(k * k), (int)fo, (int)f, (int)kp,
               (int)k, (int)(k | 1)};
-  launch_r2c(m, b, st);
+  launch_r2c(m, b, st, ws->di);
   record(ws, 2, st);
   launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, S, fo, kp, 1.0f, ws->di, st);
   record(ws, 3, st);
   C2RParams c{ws->bufD, y, (long long)(no * no), (long long)(fo * no * no), (int)fo, (int)S,
               (int)no, 0, 0, 1.0f / (float)(m * m)};
-  launch_c2r(m, c, st);
+  launch_c2r(m, c, st, ws->di);
   record(ws, 4, st);
   ws->last_launches = 4;
   ws->ctr[0] += S * f + fo * f;
@@ -396,17 +490,17 @@ void run_grad_input(fftconv_b200_ws* ws, const float* gy, size_t S, size_t fo, s
   record(ws, 0, st);
   R2CParams a{gy, ws->bufA, (long long)(fo * no * no), (long long)(no * no), (int)S, (int)fo,
               (int)kp, (int)no, (int)(no | 1)};
-  launch_r2c(m, a, st);
+  launch_r2c(m, a, st, ws->di);
   record(ws, 1, st);
   R2CParams b{w, ws->bufB, (long long)(k * k), (long long)(f * k * k), (int)f, (int)fo, (int)kp,
               (int)k, (int)(k | 1), /*conj=*/1};  // GX = GY . W = GY . conj(conj W)
-  launch_r2c(m, b, st);
+  launch_r2c(m, b, st, ws->di);
   record(ws, 2, st);
   launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, S, f, kp, 1.0f, ws->di, st);
   record(ws, 3, st);
   C2RParams c{ws->bufD, gx, (long long)(n * n), (long long)(f * n * n), (int)f, (int)S, (int)n,
               0, 0, 1.0f / (float)(m * m)};
-  launch_c2r(m, c, st);
+  launch_c2r(m, c, st, ws->di);
   record(ws, 4, st);
   ws->last_launches = 4;
   ws->ctr[0] += S * fo + fo * f;
@@ -434,17 +528,17 @@ void run_grad_weight(fftconv_b200_ws* ws, const float* gy, size_t Sg, size_t fo,
   record(ws, 0, st);
   R2CParams a{gy, ws->bufA, (long long)(no * no), (long long)(fo * no * no), (int)fo, (int)S,
               (int)kp, (int)no, (int)(no | 1)};
-  launch_r2c(m, a, st);
+  launch_r2c(m, a, st, ws->di);
   record(ws, 1, st);
   R2CParams b{x, ws->bufB, (long long)(n * n), (long long)(f * n * n), (int)f, (int)S, (int)kp,
               (int)n, (int)(n | 1)};
-  launch_r2c(m, b, st);
+  launch_r2c(m, b, st, ws->di);
   record(ws, 2, st);
   launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, fo, f, kp, -1.0f, ws->di, st);
   record(ws, 3, st);
   C2RParams c{ws->bufD, gw, (long long)(k * k), (long long)(f * k * k), (int)f, (int)fo, (int)k,
               0, 0, 1.0f / (float)(m * m)};
-  launch_c2r(m, c, st);
+  launch_c2r(m, c, st, ws->di);
   record(ws, 4, st);
   ws->last_launches = 4;
   ws->ctr[0] += S * f + S * fo;
@@ -499,9 +593,7 @@ int fftconv_b200_ws_create(const fftconv_b200_layer* configs, size_t count, int 
           nd = std::max(nd, need.d);
         }
       }
-      grow(ws->bufA, ws->nA, na);
-      grow(ws->bufB, ws->nB, nb);
-      grow(ws->bufD, ws->nD, nd);
+      set_arena(ws, na, nb, nd);
     } catch (...) {
       fftconv_b200_ws_destroy(ws);
       throw;
@@ -514,7 +606,7 @@ void fftconv_b200_ws_destroy(fftconv_b200_ws* ws) {
   if (!ws) return;
   {
     DeviceGuard g(ws->device);
-    for (float* p : {ws->bufA, ws->bufB, ws->bufD, ws->st_in0, ws->st_in1, ws->st_out})
+    for (float* p : {ws->freq, ws->st_in0, ws->st_in1, ws->st_out})
       if (p) cudaFree(p);
     if (ws->host_stream) cudaStreamDestroy(ws->host_stream);
     if (ws->ev_ready)
@@ -694,7 +786,7 @@ int fftconv_b200_debug_r2c(const float* in, size_t planes, size_t src, size_t m,
     FCB_CUDA(cudaMalloc(&F, bins * planes * kp * 2 * sizeof(float)));
     R2CParams p{in, F, (long long)(src * src), 0, (int)planes, 1, (int)kp, (int)src,
                 (int)(src | 1)};
-    launch_r2c(m, p, (cudaStream_t)stream);
+    launch_r2c(m, p, (cudaStream_t)stream, dev_info(0));
     // F[(t*planes + p)*32 + 0..1] -> out[(p*bins + t)*2]
     for (size_t pl = 0; pl < planes; ++pl)
       FCB_CUDA(cudaMemcpy2DAsync(out + pl * bins * 2, 2 * sizeof(float), F + pl * kp * 2,
@@ -719,7 +811,7 @@ int fftconv_b200_debug_c2r(const float* in, size_t planes, size_t m, size_t crop
                                  cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
     C2RParams p{P, out, 0, (long long)(crop * crop), 1, (int)planes, (int)crop, 0, 0,
                 1.0f / (float)(m * m)};
-    launch_c2r(m, p, (cudaStream_t)stream);
+    launch_c2r(m, p, (cudaStream_t)stream, dev_info(0));
     FCB_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
     cudaFree(P);
   });
