@@ -116,7 +116,8 @@ int fftconv_b200_grad_weight_host(fftconv_b200_ws* ws, const float* gy, size_t S
 /* ---- Instrumentation ----------------------------------------------------
  * When enabled, each operator records CUDA events between its stages on
  * the launching stream; fftconv_b200_stage_ms returns the last call's
- * per-stage device times (ms): [0] r2c of operand A, [1] r2c of operand B,
+ * per-stage device times (ms): [0] r2c of operand A (of both operands when
+ * one launch transforms both), [1] r2c of operand B (~0 when merged),
  * [2] per-bin complex GEMM, [3] c2r + crop.  Blocks until they are known. */
 int fftconv_b200_set_stage_timing(fftconv_b200_ws* ws, int enable);
 int fftconv_b200_stage_ms(fftconv_b200_ws* ws, float out[4]);

@@ -115,6 +115,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // prologue above overlaps the previous kernel's tail
+  pdl_trigger();
 
   const int tiles_per_bin = p.m_tiles * p.n_tiles;
   const int total_tiles = p.bins * tiles_per_bin;

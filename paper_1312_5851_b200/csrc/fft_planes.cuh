@@ -254,6 +254,8 @@ __global__ void __launch_bounds__(PlaneTraits<M>::THREADS, PlaneTraits<M>::MIN_C
   constexpr int PC = Tr::PC, UC = Tr::UC, SPLIT = Tr::SPLIT;
   constexpr int G = Tr::G;
   extern __shared__ float2 s1[];  // [G][UC][cpad]
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.y;
   const int j0 = blockIdx.x * G;
   const int u0 = blockIdx.z * UC;
@@ -383,6 +385,8 @@ __global__ void __launch_bounds__(PlaneTraits<M>::THREADS, PlaneTraits<M>::MIN_C
   constexpr int G = Tr::G;
   constexpr int NS = M / SPLIT;
   extern __shared__ float2 s1[];  // [G][PC][ccpad]
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.y;
   const int j0 = blockIdx.x * G;
   const int c0 = blockIdx.z * p.cc;
@@ -508,17 +512,25 @@ struct WsR2CTraits {
 
 enum : int { kBarFull0 = 1, kBarEmpty0 = 3 };  // named barrier ids (+buffer)
 
+// One launch transforms both operands of an operator (A groups first, then
+// B groups): the tail of one overlaps the other and a launch gap disappears.
+struct R2CPair {
+  R2CParams op[2];
+  int n;  // 1 or 2 operands
+};
+
 // grid = persistent (<= groups), block = THREADS, smem = SMEM.
 // Groups: g = r * (kpad/16) + jg.
 template <int M>
-__global__ void __launch_bounds__(WsR2CTraits<M>::THREADS, 1) r2c_ws_kernel(const R2CParams p) {
+__global__ void __launch_bounds__(WsR2CTraits<M>::THREADS, 1) r2c_ws_kernel(const R2CPair P) {
   using Tr = WsR2CTraits<M>;
   constexpr int G = Tr::G, PC = Tr::PC, NPAIR = Tr::NPAIR, CP = Tr::CP;
   constexpr int NT = Tr::THREADS;
   extern __shared__ __align__(16) float2 ws_s1[];  // [2][G][PC][CP]
-  const int ngj = p.kpad / G;
-  const int ngroups = p.R * ngj;
-  const int src = p.src;
+  const int ngA = P.op[0].R * (P.op[0].kpad / G);
+  const int ngroups = ngA + (P.n > 1 ? P.op[1].R * (P.op[1].kpad / G) : 0);
+  pdl_wait();
+  pdl_trigger();
 
   if (threadIdx.x < Tr::P1_THREADS) {
     // ---------------- producers: pass 1 (column pairs)
@@ -529,7 +541,11 @@ __global__ void __launch_bounds__(WsR2CTraits<M>::THREADS, 1) r2c_ws_kernel(cons
     int i = 0;
     for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++i) {
       const int b = i & 1;
-      const int r = g / ngj, j0 = (g - r * ngj) * G;
+      const int which = g >= ngA;
+      const R2CParams& p = P.op[which];
+      const int gl = g - which * ngA, ngj = p.kpad / G;
+      const int r = gl / ngj, j0 = (gl - r * ngj) * G;
+      const int src = p.src;
       float2 z[M];
       const bool ld = act && (j0 + jl) < p.J && c < src;
       const bool has_b = c + 1 < src;
@@ -561,12 +577,15 @@ __global__ void __launch_bounds__(WsR2CTraits<M>::THREADS, 1) r2c_ws_kernel(cons
     const int item = threadIdx.x - Tr::P1_THREADS;
     const bool act = item < G * PC;
     const int jl = item % G, u = item / G;
-    const long long bstride = (long long)p.R * p.kpad;  // float2 per bin
-    const float csign = p.conj ? -1.f : 1.f;
     int i = 0;
     for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++i) {
       const int b = i & 1;
-      const int r = g / ngj, j0 = (g - r * ngj) * G;
+      const int which = g >= ngA;
+      const R2CParams& p = P.op[which];
+      const int gl = g - which * ngA, ngj = p.kpad / G;
+      const int r = gl / ngj, j0 = (gl - r * ngj) * G;
+      const long long bstride = (long long)p.R * p.kpad;  // float2 per bin
+      const float csign = p.conj ? -1.f : 1.f;
       named_bar_sync(kBarFull0 + b, NT);
       float2 w[M];
       if (act) {
@@ -608,6 +627,8 @@ __global__ void __launch_bounds__(WsC2RTraits<M>::THREADS, 1) c2r_ws_kernel(cons
   constexpr int G = Tr::G, PC = Tr::PC, CP = Tr::CP;
   constexpr int NT = Tr::THREADS;
   extern __shared__ __align__(16) float2 ws_s1[];  // [2][G][PC][CP]
+  pdl_wait();
+  pdl_trigger();
   const int ngj = (p.J + G - 1) / G;
   const int ngroups = p.R * ngj;
   const int crop = p.crop;
@@ -705,19 +726,24 @@ struct Ws64 {
 };
 
 // grid = persistent, groups g = r * (kpad/4) + jg.
-__global__ void __maxnreg__(96) r2c_ws64_kernel(const R2CParams p) {
+__global__ void __maxnreg__(96) r2c_ws64_kernel(const R2CPair P) {
   constexpr int M = 64, G = Ws64::G, PC = Ws64::PC, CP = Ws64::CP, NT = Ws64::THREADS;
   extern __shared__ __align__(16) float2 ws_s1[];  // [2][G][PC][CP]
-  const int ngj = p.kpad / G;
-  const int ngroups = p.R * ngj;
-  const int src = p.src;
+  const int ngA = P.op[0].R * (P.op[0].kpad / G);
+  const int ngroups = ngA + (P.n > 1 ? P.op[1].R * (P.op[1].kpad / G) : 0);
+  pdl_wait();
+  pdl_trigger();
   if (threadIdx.x < Ws64::COLS_THREADS) {
     // ---------------- producers: one real column per thread
     const int jl = threadIdx.x / M, c = threadIdx.x % M;
     int i = 0;
     for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++i) {
       const int b = i & 1;
-      const int r = g / ngj, j0 = (g - r * ngj) * G;
+      const int which = g >= ngA;
+      const R2CParams& p = P.op[which];
+      const int gl = g - which * ngA, ngj = p.kpad / G;
+      const int r = gl / ngj, j0 = (gl - r * ngj) * G;
+      const int src = p.src;
       const bool ld = (j0 + jl) < p.J && c < src;
       const float* col = p.in + (long long)r * p.in_sr + (long long)(j0 + jl) * p.in_sj + c;
       float x[M];
@@ -734,12 +760,15 @@ __global__ void __maxnreg__(96) r2c_ws64_kernel(const R2CParams p) {
     const int item = threadIdx.x - Ws64::COLS_THREADS;
     const bool act = item < G * PC * 2;
     const int jl = item % G, h = (item / G) & 1, u = item / (2 * G);
-    const long long bstride = (long long)p.R * p.kpad;  // float2 per bin
-    const float csign = p.conj ? -1.f : 1.f;
     int i = 0;
     for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++i) {
       const int b = i & 1;
-      const int r = g / ngj, j0 = (g - r * ngj) * G;
+      const int which = g >= ngA;
+      const R2CParams& p = P.op[which];
+      const int gl = g - which * ngA, ngj = p.kpad / G;
+      const int r = gl / ngj, j0 = (gl - r * ngj) * G;
+      const long long bstride = (long long)p.R * p.kpad;  // float2 per bin
+      const float csign = p.conj ? -1.f : 1.f;
       named_bar_sync(kBarFull0 + b, NT);
       float2 z[32];
       if (act) {
@@ -775,6 +804,8 @@ __global__ void __maxnreg__(96) r2c_ws64_kernel(const R2CParams p) {
 __global__ void __maxnreg__(96) c2r_ws64_kernel(const C2RParams p) {
   constexpr int M = 64, G = Ws64::G, PC = Ws64::PC, CP = Ws64::CP, NT = Ws64::THREADS;
   extern __shared__ __align__(16) float2 ws_s1[];  // [2][G][PC][CP]
+  pdl_wait();
+  pdl_trigger();
   const int ngj = (p.J + G - 1) / G;
   const int ngroups = p.R * ngj;
   const int crop = p.crop;

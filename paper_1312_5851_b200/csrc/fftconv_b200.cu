@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -123,73 +124,136 @@ static DevInfo dev_info(int device) {
   return d;
 }
 
+// Every launch goes through cudaLaunchKernelEx with programmatic stream
+// serialisation: a kernel's CTAs may start (prologue: smem carve-up, mbarrier
+// init, TMEM alloc, descriptor prefetch) while the previous kernel on the
+// stream drains; each kernel calls griddepcontrol.wait before touching
+// global memory, so ordering is unchanged.
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  FCB_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
+
+// Per-kernel host-side caches, keyed by the kernel's address (several
+// kernels share a signature, so a function-local static would be shared).
+static std::mutex g_kcache_mu;
+static std::unordered_map<const void*, int> g_smem_done, g_occ;
+
+// Opt a kernel into > 48 KB dynamic shared memory (once per size).
+template <typename K>
+static void smem_optin(K kern, int bytes) {
+  if (bytes <= 48 * 1024) return;
+  std::lock_guard<std::mutex> lk(g_kcache_mu);
+  int& done = g_smem_done[reinterpret_cast<const void*>(kern)];
+  if (bytes > done) {
+    FCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    done = bytes;
+  }
+}
+
+template <typename K>
+static int occupancy(K kern, int threads, int smem) {
+  std::lock_guard<std::mutex> lk(g_kcache_mu);
+  auto it = g_occ.find(reinterpret_cast<const void*>(kern));
+  if (it != g_occ.end()) return it->second;
+  int per_sm = 1;
+  FCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+  return g_occ[reinterpret_cast<const void*>(kern)] = std::max(per_sm, 1);
+}
+
+// ---- K1 ---------------------------------------------------------------
 template <int M>
-static void launch_r2c_m(const R2CParams& p, cudaStream_t st) {
+static void launch_r2c_legacy(const R2CParams& p, cudaStream_t st) {
   using Tr = PlaneTraits<M>;
   auto kern = r2c_planes_kernel<M>;
   const size_t smem = (size_t)Tr::G * Tr::UC * p.cpad * sizeof(float2);
-  if (smem > 48 * 1024)
-    FCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  smem_optin(kern, (int)smem);
   dim3 grid(p.kpad / Tr::G, p.R, (Tr::PC + Tr::UC - 1) / Tr::UC);
-  kern<<<grid, Tr::THREADS, smem, st>>>(p);
-  FCB_CUDA(cudaGetLastError());
+  launch_pdl(kern, grid, dim3(Tr::THREADS), smem, st, p);
+}
+
+// Warp-specialised kernels: m in {4..32}, or m = 64 with planes wider than
+// 32 (kernels at m = 64 keep 16-plane groups so every store is a full line).
+static bool r2c_ws_capable(size_t m, const R2CParams& p) {
+  return (m >= 4 && m <= 32) || (m == 64 && p.src > 32);
 }
 
 template <int M>
-static void launch_r2c_ws(const R2CParams& p, const DevInfo& di, cudaStream_t st) {
+static void launch_r2c_ws(const R2CPair& P, const DevInfo& di, cudaStream_t st) {
   using Tr = WsR2CTraits<M>;
   auto kern = r2c_ws_kernel<M>;
-  static bool attr = false;
-  if (!attr) {
-    FCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Tr::SMEM));
-    attr = true;
-  }
-  int per_sm = 1;
-  FCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Tr::THREADS, Tr::SMEM));
-  const int groups = p.R * (p.kpad / Tr::G);
-  const int grid = std::max(1, std::min(groups, di.sms * std::max(per_sm, 1)));
-  kern<<<grid, Tr::THREADS, Tr::SMEM, st>>>(p);
-  FCB_CUDA(cudaGetLastError());
+  smem_optin(kern, Tr::SMEM);
+  int groups = 0;
+  for (int i = 0; i < P.n; ++i) groups += P.op[i].R * (P.op[i].kpad / Tr::G);
+  const int grid = std::max(1, std::min(groups, di.sms * occupancy(kern, Tr::THREADS, Tr::SMEM)));
+  launch_pdl(kern, dim3(grid), dim3(Tr::THREADS), Tr::SMEM, st, P);
 }
 
-static void launch_r2c(size_t m, const R2CParams& p, cudaStream_t st, const DevInfo& di) {
+static void launch_r2c_ws64(const R2CPair& P, const DevInfo& di, cudaStream_t st) {
+  smem_optin(r2c_ws64_kernel, Ws64::SMEM);
+  int groups = 0;
+  for (int i = 0; i < P.n; ++i) groups += P.op[i].R * (P.op[i].kpad / Ws64::G);
+  const int grid = std::max(1, std::min(groups, di.sms));
+  launch_pdl(r2c_ws64_kernel, dim3(grid), dim3(Ws64::THREADS), Ws64::SMEM, st, P);
+}
+
+static void launch_r2c_group(size_t m, const R2CPair& P, cudaStream_t st, const DevInfo& di) {
   switch (m) {
-    case 4: return launch_r2c_ws<4>(p, di, st);
-    case 8: return launch_r2c_ws<8>(p, di, st);
-    case 16: return launch_r2c_ws<16>(p, di, st);
-    case 32: return launch_r2c_ws<32>(p, di, st);
-    case 64: {
-      if (p.src <= 32) break;  // small planes (kernels): 16-plane groups write full lines
-      static bool attr = false;
-      if (!attr) {
-        FCB_CUDA(cudaFuncSetAttribute(r2c_ws64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      Ws64::SMEM));
-        attr = true;
-      }
-      const int groups = p.R * (p.kpad / Ws64::G);
-      const int grid = std::max(1, std::min(groups, di.sms));
-      r2c_ws64_kernel<<<grid, Ws64::THREADS, Ws64::SMEM, st>>>(p);
-      FCB_CUDA(cudaGetLastError());
-      return;
-    }
-    default: break;
+    case 4: return launch_r2c_ws<4>(P, di, st);
+    case 8: return launch_r2c_ws<8>(P, di, st);
+    case 16: return launch_r2c_ws<16>(P, di, st);
+    case 32: return launch_r2c_ws<32>(P, di, st);
+    case 64: return launch_r2c_ws64(P, di, st);
+  }
+}
+
+static void launch_r2c_one(size_t m, const R2CParams& p, cudaStream_t st, const DevInfo& di) {
+  if (r2c_ws_capable(m, p)) {
+    R2CPair P{{p, p}, 1};
+    return launch_r2c_group(m, P, st, di);
   }
   switch (m) {
-    case 1: return launch_r2c_m<1>(p, st);
-    case 2: return launch_r2c_m<2>(p, st);
-    case 4: return launch_r2c_m<4>(p, st);
-    case 8: return launch_r2c_m<8>(p, st);
-    case 16: return launch_r2c_m<16>(p, st);
-    case 32: return launch_r2c_m<32>(p, st);
-    case 64: return launch_r2c_m<64>(p, st);
+    case 1: return launch_r2c_legacy<1>(p, st);
+    case 2: return launch_r2c_legacy<2>(p, st);
+    case 4: return launch_r2c_legacy<4>(p, st);
+    case 8: return launch_r2c_legacy<8>(p, st);
+    case 16: return launch_r2c_legacy<16>(p, st);
+    case 32: return launch_r2c_legacy<32>(p, st);
+    case 64: return launch_r2c_legacy<64>(p, st);
     default:
       throw Error(FFTCONV_B200_SIZE_ERROR,
                   "fft size " + std::to_string(m) + " not supported by the B200 kernels (max 64)");
   }
 }
 
+// Both forward transforms of an operator: one launch when one kernel can
+// take both operands.  Returns the number of launches.
+static int launch_r2c_both(size_t m, const R2CParams& a, const R2CParams& b, cudaStream_t st,
+                           const DevInfo& di) {
+  if (r2c_ws_capable(m, a) && r2c_ws_capable(m, b)) {
+    R2CPair P{{a, b}, 2};
+    launch_r2c_group(m, P, st, di);
+    return 1;
+  }
+  launch_r2c_one(m, a, st, di);
+  launch_r2c_one(m, b, st, di);
+  return 2;
+}
+
+// ---- K4 ---------------------------------------------------------------
 template <int M>
-static void launch_c2r_m(C2RParams p, cudaStream_t st) {
+static void launch_c2r_legacy(C2RParams p, cudaStream_t st) {
   using Tr = PlaneTraits<M>;
   constexpr int CCMAX = (M == 64) ? 22 : 32;
   const int nchunks = (p.crop + CCMAX - 1) / CCMAX;
@@ -197,28 +261,19 @@ static void launch_c2r_m(C2RParams p, cudaStream_t st) {
   p.ccpad = (p.cc % 2) ? p.cc : p.cc + 1;
   auto kern = c2r_planes_kernel<M>;
   const size_t smem = (size_t)Tr::G * Tr::PC * p.ccpad * sizeof(float2);
-  if (smem > 48 * 1024)
-    FCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  smem_optin(kern, (int)smem);
   dim3 grid((p.J + Tr::G - 1) / Tr::G, p.R, nchunks);
-  kern<<<grid, Tr::THREADS, smem, st>>>(p);
-  FCB_CUDA(cudaGetLastError());
+  launch_pdl(kern, grid, dim3(Tr::THREADS), smem, st, p);
 }
 
 template <int M>
 static void launch_c2r_ws(const C2RParams& p, const DevInfo& di, cudaStream_t st) {
   using Tr = WsC2RTraits<M>;
   auto kern = c2r_ws_kernel<M>;
-  static bool attr = false;
-  if (!attr) {
-    FCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Tr::SMEM));
-    attr = true;
-  }
-  int per_sm = 1;
-  FCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Tr::THREADS, Tr::SMEM));
+  smem_optin(kern, Tr::SMEM);
   const int groups = p.R * ((p.J + Tr::G - 1) / Tr::G);
-  const int grid = std::max(1, std::min(groups, di.sms * std::max(per_sm, 1)));
-  kern<<<grid, Tr::THREADS, Tr::SMEM, st>>>(p);
-  FCB_CUDA(cudaGetLastError());
+  const int grid = std::max(1, std::min(groups, di.sms * occupancy(kern, Tr::THREADS, Tr::SMEM)));
+  launch_pdl(kern, dim3(grid), dim3(Tr::THREADS), Tr::SMEM, st, p);
 }
 
 static void launch_c2r(size_t m, const C2RParams& p, cudaStream_t st, const DevInfo& di) {
@@ -229,28 +284,22 @@ static void launch_c2r(size_t m, const C2RParams& p, cudaStream_t st, const DevI
     case 32: return launch_c2r_ws<32>(p, di, st);
     case 64: {
       if (p.crop <= 32) break;  // small crops (gw): 16-plane groups read full lines
-      static bool attr = false;
-      if (!attr) {
-        FCB_CUDA(cudaFuncSetAttribute(c2r_ws64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      Ws64::SMEM));
-        attr = true;
-      }
+      smem_optin(c2r_ws64_kernel, Ws64::SMEM);
       const int groups = p.R * ((p.J + Ws64::G - 1) / Ws64::G);
       const int grid = std::max(1, std::min(groups, di.sms));
-      c2r_ws64_kernel<<<grid, Ws64::THREADS, Ws64::SMEM, st>>>(p);
-      FCB_CUDA(cudaGetLastError());
+      launch_pdl(c2r_ws64_kernel, dim3(grid), dim3(Ws64::THREADS), Ws64::SMEM, st, p);
       return;
     }
     default: break;
   }
   switch (m) {
-    case 1: return launch_c2r_m<1>(p, st);
-    case 2: return launch_c2r_m<2>(p, st);
-    case 4: return launch_c2r_m<4>(p, st);
-    case 8: return launch_c2r_m<8>(p, st);
-    case 16: return launch_c2r_m<16>(p, st);
-    case 32: return launch_c2r_m<32>(p, st);
-    case 64: return launch_c2r_m<64>(p, st);
+    case 1: return launch_c2r_legacy<1>(p, st);
+    case 2: return launch_c2r_legacy<2>(p, st);
+    case 4: return launch_c2r_legacy<4>(p, st);
+    case 8: return launch_c2r_legacy<8>(p, st);
+    case 16: return launch_c2r_legacy<16>(p, st);
+    case 32: return launch_c2r_legacy<32>(p, st);
+    case 64: return launch_c2r_legacy<64>(p, st);
     default:
       throw Error(FFTCONV_B200_SIZE_ERROR,
                   "fft size " + std::to_string(m) + " not supported by the B200 kernels (max 64)");
@@ -294,16 +343,10 @@ static void launch_gemm(const float* A, const float* B, float* out, size_t bins,
   p.nc = g.nc;
   p.stages = g.stages;
   p.im_sign = im_sign;
-  static int smem_set = 0;  // opt-in once per process for the largest size seen
-  if ((int)g.smem > smem_set) {
-    FCB_CUDA(cudaFuncSetAttribute(cgemm_bins_tcgen05, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)g.smem));
-    smem_set = (int)g.smem;
-  }
+  smem_optin(cgemm_bins_tcgen05, (int)g.smem);
   const long long tiles = (long long)bins * g.m_tiles * g.n_tiles;
   const int grid = (int)std::min<long long>(tiles, di.sms);
-  cgemm_bins_tcgen05<<<grid, kGemmThreads, g.smem, st>>>(ta, tb, p);
-  FCB_CUDA(cudaGetLastError());
+  launch_pdl(cgemm_bins_tcgen05, dim3(grid), dim3(kGemmThreads), g.smem, st, ta, tb, p);
 }
 
 // Negates every imaginary part of n complex values (debug hook helper).
@@ -454,11 +497,10 @@ void run_forward(fftconv_b200_ws* ws, const float* x, size_t S, size_t f, size_t
   record(ws, 0, st);
   R2CParams a{x, ws->bufA, (long long)(f * n * n), (long long)(n * n), (int)S, (int)f, (int)kp,
               (int)n, (int)(n | 1)};
-  launch_r2c(m, a, st, ws->di);
-  record(ws, 1, st);
   R2CParams b{w, ws->bufB, (long long)(f * k * k), (long long)(k * k), (int)fo, (int)f, (int)kp,
               (int)k, (int)(k | 1)};
-  launch_r2c(m, b, st, ws->di);
+  const int nl = launch_r2c_both(m, a, b, st, ws->di);
+  record(ws, 1, st);  // both forward transforms
   record(ws, 2, st);
   launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, S, fo, kp, 1.0f, ws->di, st);
   record(ws, 3, st);
@@ -466,7 +508,7 @@ void run_forward(fftconv_b200_ws* ws, const float* x, size_t S, size_t f, size_t
               (int)no, 0, 0, 1.0f / (float)(m * m)};
   launch_c2r(m, c, st, ws->di);
   record(ws, 4, st);
-  ws->last_launches = 4;
+  ws->last_launches = nl + 2;
   ws->ctr[0] += S * f + fo * f;
   ws->ctr[1] += S * fo;
   ws->ctr[2] += (uint64_t)bins * fo * f * S;
@@ -490,11 +532,10 @@ void run_grad_input(fftconv_b200_ws* ws, const float* gy, size_t S, size_t fo, s
   record(ws, 0, st);
   R2CParams a{gy, ws->bufA, (long long)(fo * no * no), (long long)(no * no), (int)S, (int)fo,
               (int)kp, (int)no, (int)(no | 1)};
-  launch_r2c(m, a, st, ws->di);
-  record(ws, 1, st);
   R2CParams b{w, ws->bufB, (long long)(k * k), (long long)(f * k * k), (int)f, (int)fo, (int)kp,
               (int)k, (int)(k | 1), /*conj=*/1};  // GX = GY . W = GY . conj(conj W)
-  launch_r2c(m, b, st, ws->di);
+  const int nl = launch_r2c_both(m, a, b, st, ws->di);
+  record(ws, 1, st);  // both forward transforms
   record(ws, 2, st);
   launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, S, f, kp, 1.0f, ws->di, st);
   record(ws, 3, st);
@@ -502,7 +543,7 @@ void run_grad_input(fftconv_b200_ws* ws, const float* gy, size_t S, size_t fo, s
               0, 0, 1.0f / (float)(m * m)};
   launch_c2r(m, c, st, ws->di);
   record(ws, 4, st);
-  ws->last_launches = 4;
+  ws->last_launches = nl + 2;
   ws->ctr[0] += S * fo + fo * f;
   ws->ctr[1] += S * f;
   ws->ctr[2] += (uint64_t)bins * fo * f * S;
@@ -528,11 +569,10 @@ void run_grad_weight(fftconv_b200_ws* ws, const float* gy, size_t Sg, size_t fo,
   record(ws, 0, st);
   R2CParams a{gy, ws->bufA, (long long)(no * no), (long long)(fo * no * no), (int)fo, (int)S,
               (int)kp, (int)no, (int)(no | 1)};
-  launch_r2c(m, a, st, ws->di);
-  record(ws, 1, st);
   R2CParams b{x, ws->bufB, (long long)(n * n), (long long)(f * n * n), (int)f, (int)S, (int)kp,
               (int)n, (int)(n | 1)};
-  launch_r2c(m, b, st, ws->di);
+  const int nl = launch_r2c_both(m, a, b, st, ws->di);
+  record(ws, 1, st);  // both forward transforms
   record(ws, 2, st);
   launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, fo, f, kp, -1.0f, ws->di, st);
   record(ws, 3, st);
@@ -540,7 +580,7 @@ void run_grad_weight(fftconv_b200_ws* ws, const float* gy, size_t Sg, size_t fo,
               0, 0, 1.0f / (float)(m * m)};
   launch_c2r(m, c, st, ws->di);
   record(ws, 4, st);
-  ws->last_launches = 4;
+  ws->last_launches = nl + 2;
   ws->ctr[0] += S * f + S * fo;
   ws->ctr[1] += fo * f;
   ws->ctr[2] += (uint64_t)bins * fo * f * S;
@@ -786,7 +826,7 @@ int fftconv_b200_debug_r2c(const float* in, size_t planes, size_t src, size_t m,
     FCB_CUDA(cudaMalloc(&F, bins * planes * kp * 2 * sizeof(float)));
     R2CParams p{in, F, (long long)(src * src), 0, (int)planes, 1, (int)kp, (int)src,
                 (int)(src | 1)};
-    launch_r2c(m, p, (cudaStream_t)stream, dev_info(0));
+    launch_r2c_one(m, p, (cudaStream_t)stream, dev_info(0));
     // F[(t*planes + p)*32 + 0..1] -> out[(p*bins + t)*2]
     for (size_t pl = 0; pl < planes; ++pl)
       FCB_CUDA(cudaMemcpy2DAsync(out + pl * bins * 2, 2 * sizeof(float), F + pl * kp * 2,

@@ -19,7 +19,7 @@ def test_bench_json_contract():
                 "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e",
                 "gpu_launches", "clocks"):
         assert key in line, key
-    assert line["value"] > 0 and line["gpu_launches"] == 12 * 3
+    assert line["value"] > 0 and 9 * 3 <= line["gpu_launches"] <= 12 * 3
     assert line["roofline"]["bound"] in ("hbm", "tensor") and line["roofline"]["frac"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["d2h_bytes_per_step"] > 0
     assert "workload" in line["config"]
