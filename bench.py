@@ -171,6 +171,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--dist-backend", default="nccl",
+                    help="nccl (one GPU per rank); gloo lets ranks share a GPU for testing")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg, label = parse_config(args.config)
@@ -187,10 +189,14 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
 
     k, n, f, fo, S = cfg
     no = n - k + 1
@@ -344,23 +350,27 @@ def main():
     # ---- end to end through the public API with host (pinned) buffers
     e2e = None
     if world == 1:
-        xp = torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()
-        wp = torch.from_numpy(np.ascontiguousarray(w)).pin_memory().numpy()
-        gyp = torch.from_numpy(np.ascontiguousarray(gy)).pin_memory().numpy()
+        def pinned(shape):
+            return torch.empty(shape, dtype=torch.float32).pin_memory().numpy()
+
+        xp, wp, gyp = pinned(x.shape), pinned(w.shape), pinned(gy.shape)
+        xp[...], wp[...], gyp[...] = x, w, gy
+        y_h, gx_h, gw_h = pinned((Sl, fo, no, no)), pinned((Sl, f, n, n)), pinned((fo, f, k, k))
         for _ in range(2):
-            ws.forward(xp, wp), ws.grad_input(gyp, wp), ws.grad_weight(gyp, xp)
+            ws.forward(xp, wp, out=y_h), ws.grad_input(gyp, wp, out=gx_h), ws.grad_weight(gyp, xp, out=gw_h)
         e2e_ms = []
         for _ in range(args.e2e_steps):
             t0 = time.perf_counter()
-            y_h = ws.forward(xp, wp)
-            gx_h = ws.grad_input(gyp, wp)
-            gw_h = ws.grad_weight(gyp, xp)
+            ws.forward(xp, wp, out=y_h)
+            ws.grad_input(gyp, wp, out=gx_h)
+            ws.grad_weight(gyp, xp, out=gw_h)
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
         h2d = 4 * (x.size + w.size + gy.size + w.size + gy.size + x.size)
         d2h = 4 * (y_h.size + gx_h.size + gw_h.size)
         e2e = {"value": statistics.mean(e2e_ms), "unit": "ms", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h),
-               "path": "ConvWorkspace.forward/grad_input/grad_weight on pinned numpy -> fftconv_b200_*_host C ABI"}
+               "path": "ConvWorkspace.forward/grad_input/grad_weight(out=) on pinned numpy -> "
+                       "fftconv_b200_*_host C ABI (H2D inputs, compute, D2H result, sync per call)"}
 
     # ---- CPU reference beside it (rank 0, N=1 only)
     cpu = None

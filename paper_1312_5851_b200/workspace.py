@@ -158,7 +158,16 @@ class ConvWorkspace:
         a = np.ascontiguousarray(a, dtype=np.float32)
         return a, a.ctypes.data_as(C.c_void_p)
 
-    def forward(self, x, w, threads: int = 1):
+    @staticmethod
+    def _host_out(out, shape):
+        """Result buffer for the host path: `out` (e.g. pinned) when given."""
+        if out is None:
+            return np.zeros(shape, dtype=np.float32)
+        if out.shape != tuple(shape) or out.dtype != np.float32 or not out.flags.c_contiguous:
+            raise ValueError(f"out must be a C-contiguous float32 array of shape {tuple(shape)}")
+        return out
+
+    def forward(self, x, w, threads: int = 1, out=None):
         """conv_fft.hpp:74-113: y = valid cross-correlation of x by w."""
         S, f, xr, xc = _shape4(x)
         wo, wi, k = _weights_shape(w)
@@ -174,13 +183,13 @@ class ConvWorkspace:
             return y
         xa, xp = self._host(x)
         wa, wp = self._host(w)
-        y = np.zeros((S, wo, max(no, 1), max(no, 1)), dtype=np.float32)
+        y = self._host_out(out, (S, wo, max(no, 1), max(no, 1)))
         code = L.fftconv_b200_forward_host(self._h, xp, S, f, xr, xc, wp, wo, wi, k,
                                            y.ctypes.data_as(C.c_void_p), int(threads))
         self._check(code)
         return y
 
-    def grad_input(self, gy, w, threads: int = 1):
+    def grad_input(self, gy, w, threads: int = 1, out=None):
         """conv_fft.hpp:115-152: gx = full convolution of gy by w."""
         S, fo, gr, gc = _shape4(gy)
         wo, wi, k = _weights_shape(w)
@@ -196,13 +205,13 @@ class ConvWorkspace:
             return gx
         ga, gp = self._host(gy)
         wa, wp = self._host(w)
-        gx = np.zeros((S, wi, n, n), dtype=np.float32)
+        gx = self._host_out(out, (S, wi, n, n))
         code = L.fftconv_b200_grad_input_host(self._h, gp, S, fo, gr, gc, wp, wo, wi, k,
                                               gx.ctypes.data_as(C.c_void_p), int(threads))
         self._check(code)
         return gx
 
-    def grad_weight(self, gy, x, threads: int = 1):
+    def grad_weight(self, gy, x, threads: int = 1, out=None):
         """conv_fft.hpp:154-206: gw = batch-summed valid correlation of x by gy."""
         Sg, fo, gr, gc = _shape4(gy)
         Sx, f, xr, xc = _shape4(x)
@@ -218,7 +227,7 @@ class ConvWorkspace:
             return gw
         ga, gp = self._host(gy)
         xa, xp = self._host(x)
-        gw = np.zeros((fo, f, k, k), dtype=np.float32)
+        gw = self._host_out(out, (fo, f, k, k))
         code = L.fftconv_b200_grad_weight_host(self._h, gp, Sg, fo, gr, gc, xp, Sx, f, xr, xc,
                                                gw.ctypes.data_as(C.c_void_p), int(threads))
         self._check(code)

@@ -1,0 +1,57 @@
+"""The N>1 bench path (minibatch sharding + all-reduce of gw) end to end on
+whatever GPUs the box has: two ranks via torchrun, gloo so they may share a
+single GPU.  NCCL itself is exercised by the driver's multi-GPU runs."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_bench_two_ranks_gloo():
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--config", "small", "--dist-backend", "gloo"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1  # rank 0 only
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["config"]["S_per_gpu"] == 4 and line["value"] > 0
+
+
+def test_sharded_grad_weight_matches_full_batch(dev):
+    """Two 'ranks' on one GPU in one process: per-slice gw summed == full gw."""
+    import numpy as np
+    import torch
+
+    import oracle
+    from paper_1312_5851_b200 import ConvWorkspace, LayerConfig
+    from paper_1312_5851_b200.sharded import shard_range
+
+    k, n, f, fo, S = 7, 32, 24, 20, 10
+    x = oracle.fill_uniform((S, f, n, n), 3, 1)
+    gy = oracle.fill_uniform((S, fo, n - k + 1, n - k + 1), 3, 3)
+    full = ConvWorkspace([LayerConfig(k, n, f, fo, S)]).grad_weight(torch.from_numpy(gy).to(dev),
+                                                                   torch.from_numpy(x).to(dev))
+    parts = []
+    for r in range(3):
+        b0, b1 = shard_range(S, 3, r)
+        ws = ConvWorkspace([LayerConfig(k, n, f, fo, b1 - b0)])
+        parts.append(ws.grad_weight(torch.from_numpy(gy[b0:b1]).to(dev), torch.from_numpy(x[b0:b1]).to(dev)))
+    tot = sum(parts).cpu().numpy()
+    assert oracle.max_rel_error(tot, full.cpu().numpy()) < 1e-5
+    del np
