@@ -136,13 +136,14 @@ def run_reference_arm(args, cfg, label):
         return
     threads = cpu_threads()
     k, n, f, fo, S = cfg
+    # Each step: the reference's own run_op_bench per operator (workspace and
+    # inputs built outside its clock, bench.hpp:100-142), one warm-up + one
+    # timed call; the step time is the sum of the three timed operators.
     for _ in range(args.warmup):
         cpu_reference_step_ms(cfg, 1, 0, threads)
     steps = []
     for _ in range(args.steps):
-        t0 = time.perf_counter()
-        cpu_reference_step_ms(cfg, 1, 0, threads)
-        steps.append((time.perf_counter() - t0) * 1e3)
+        steps.append(sum(cpu_reference_step_ms(cfg, 1, 1, threads).values()))
     ms = statistics.mean(steps)
     E = 2 * S * f * fo * (n - k + 1) ** 2 * k * k
     line = {
@@ -154,8 +155,9 @@ def run_reference_arm(args, cfg, label):
         "impl": "reference",
         "tflops_equiv": 3 * E / (ms * 1e-3) / 1e12,
         "cpu_baseline": {"value": ms, "unit": "ms", "cores": threads, "kind": "reference",
-                         "sample": f"reference ConvWorkspace<float> fprop+bprop+accGrad on the full layer, "
-                                   f"{args.steps} steps after {args.warmup} warm-up"},
+                         "sample": f"reference run_op_bench<float> (FFT method) fprop+bprop+accGrad on the "
+                                   f"full layer, {args.steps} steps (1 warm-up + 1 timed call per operator "
+                                   f"each) after {args.warmup} warm-up steps"},
         "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
