@@ -71,8 +71,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     cgemm_bins_tcgen05(const __grid_constant__ CUtensorMap tmA,
                        const __grid_constant__ CUtensorMap tmB, const GemmParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // 1024-B alignment for the swizzle atoms, derived from the __shared__
+  // pointer so the converters' accesses compile to LDS/STS.
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int nc = p.nc;
   const int S = p.stages;
   const int rowsB = nc * 128;  // bytes of nc rows
@@ -128,11 +129,26 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       int s = 0;
       uint32_t ph = 0;
       const uint32_t tx = kChunkBytesA + rowsB;
+      // L2 prefetch runs kPrefetch chunks ahead of the smem ring, so more
+      // bytes are in flight than the stages alone can hold.
+      constexpr int kPrefetch = 6;
+      int pf_tile = blockIdx.x, pf_kc = 0;
+      auto prefetch_next = [&]() {
+        if (pf_tile >= total_tiles) return;
+        const int t = pf_tile / tiles_per_bin;
+        const int rem = pf_tile - t * tiles_per_bin;
+        const int mt = rem / p.n_tiles, nt = rem - mt * p.n_tiles;
+        tma_prefetch_l2_3d(&tmA, pf_kc * 32, mt * kTileM, t);
+        tma_prefetch_l2_3d(&tmB, pf_kc * 32, nt * nc, t);
+        if (++pf_kc == kc_n) { pf_kc = 0; pf_tile += gridDim.x; }
+      };
+      for (int i = 0; i < kPrefetch; ++i) prefetch_next();
       for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
         const int t = tile / tiles_per_bin;
         const int rem = tile - t * tiles_per_bin;
         const int mt = rem / p.n_tiles, nt = rem - mt * p.n_tiles;
         for (int kc = 0; kc < kc_n; ++kc) {
+          prefetch_next();
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = smem + s * stageBytes;
           mbar_arrive_expect_tx(&full[s], tx);
