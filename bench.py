@@ -165,6 +165,10 @@ def run_reference_arm(args, cfg, label):
 
 # ---------------------------------------------------------------- our arm
 def main():
+    if os.environ.get("FFTCONV_B200_WATCHDOG"):  # debugging aid: dump stacks if stuck
+        import faulthandler
+
+        faulthandler.dump_traceback_later(float(os.environ["FFTCONV_B200_WATCHDOG"]), exit=True)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -215,11 +219,11 @@ def main():
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
-    def step():
+    def step(reduce=True):
         y = ws.forward(xd, wd)
         gx = ws.grad_input(gyd, wd)
         gw = ws.grad_weight(gyd, xd)
-        if world > 1:
+        if world > 1 and reduce:
             dist.all_reduce(gw)
         return y, gx, gw
 
@@ -227,9 +231,10 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    # time-based loops run a rank-dependent number of steps: no collectives there
     t_end = time.time() + 1.0
     while time.time() < t_end:
-        step()
+        step(reduce=False)
         flush.fill_(1.0)
     torch.cuda.synchronize()
 
@@ -239,7 +244,7 @@ def main():
     # keep the GPU busy while the sampler spins up, then the timed steps
     t_end = time.time() + 0.5
     while time.time() < t_end:
-        step()
+        step(reduce=False)
         flush.fill_(1.0)
     if world > 1:
         dist.barrier()
@@ -260,7 +265,7 @@ def main():
     # hold load a little longer so the sampler sees the clocks under load
     t_end = time.time() + 0.3
     while time.time() < t_end:
-        step()
+        step(reduce=False)
         flush.fill_(1.0)
     torch.cuda.synchronize()
     clocks = sampler.stop()

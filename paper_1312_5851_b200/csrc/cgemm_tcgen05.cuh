@@ -47,7 +47,7 @@
 namespace fcb {
 
 struct GemmParams {
-  float* out;     // P[t][n][2*m_valid]
+  float* out;     // P[t][n][ldm] complex
   int bins;
   int m_valid;    // A rows (M)
   int n_valid;    // complex output columns (N)
@@ -56,6 +56,7 @@ struct GemmParams {
   int nc;         // complex columns per N tile (multiple of 16, <= 96)
   int stages;
   float im_sign;  // +1 (fprop, bprop) or -1 (accGrad)
+  int ldm;        // output row stride in complex elements (>= m_valid)
 };
 
 constexpr int kGemmThreads = 512;
@@ -272,7 +273,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int m = mt * kTileM + row;
       const bool mok = m < p.m_valid;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + a * (2 * nc);
-      float2* out = reinterpret_cast<float2*>(p.out) + (long long)t * p.n_valid * p.m_valid + m;
+      float2* out = reinterpret_cast<float2*>(p.out) + (long long)t * p.n_valid * p.ldm + m;
       for (int nb = 0; nb < nc; nb += 16) {
         float re[16], im[16];
         tmem_ld_32x32b_x16(tbase + nb, re);
@@ -283,7 +284,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int i = 0; i < 16; ++i) {
           const int n = n0 + i;
           if (mok && n < p.n_valid)
-            out[(long long)n * p.m_valid] = make_float2(re[i], im_sign * im[i]);
+            out[(long long)n * p.ldm] = make_float2(re[i], im_sign * im[i]);
         }
       }
       tc_fence_before();

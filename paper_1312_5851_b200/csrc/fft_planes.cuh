@@ -50,13 +50,12 @@ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
 }
 __device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
 
-// exp(-+2 pi i k / 128) from the constant table (index folds to an immediate
-// constant-bank operand once loops are unrolled).
-template <bool INV>
-__device__ __forceinline__ float2 tw128(int k) {
-  float2 w = c_tw128[k & 127];
-  if (INV) w.y = -w.y;
-  return w;
+// exp(-+2 pi i K / 128), folded at compile time into instruction immediates.
+template <bool INV, int K>
+__device__ __forceinline__ float2 tw128c() {
+  constexpr float re = tw128_re(K);
+  constexpr float im = tw128_im(K);
+  return make_float2(re, INV ? -im : im);
 }
 
 // Compile-time loop: f(std::integral_constant<int, i>) for i in [B, E), so
@@ -77,7 +76,7 @@ __device__ __forceinline__ float2 twiddle_mul(float2 v) {
   } else if constexpr (4 * J == LEN) {  // w = -i (forward) / +i (inverse)
     return INV ? make_float2(-v.y, v.x) : make_float2(v.y, -v.x);
   } else {
-    return cmul(v, tw128<INV>(J * (128 / LEN)));
+    return cmul(v, tw128c<INV, J * (128 / LEN)>());
   }
 }
 
@@ -113,6 +112,9 @@ __device__ __forceinline__ void fft_reg(float2 (&a)[N]) {
   }
 }
 
+template <int N, typename Emit>
+__device__ __forceinline__ void rfft_packed_emit(float2 (&z)[N / 2], Emit&& emit);
+
 // Real-input forward DFT of length N (zero-padded column), emitting the
 // N/2+1 non-redundant outputs X[k] through emit(k, X[k]).  N >= 4 uses the
 // half-length complex FFT on (even, odd) pairs plus the split post-twiddle.
@@ -130,6 +132,17 @@ __device__ __forceinline__ void rfft_emit(const float (&x)[N], Emit&& emit) {
       constexpr int i = decltype(I)::value;
       z[i] = make_float2(x[2 * i], x[2 * i + 1]);
     });
+    rfft_packed_emit<N>(z, emit);
+  }
+}
+
+// rfft_emit with the (even, odd) pairs already packed: z[i] = x[2i] + i x[2i+1]
+// (saves holding the N reals and the N/2 complex values at once).
+template <int N, typename Emit>
+__device__ __forceinline__ void rfft_packed_emit(float2 (&z)[N / 2], Emit&& emit) {
+  static_assert(N >= 4, "rfft_packed_emit");
+  {
+    constexpr int H = N / 2;
     fft_reg<H, false>(z);
     static_for<0, H + 1>([&](auto K) {
       constexpr int k = decltype(K)::value;
@@ -141,7 +154,7 @@ __device__ __forceinline__ void rfft_emit(const float (&x)[N], Emit&& emit) {
       float2 wo;
       if constexpr (k == 0) wo = o;
       else if constexpr (k == H) wo = make_float2(-o.x, -o.y);
-      else wo = cmul(o, tw128<false>(k * (128 / N)));
+      else wo = cmul(o, tw128c<false, k * (128 / N)>());
       emit(k, cadd(e, wo));
     });
   }
@@ -167,7 +180,7 @@ __device__ __forceinline__ void irfft_reg(float2 (&X)[N / 2 + 1], float (&x)[N])
       const float2 xc = cconj(X[H - k]);
       const float2 e = cadd(xk, xc);
       float2 o = csub(xk, xc);
-      if constexpr (k != 0) o = cmul(o, tw128<true>(k * (128 / N)));
+      if constexpr (k != 0) o = cmul(o, tw128c<true, k * (128 / N)>());
       z[k] = make_float2(e.x - o.y, e.y + o.x);  // e + i*o
     });
     fft_reg<H, true>(z);
@@ -222,7 +235,7 @@ __device__ __forceinline__ void irfft_emit(float2 (&X)[N / 2 + 1], Emit&& emit) 
     const float2 xc = cconj(X[H - k]);
     const float2 e = cadd(xk, xc);
     float2 o = csub(xk, xc);
-    if constexpr (k != 0) o = cmul(o, tw128<true>(k * (128 / N)));
+    if constexpr (k != 0) o = cmul(o, tw128c<true, k * (128 / N)>());
     z[k] = make_float2(e.x - o.y, e.y + o.x);  // e + i*o
   });
   fft_reg<H, true>(z);
@@ -353,7 +366,7 @@ __global__ void __launch_bounds__(PlaneTraits<M>::THREADS, PlaneTraits<M>::MIN_C
           z[c] = cadd(a, b);
         } else {
           if constexpr (c == 0) z[c] = csub(a, b);
-          else z[c] = cmul(csub(a, b), tw128<false>(c * (128 / M)));
+          else z[c] = cmul(csub(a, b), tw128c<false, c * (128 / M)>());
         }
       });
     }
@@ -374,6 +387,7 @@ struct C2RParams {
   int cc;       // output columns per CTA chunk
   int ccpad;    // odd smem stride >= cc
   float scale;  // 1 / m^2 (negated to fold a sign flip of the product)
+  int ld;       // row stride of P in complex elements (>= J, even)
 };
 
 // grid = (ceil(J/G), R, ceil(crop/cc)), block = PlaneTraits<M>::THREADS.
@@ -393,8 +407,8 @@ __global__ void __launch_bounds__(PlaneTraits<M>::THREADS, PlaneTraits<M>::MIN_C
   const int ncols = min(p.cc, p.crop - c0);
   const int jvalid = min(G, p.J - j0);
   const int ccpad = p.ccpad;
-  const long long bstride = (long long)p.R * p.J;  // float2 per bin
-  const float2* inbase = reinterpret_cast<const float2*>(p.in) + (long long)r * p.J + j0;
+  const long long bstride = (long long)p.R * p.ld;  // float2 per bin
+  const float2* inbase = reinterpret_cast<const float2*>(p.in) + (long long)r * p.ld + j0;
 
   // Pass 1: per (plane, u[, half]) inverse row FFT over v, keep cropped
   // columns of this chunk.  Lanes = consecutive planes -> 128-B loads.
@@ -419,7 +433,7 @@ __global__ void __launch_bounds__(PlaneTraits<M>::THREADS, PlaneTraits<M>::MIN_C
           z[v] = cadd(a, b);
         } else {
           if constexpr (v == 0) z[v] = csub(a, b);
-          else z[v] = cmul(csub(a, b), tw128<true>(v * (128 / M)));
+          else z[v] = cmul(csub(a, b), tw128c<true, v * (128 / M)>());
         }
       });
     }
@@ -632,7 +646,7 @@ __global__ void __launch_bounds__(WsC2RTraits<M>::THREADS, 1) c2r_ws_kernel(cons
   const int ngj = (p.J + G - 1) / G;
   const int ngroups = p.R * ngj;
   const int crop = p.crop;
-  const long long bstride = (long long)p.R * p.J;  // float2 per bin
+  const long long bstride = (long long)p.R * p.ld;  // float2 per bin
 
   if (threadIdx.x < Tr::P1_THREADS) {
     // ---------------- producers: inverse row FFT over v (lanes = planes)
@@ -645,7 +659,7 @@ __global__ void __launch_bounds__(WsC2RTraits<M>::THREADS, 1) c2r_ws_kernel(cons
       const int r = g / ngj, j0 = (g - r * ngj) * G;
       const bool ld = act && (j0 + jl) < p.J;
       float2 z[M];
-      const float2* srcp = reinterpret_cast<const float2*>(p.in) + (long long)r * p.J + j0 + jl +
+      const float2* srcp = reinterpret_cast<const float2*>(p.in) + (long long)r * p.ld + j0 + jl +
                            (long long)(u * M) * bstride;
 #pragma unroll
       for (int v = 0; v < M; ++v) {
@@ -780,7 +794,7 @@ __global__ void __maxnreg__(96) r2c_ws64_kernel(const R2CPair P) {
             z[cc] = cadd(a0, a1);
           } else {
             if constexpr (cc == 0) z[cc] = csub(a0, a1);
-            else z[cc] = cmul(csub(a0, a1), tw128<false>(cc * 2));
+            else z[cc] = cmul(csub(a0, a1), tw128c<false, cc * 2>());
           }
         });
       }
@@ -809,7 +823,7 @@ __global__ void __maxnreg__(96) c2r_ws64_kernel(const C2RParams p) {
   const int ngj = (p.J + G - 1) / G;
   const int ngroups = p.R * ngj;
   const int crop = p.crop;
-  const long long bstride = (long long)p.R * p.J;  // float2 per bin
+  const long long bstride = (long long)p.R * p.ld;  // float2 per bin
   if (threadIdx.x >= Ws64::COLS_THREADS) {
     // ---------------- producers: (plane, u, half) inverse 64-point row FFT
     const int item = threadIdx.x - Ws64::COLS_THREADS;
@@ -820,7 +834,7 @@ __global__ void __maxnreg__(96) c2r_ws64_kernel(const C2RParams p) {
       const int b = i & 1;
       const int r = g / ngj, j0 = (g - r * ngj) * G;
       const bool ld = act && (j0 + jl) < p.J;
-      const float2* srcp = reinterpret_cast<const float2*>(p.in) + (long long)r * p.J + j0 + jl +
+      const float2* srcp = reinterpret_cast<const float2*>(p.in) + (long long)r * p.ld + j0 + jl +
                            (long long)(u * M) * bstride;
       float2 z[32];
       static_for<0, 32>([&](auto Vv) {
@@ -831,7 +845,7 @@ __global__ void __maxnreg__(96) c2r_ws64_kernel(const C2RParams p) {
           z[v] = cadd(a0, a1);
         } else {
           if constexpr (v == 0) z[v] = csub(a0, a1);
-          else z[v] = cmul(csub(a0, a1), tw128<true>(v * 2));
+          else z[v] = cmul(csub(a0, a1), tw128c<true, v * 2>());
         }
       });
       fft_reg<32, true>(z);

@@ -1,0 +1,519 @@
+// K1 (r2c) and K4 (c2r) plane transforms, TMA-fed (m in {4, 8, 16, 32, 64}).
+//
+// Same maths and frequency layout as fft_planes.cuh (see the header there;
+// reference: detail::r2c_plane / c2r_plane, fft.hpp:160-203, and the
+// bin-major glue of ConvWorkspace, conv_fft.hpp:242-304), re-pipelined for
+// the memory system:
+//
+// * Plane groups (16 planes; 4 at m = 64) stream into a ring of S
+//   shared-memory stages with bulk async copies (cp.async.bulk for the
+//   real planes, cp.async.bulk.tensor for the product spectrum), counted by
+//   transaction bytes on FULL[s].
+// * Two consumer groups ping-pong over the CTA's groups.  Each runs both
+//   1-D passes of its group: pass 1 reads the stage into registers, the
+//   intermediate is written IN PLACE over the stage, pass 2 reads it back.
+//   Once its pass-2 operands are in registers the group itself issues the
+//   copy of the group S ahead into the freed stage (no producer warp).
+// * Column work is packed densely over the src (or crop) non-zero columns
+//   of the valid planes (r2c pass 1, c2r pass 2), so small kernels and
+//   crops leave warps idle instead of running masked FFTs; full planes
+//   (src == m) take a specialised path with constant offsets.
+//
+// Earlier cuts loaded planes straight into registers (one group's loads in
+// flight per CTA; ncu: 27-41% DRAM) or split the passes over separate warp
+// roles (the busier role had too few warps to hide FFT latency).
+#pragma once
+#include <cuda.h>
+
+#include <cstdint>
+
+#include "fft_planes.cuh"
+#include "ptx.cuh"
+
+namespace fcb {
+
+__host__ __device__ constexpr int cmax_i(int a, int b) { return a > b ? a : b; }
+__host__ __device__ constexpr int cmin_i(int a, int b) { return a < b ? a : b; }
+__host__ __device__ constexpr int round_up_i(int a, int b) { return (a + b - 1) / b * b; }
+__host__ __device__ constexpr int ceil32_i(int a) { return (a + 31) / 32 * 32; }
+
+constexpr int kTmaSmemBudget = 220 * 1024;
+// Development switch for bottleneck experiments (default 0 = real kernel):
+// 1 skips the FFT arithmetic, 2 skips the HBM stores, 3 skips the HBM loads,
+// 4 = stores only, 5 = stores only into a group-contiguous layout.
+#ifndef FCB_XFORM_EXP
+#define FCB_XFORM_EXP 0
+#endif
+constexpr int kConsumers = 2;  // consumer groups per CTA (named barriers 1, 2)
+
+// ---------------------------------------------------------------- K1: r2c
+template <int M>
+struct TR2C {
+  static constexpr bool BIG = (M == 64);
+  static constexpr int G = BIG ? 4 : 16;  // planes (K indices) per group
+  static constexpr int PC = M / 2 + 1;
+  static constexpr int CP = M + 1;        // intermediate row stride (float2)
+  // raw plane incl. 16-B alignment slack, in float2
+  static constexpr int RAWF2 = (M * M * 4 + 16 + 7) / 8;
+  static constexpr int PS0 = cmax_i(PC * CP, RAWF2 + 1);
+  // Plane stride (float2).  m <= 32: odd, so the 16 planes a half-warp
+  // reads in pass 2 hit distinct banks.  m = 64: 4 (mod 16), so the
+  // (plane, u) pairs of a warp are spread over the banks.
+  static constexpr int PS = BIG ? PS0 + ((4 - PS0 % 16) + 16) % 16 : (PS0 | 1);
+  static constexpr int STAGE = round_up_i(G * PS * 8 + 8, 128);
+  static constexpr int S = cmin_i(8, kTmaSmemBudget / STAGE);
+  // threads per consumer group = work items per pass (m = 64: one column /
+  // half-row per thread)
+  static constexpr int P1 = BIG ? G * M : G * (M / 2);  // column (pair) items
+  static constexpr int P2 = BIG ? G * PC * 2 : G * PC;  // (plane, u[, half]) row items
+  static constexpr int CT = ceil32_i(cmax_i(P1, P2));   // threads per consumer group
+  static constexpr int THREADS = kConsumers * CT;
+  static constexpr int SMEM = S * STAGE + 2 * S * 8 + 128;
+};
+
+// byte offset of plane jl's raw copy inside a stage (16-B aligned, at or
+// just after the plane's intermediate base jl * PS * 8)
+__device__ __forceinline__ int r2c_raw_off(int jl, int ps) { return (jl * ps * 8 + 15) & ~15; }
+
+struct GroupRef {
+  const R2CParams* p;
+  int r, j0;
+};
+
+template <int G>
+__device__ __forceinline__ GroupRef r2c_group(const R2CPair& P, int ngA, int g) {
+  const int which = g >= ngA;
+  const R2CParams& p = P.op[which];
+  const int gl = g - which * ngA, ngj = p.kpad / G;
+  const int r = gl / ngj;
+  return {&p, r, (gl - r * ngj) * G};
+}
+
+// Stores one spectrum row (bin-major, stride bstride) with the conjugation
+// sign of the operand.
+template <int N>
+__device__ __forceinline__ void store_row(float2* o, long long stride, const float2 (&w)[N], float csign) {
+#pragma unroll
+  for (int v = 0; v < N; ++v) {
+    *o = make_float2(w[v].x, csign * w[v].y);
+    o += stride;
+  }
+}
+
+// grid = persistent (<= groups), block = THREADS, smem = SMEM.
+template <int M>
+__global__ void __launch_bounds__(TR2C<M>::THREADS, 1) r2c_tma_kernel(const __grid_constant__ R2CPair P) {
+  using T = TR2C<M>;
+  constexpr int G = T::G, PC = T::PC, CP = T::CP, PS = T::PS, S = T::S, CT = T::CT;
+  extern __shared__ __align__(128) uint8_t smem[];
+  // FULL[s]: the group's copies landed.  EMPTY[s]: the previous user of the
+  // stage released it.  With two consumers a group's consumer may reach its
+  // FULL wait before the previous use of the stage has even completed; it
+  // waits EMPTY first so the FULL parity it waits on cannot alias.
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * T::STAGE);
+  uint64_t* empty = full + S;
+  const int ngA = P.op[0].R * (P.op[0].kpad / G);
+  const int ngroups = ngA + (P.n > 1 ? P.op[1].R * (P.op[1].kpad / G) : 0);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  pdl_wait();
+  pdl_trigger();
+
+  // copies of this CTA's i-th group into stage i % S (one thread)
+  auto issue = [&](int i) {
+    const int g = blockIdx.x + i * gridDim.x;
+    if (g >= ngroups) return;
+    const uint64_t pol = l2_policy_evict_first();
+    const int s = i % S;
+    const GroupRef q = r2c_group<G>(P, ngA, g);
+    const R2CParams& p = *q.p;
+    const int jv = min(G, p.J - q.j0);  // <= 0: a pure K-padding group
+    const uint32_t pb = (uint32_t)(p.src * p.src) * 4u;
+    const float* base = p.in + (long long)q.r * p.in_sr + (long long)q.j0 * p.in_sj;
+    uint32_t total = 0;
+    const int jv_copy = (FCB_XFORM_EXP == 3 || FCB_XFORM_EXP >= 4) ? 0 : jv;
+    for (int jl = 0; jl < jv_copy; ++jl) {
+      const uintptr_t a = reinterpret_cast<uintptr_t>(base + (long long)jl * p.in_sj);
+      total += ((uint32_t)(a & 15) + pb + 15) & ~15u;
+    }
+    mbar_arrive_expect_tx(&full[s], total);
+    uint8_t* st = smem + s * T::STAGE;
+    for (int jl = 0; jl < jv_copy; ++jl) {
+      // the plane's enclosing 16-B aligned range (planes need not be aligned)
+      const uintptr_t a = reinterpret_cast<uintptr_t>(base + (long long)jl * p.in_sj);
+      const uint32_t sz = ((uint32_t)(a & 15) + pb + 15) & ~15u;
+      bulk_load(st + r2c_raw_off(jl, PS), reinterpret_cast<const void*>(a & ~uintptr_t(15)), sz,
+                &full[s], pol);
+    }
+  };
+  if (threadIdx.x == 0) {
+#pragma unroll 1
+    for (int i = 0; i < S; ++i) issue(i);
+  }
+
+  const int cg = threadIdx.x / CT;  // consumer group
+  const int t = threadIdx.x - cg * CT;
+  const int bar = 1 + cg;
+#pragma unroll 1
+  for (int i = cg;; i += kConsumers) {
+    const int g = blockIdx.x + i * gridDim.x;
+    if (g >= ngroups) break;
+    const int s = i % S;
+    const GroupRef q = r2c_group<G>(P, ngA, g);
+    const R2CParams& p = *q.p;
+    const int src = p.src;
+    const int jv = max(0, min(G, p.J - q.j0));
+    uint8_t* st = smem + s * T::STAGE;
+    if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
+    mbar_wait(&full[s], (i / S) & 1);
+
+    // ---------------- pass 1: real column FFTs over the src non-zero columns
+    // of the valid planes, (plane, column[-pair]) items packed densely.
+    // Each specialisation keeps its own register arrays (a branch that
+    // writes one array from two paths demotes it to local memory).
+    if constexpr (!T::BIG) {
+      // column pairs (c, c + H) packed as one complex FFT
+      const int H = (src + 1) >> 1;
+      const bool act = t < jv * H;
+      const int jl = act ? t / H : 0, c = t - jl * H;
+      const bool hb = c + H < src;
+      const float* pin = p.in + (long long)q.r * p.in_sr + (long long)(q.j0 + jl) * p.in_sj;
+      const float* raw = reinterpret_cast<const float*>(st + r2c_raw_off(jl, PS)) +
+                         ((reinterpret_cast<uintptr_t>(pin) & 15) >> 2) + c;
+      float2* dst = reinterpret_cast<float2*>(st + jl * PS * 8) + c;
+      auto pass1 = [&](auto full_tag) {
+        constexpr bool FULL = decltype(full_tag)::value;
+        float2 z[M];
+#pragma unroll
+        for (int row = 0; row < M; ++row) {
+          if constexpr (FULL) {  // full plane: constant offsets, no predicates
+            z[row].x = act ? raw[row * M] : 0.f;
+            z[row].y = act ? raw[row * M + M / 2] : 0.f;
+          } else {
+            const bool ok = act && row < src;
+            z[row].x = ok ? raw[0] : 0.f;
+            z[row].y = (ok && hb) ? raw[H] : 0.f;
+            raw += src;
+          }
+        }
+        named_bar_sync(bar, CT);  // every raw plane is read: overwrite in place
+        if (act) {
+          if (FCB_XFORM_EXP != 1 && FCB_XFORM_EXP < 4) fft_reg<M, false>(z);
+          static_for<0, PC>([&](auto U) {
+            constexpr int u = decltype(U)::value;
+            const float2 zu = z[u];
+            const float2 zc = cconj(z[(M - u) % M]);
+            dst[u * CP] = make_float2(0.5f * (zu.x + zc.x), 0.5f * (zu.y + zc.y));
+            if (FULL || hb) {
+              const float2 d = csub(zu, zc);
+              dst[u * CP + (FULL ? M / 2 : H)] = make_float2(0.5f * d.y, -0.5f * d.x);  // (zu - zc) / (2i)
+            }
+          });
+        }
+      };
+      if (src == M) pass1(std::true_type{});
+      else pass1(std::false_type{});
+    } else {
+      // m = 64: one real column per thread (half-length complex FFT)
+      const bool act = t < jv * src;
+      const int jl = act ? t / src : 0, c = t - jl * src;
+      const float* pin = p.in + (long long)q.r * p.in_sr + (long long)(q.j0 + jl) * p.in_sj;
+      const float* raw = reinterpret_cast<const float*>(st + r2c_raw_off(jl, PS)) +
+                         ((reinterpret_cast<uintptr_t>(pin) & 15) >> 2) + c;
+      float2* dst = reinterpret_cast<float2*>(st + jl * PS * 8) + c;
+      auto pass1 = [&](auto full_tag) {
+        constexpr bool FULL = decltype(full_tag)::value;
+        float2 z[M / 2];  // (even, odd) rows packed for the half-length FFT
+#pragma unroll
+        for (int i2 = 0; i2 < M / 2; ++i2) {
+          if constexpr (FULL) {
+            z[i2].x = act ? raw[(2 * i2) * M] : 0.f;
+            z[i2].y = act ? raw[(2 * i2 + 1) * M] : 0.f;
+          } else {
+            z[i2].x = (act && 2 * i2 < src) ? raw[(2 * i2) * src] : 0.f;
+            z[i2].y = (act && 2 * i2 + 1 < src) ? raw[(2 * i2 + 1) * src] : 0.f;
+          }
+        }
+        named_bar_sync(bar, CT);  // a plane spans two warps
+        if (act) rfft_packed_emit<M>(z, [&](int u, float2 v) { dst[u * CP] = v; });
+      };
+      if (src == M) pass1(std::true_type{});
+      else pass1(std::false_type{});
+    }
+    named_bar_sync(bar, CT);  // intermediate complete
+
+    // ---------------- pass 2: complex row FFTs -> bin-major HBM
+    const long long bstride = (long long)p.R * p.kpad;  // float2 per bin
+    const float csign = p.conj ? -1.f : 1.f;
+    float2* obase = reinterpret_cast<float2*>(p.out) + (long long)q.r * p.kpad + q.j0;
+    if constexpr (!T::BIG) {
+      const int jl = t % G, u = t / G;
+      const bool act = t < T::P2;
+      const bool valid = act && jl < jv;
+      const float2* row = reinterpret_cast<const float2*>(st + jl * PS * 8) + u * CP;
+      float2* o = obase + jl + (long long)(u * M) * bstride;
+#if FCB_XFORM_EXP == 5
+      o = reinterpret_cast<float2*>(p.out) + (long long)(q.r * (p.kpad / G) + q.j0 / G) * (M * PC * G) + (u * M) * G + jl;
+      const long long bstride_e = G;
+#else
+      const long long bstride_e = bstride;
+#endif
+      auto pass2 = [&](auto full_tag) {
+        constexpr bool FULL = decltype(full_tag)::value;
+        float2 w[M];
+#pragma unroll
+        for (int cc = 0; cc < M; ++cc)
+          w[cc] = (valid && (FULL || cc < src)) ? row[cc] : make_float2(0.f, 0.f);
+        named_bar_sync(bar, CT);  // the stage is free: refill it S groups ahead
+        if (t == 0) {
+          mbar_arrive(&empty[s]);
+          issue(i + S);
+        }
+        if (act) {  // K padding (invalid planes) stores exact zeros
+          if (FCB_XFORM_EXP != 1 && FCB_XFORM_EXP < 4) fft_reg<M, false>(w);
+          if (FCB_XFORM_EXP != 2) store_row<M>(o, bstride_e, w, csign);
+        }
+      };
+      if (src == M) pass2(std::true_type{});
+      else pass2(std::false_type{});
+    } else {
+      // (plane, u, half): one decimation-in-frequency stage splits the
+      // 64-point row FFT into two 32-point halves, outputs v = 2k + h
+      const int jl = t % G, h = (t / G) & 1, u = t / (2 * G);
+      const bool act = t < T::P2;
+      const bool valid = act && jl < jv;
+      const float2* row = reinterpret_cast<const float2*>(st + jl * PS * 8) + u * CP;
+      float2 z[32];
+      static_for<0, 32>([&](auto Cc) {
+        constexpr int cc = decltype(Cc)::value;
+        const float2 a0 = (valid && cc < src) ? row[cc] : make_float2(0.f, 0.f);
+        const float2 a1 = (valid && cc + 32 < src) ? row[cc + 32] : make_float2(0.f, 0.f);
+        const float2 d = csub(a0, a1);
+        if constexpr (cc == 0) z[cc] = h ? d : cadd(a0, a1);
+        else z[cc] = h ? cmul(d, tw128c<false, cc * 2>()) : cadd(a0, a1);
+      });
+      named_bar_sync(bar, CT);
+      if (t == 0) {
+        mbar_arrive(&empty[s]);
+        issue(i + S);
+      }
+      if (act) {
+        fft_reg<32, false>(z);
+        store_row<32>(obase + jl + (long long)(u * M + h) * bstride, 2 * bstride, z, csign);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- K4: c2r
+template <int M>
+struct TC2R {
+  static constexpr bool BIG = (M == 64);
+  static constexpr int G = BIG ? 4 : 16;
+  static constexpr int PC = M / 2 + 1;
+  static constexpr int CP = M + 1;  // intermediate row stride (float2), >= crop
+  static constexpr int PS = BIG ? PC * CP + ((4 - (PC * CP) % 16) + 16) % 16 : ((PC * CP) | 1);
+  // raw u-row stride (float2): one TMA box of M bins x G planes per u row
+  // (tensor-copy destinations must be 128-B aligned, so no bank padding)
+  static constexpr int RS = M * G;
+  static constexpr int RAW = PC * RS * 8;
+  static constexpr int INTER = G * PS * 8;
+  static constexpr int STAGE = round_up_i(cmax_i(RAW, INTER), 128);
+  static constexpr int S = cmin_i(8, kTmaSmemBudget / STAGE);
+  static constexpr int P1 = BIG ? G * PC * 2 : G * PC;  // (plane, u[, half]) row items
+  static constexpr int P2 = BIG ? G * M : G * (M / 2);  // column (pair) items
+  static constexpr int CT = ceil32_i(cmax_i(P1, P2));
+  static constexpr int THREADS = kConsumers * CT;
+  static constexpr int SMEM = S * STAGE + 2 * S * 8 + 128;
+  static constexpr uint32_t BOX_BYTES = 2 * G * 4 * M;  // one u row
+};
+
+// tm: 3-D fp32 map over the product spectrum P[t][r][2*ld] with box
+// {2G floats, 1 row, M bins}.  grid = persistent, groups g = r*ceil(J/G)+jg.
+template <int M>
+__global__ void __launch_bounds__(TC2R<M>::THREADS, 1)
+    c2r_tma_kernel(const __grid_constant__ CUtensorMap tm, const C2RParams p) {
+  using T = TC2R<M>;
+  constexpr int G = T::G, PC = T::PC, CP = T::CP, PS = T::PS, RS = T::RS, S = T::S, CT = T::CT;
+  extern __shared__ __align__(128) uint8_t smem[];
+  // FULL[s]: the group's copies landed.  EMPTY[s]: the previous user of the
+  // stage released it.  With two consumers a group's consumer may reach its
+  // FULL wait before the previous use of the stage has even completed; it
+  // waits EMPTY first so the FULL parity it waits on cannot alias.
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * T::STAGE);
+  uint64_t* empty = full + S;
+  const int ngj = (p.J + G - 1) / G;
+  const int ngroups = p.R * ngj;
+  const int crop = p.crop;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    fence_barrier_init();
+    tma_prefetch_desc(&tm);
+  }
+  __syncthreads();
+  pdl_wait();
+  pdl_trigger();
+
+  auto issue = [&](int i) {
+    const int g = blockIdx.x + i * gridDim.x;
+    if (g >= ngroups) return;
+    const uint64_t pol = l2_policy_evict_first();
+    const int s = i % S;
+    const int r = g / ngj, j0 = (g - r * ngj) * G;
+    mbar_arrive_expect_tx(&full[s], PC * T::BOX_BYTES);
+    uint8_t* st = smem + s * T::STAGE;
+    for (int u = 0; u < PC; ++u) tma_load_3d_hint(st + u * RS * 8, &tm, &full[s], 2 * j0, r, u * M, pol);
+  };
+  if (threadIdx.x == 0) {
+#pragma unroll 1
+    for (int i = 0; i < S; ++i) issue(i);
+  }
+
+  const int cg = threadIdx.x / CT;
+  const int t = threadIdx.x - cg * CT;
+  const int bar = 1 + cg;
+  const float scale = p.scale;
+#pragma unroll 1
+  for (int i = cg;; i += kConsumers) {
+    const int g = blockIdx.x + i * gridDim.x;
+    if (g >= ngroups) break;
+    const int s = i % S;
+    const int r = g / ngj, j0 = (g - r * ngj) * G;
+    const int jv = min(G, p.J - j0);
+    uint8_t* st = smem + s * T::STAGE;
+    const float2* raw = reinterpret_cast<const float2*>(st);
+    float2* inter = reinterpret_cast<float2*>(st);
+    if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
+    mbar_wait(&full[s], (i / S) & 1);
+
+    // ---------------- pass 1: inverse row FFTs over v, cropped columns kept
+    const bool act1 = t < T::P1;
+    if constexpr (!T::BIG) {
+      const int jl = t % G, u = t / G;
+      const float2* src = raw + u * RS + jl;
+      float2 z[M];
+#pragma unroll
+      for (int v = 0; v < M; ++v) z[v] = act1 ? src[v * G] : make_float2(0.f, 0.f);
+      named_bar_sync(bar, CT);  // the whole stage is read: overwrite in place
+      if (act1 && jl < jv) {
+        fft_reg<M, true>(z);
+        float2* dst = inter + jl * PS + u * CP;
+#pragma unroll
+        for (int c = 0; c < M; ++c)
+          if (c < crop) dst[c] = z[c];
+      }
+    } else {
+      const int jl = t % G, h = (t / G) & 1, u = t / (2 * G);
+      const float2* src = raw + u * RS + jl;
+      float2 z[32];
+      static_for<0, 32>([&](auto Vv) {
+        constexpr int v = decltype(Vv)::value;
+        const float2 a0 = act1 ? src[v * G] : make_float2(0.f, 0.f);
+        const float2 a1 = act1 ? src[(v + 32) * G] : make_float2(0.f, 0.f);
+        const float2 d = csub(a0, a1);
+        if constexpr (v == 0) z[v] = h ? d : cadd(a0, a1);
+        else z[v] = h ? cmul(d, tw128c<true, v * 2>()) : cadd(a0, a1);
+      });
+      named_bar_sync(bar, CT);
+      if (act1 && jl < jv) {
+        fft_reg<32, true>(z);
+        float2* dst = inter + jl * PS + u * CP + h;
+#pragma unroll
+        for (int k = 0; k < 32; ++k)
+          if (2 * k + h < crop) dst[2 * k] = z[k];
+      }
+    }
+    named_bar_sync(bar, CT);  // intermediate complete
+
+    // ---------------- pass 2: Hermitian c2r over u -> HBM, (plane, column[-pair])
+    // items packed densely over the valid planes
+    if constexpr (!T::BIG) {
+      // column pairs (c, c + H) packed as one complex inverse FFT
+      const int H = (crop + 1) >> 1;
+      const bool act = t < jv * H;
+      const int jl = act ? t / H : 0, c = t - jl * H;
+      const bool hb = c + H < crop;
+      float2 zz[M];
+      {
+        const float2* col = inter + jl * PS + c;
+        static_for<0, PC>([&](auto U) {
+          constexpr int uu = decltype(U)::value;
+          float2 a = act ? col[uu * CP] : make_float2(0.f, 0.f);
+          float2 b = (act && hb) ? col[uu * CP + H] : make_float2(0.f, 0.f);
+          if constexpr (uu == 0 || 2 * uu == M) {  // c2r ignores these imaginary parts
+            a.y = 0.f;
+            b.y = 0.f;
+          }
+          zz[uu] = make_float2(a.x - b.y, a.y + b.x);  // a + i b
+          if constexpr (uu != 0 && 2 * uu != M) zz[M - uu] = make_float2(a.x + b.y, b.x - a.y);
+        });
+      }
+      named_bar_sync(bar, CT);  // the stage is free: refill it S groups ahead
+      if (t == 0) {
+        mbar_arrive(&empty[s]);
+        issue(i + S);
+      }
+      if (act) {
+        fft_reg<M, true>(zz);
+        float* dst = p.out + (long long)r * p.out_sr + (long long)(j0 + jl) * p.out_sj + c;
+#pragma unroll
+        for (int row = 0; row < M; ++row) {
+          if (row < crop) {
+            dst[0] = zz[row].x * scale;
+            if (hb) dst[H] = zz[row].y * scale;
+            dst += crop;
+          }
+        }
+      }
+    } else {
+      // one Hermitian column per thread: the half-length pre-twiddle is
+      // formed straight from shared memory (X[k], X[H-k] pairs), so the
+      // 33-entry column is never held whole in registers
+      const bool act = t < jv * crop;
+      const int jl = act ? t / crop : 0, c = t - jl * crop;
+      constexpr int H = M / 2;
+      float2 z[H];
+      {
+        const float2* col = inter + jl * PS + c;
+        static_for<0, H>([&](auto K) {
+          constexpr int k = decltype(K)::value;
+          float2 xk = act ? col[k * CP] : make_float2(0.f, 0.f);
+          float2 xc = cconj(act ? col[(H - k) * CP] : make_float2(0.f, 0.f));
+          if constexpr (k == 0) {  // c2r ignores Im X[0] and Im X[H]
+            xk.y = 0.f;
+            xc.y = 0.f;
+          }
+          const float2 e = cadd(xk, xc);
+          float2 o = csub(xk, xc);
+          if constexpr (k != 0) o = cmul(o, tw128c<true, k * (128 / M)>());
+          z[k] = make_float2(e.x - o.y, e.y + o.x);  // e + i*o
+        });
+      }
+      named_bar_sync(bar, CT);
+      if (t == 0) {
+        mbar_arrive(&empty[s]);
+        issue(i + S);
+      }
+      if (act) {
+        fft_reg<H, true>(z);
+        float* dst = p.out + (long long)r * p.out_sr + (long long)(j0 + jl) * p.out_sj + c;
+#pragma unroll
+        for (int i2 = 0; i2 < H; ++i2) {
+          if (2 * i2 < crop) dst[(2 * i2) * crop] = z[i2].x * scale;
+          if (2 * i2 + 1 < crop) dst[(2 * i2 + 1) * crop] = z[i2].y * scale;
+        }
+      }
+    }
+  }
+}
+
+}  // namespace fcb

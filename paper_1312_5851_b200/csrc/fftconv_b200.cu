@@ -25,6 +25,7 @@
 #include "../../include/fftconv_b200.h"
 #include "cgemm_tcgen05.cuh"
 #include "fft_planes.cuh"
+#include "fft_tma.cuh"
 
 namespace fcb {
 
@@ -71,11 +72,14 @@ static PassNeed pass_need(Pass pass, size_t S, size_t f, size_t fo, size_t m) {
   const size_t bins = m * (m / 2 + 1);
   switch (pass) {
     case kFprop:
-      return {bins * S * 2 * round_up(f, 16), bins * fo * 2 * round_up(f, 16), bins * fo * 2 * S};
+      return {bins * S * 2 * round_up(f, 16), bins * fo * 2 * round_up(f, 16),
+              bins * fo * 2 * round_up(S, 2)};
     case kBprop:
-      return {bins * S * 2 * round_up(fo, 16), bins * f * 2 * round_up(fo, 16), bins * f * 2 * S};
+      return {bins * S * 2 * round_up(fo, 16), bins * f * 2 * round_up(fo, 16),
+              bins * f * 2 * round_up(S, 2)};
     default:
-      return {bins * fo * 2 * round_up(S, 16), bins * f * 2 * round_up(S, 16), bins * f * 2 * fo};
+      return {bins * fo * 2 * round_up(S, 16), bins * f * 2 * round_up(S, 16),
+              bins * f * 2 * round_up(fo, 2)};
   }
 }
 
@@ -185,7 +189,9 @@ static void launch_r2c_legacy(const R2CParams& p, cudaStream_t st) {
 
 // Warp-specialised kernels: m in {4..32}, or m = 64 with planes wider than
 // 32 (kernels at m = 64 keep 16-plane groups so every store is a full line).
+static bool legacy_xform();
 static bool r2c_ws_capable(size_t m, const R2CParams& p) {
+  if (!legacy_xform()) return m >= 4 && m <= 64;
   return (m >= 4 && m <= 32) || (m == 64 && p.src > 32);
 }
 
@@ -208,7 +214,37 @@ static void launch_r2c_ws64(const R2CPair& P, const DevInfo& di, cudaStream_t st
   launch_pdl(r2c_ws64_kernel, dim3(grid), dim3(Ws64::THREADS), Ws64::SMEM, st, P);
 }
 
+// TMA-fed transforms (fft_tma.cuh) for m in {4..64}; FFTCONV_B200_LEGACY_XFORM=1
+// selects the first-cut register-fed kernels (A/B measurements only).
+static bool legacy_xform() {
+  static const bool v = [] {
+    const char* e = getenv("FFTCONV_B200_LEGACY_XFORM");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
+template <int M>
+static void launch_r2c_tma(const R2CPair& P, const DevInfo& di, cudaStream_t st) {
+  using T = TR2C<M>;
+  auto kern = r2c_tma_kernel<M>;
+  smem_optin(kern, T::SMEM);
+  int groups = 0;
+  for (int i = 0; i < P.n; ++i) groups += P.op[i].R * (P.op[i].kpad / T::G);
+  const int grid = std::max(1, std::min(groups, di.sms));
+  launch_pdl(kern, dim3(grid), dim3(T::THREADS), T::SMEM, st, P);
+}
+
 static void launch_r2c_group(size_t m, const R2CPair& P, cudaStream_t st, const DevInfo& di) {
+  if (!legacy_xform()) {
+    switch (m) {
+      case 4: return launch_r2c_tma<4>(P, di, st);
+      case 8: return launch_r2c_tma<8>(P, di, st);
+      case 16: return launch_r2c_tma<16>(P, di, st);
+      case 32: return launch_r2c_tma<32>(P, di, st);
+      case 64: return launch_r2c_tma<64>(P, di, st);
+    }
+  }
   switch (m) {
     case 4: return launch_r2c_ws<4>(P, di, st);
     case 8: return launch_r2c_ws<8>(P, di, st);
@@ -276,7 +312,45 @@ static void launch_c2r_ws(const C2RParams& p, const DevInfo& di, cudaStream_t st
   launch_pdl(kern, dim3(grid), dim3(Tr::THREADS), Tr::SMEM, st, p);
 }
 
+// 3-D fp32 map over P[t][R][2*ld]; box {2G floats, 1, m bins} = one u row.
+static CUtensorMap make_spectrum_map(const float* base, size_t ld, size_t R, size_t bins,
+                                     uint32_t g, uint32_t m) {
+  CUtensorMap t;
+  const cuuint64_t dims[3] = {2 * ld, R, bins};
+  const cuuint64_t strides[2] = {2 * ld * sizeof(float), R * 2 * ld * sizeof(float)};
+  const cuuint32_t box[3] = {2 * g, 1, m};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&t, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw Error(FFTCONV_B200_CUDA_ERROR, "cuTensorMapEncodeTiled (spectrum) failed: " + std::to_string(r));
+  return t;
+}
+
+template <int M>
+static void launch_c2r_tma(const C2RParams& p, const DevInfo& di, cudaStream_t st) {
+  using T = TC2R<M>;
+  auto kern = c2r_tma_kernel<M>;
+  smem_optin(kern, T::SMEM);
+  const size_t bins = (size_t)M * (M / 2 + 1);
+  const CUtensorMap tm = make_spectrum_map(p.in, p.ld, p.R, bins, T::G, M);
+  const int groups = p.R * ((p.J + T::G - 1) / T::G);
+  const int grid = std::max(1, std::min(groups, di.sms));
+  launch_pdl(kern, dim3(grid), dim3(T::THREADS), T::SMEM, st, tm, p);
+}
+
 static void launch_c2r(size_t m, const C2RParams& p, cudaStream_t st, const DevInfo& di) {
+  if (!legacy_xform()) {
+    switch (m) {
+      case 4: return launch_c2r_tma<4>(p, di, st);
+      case 8: return launch_c2r_tma<8>(p, di, st);
+      case 16: return launch_c2r_tma<16>(p, di, st);
+      case 32: return launch_c2r_tma<32>(p, di, st);
+      case 64: return launch_c2r_tma<64>(p, di, st);
+    }
+  }
   switch (m) {
     case 4: return launch_c2r_ws<4>(p, di, st);
     case 8: return launch_c2r_ws<8>(p, di, st);
@@ -327,7 +401,7 @@ static GemmGeom gemm_geom(size_t M, size_t N, const DevInfo& di) {
 // D[t] = A[t] . conj(B[t])^T per bin; im_sign = -1 returns conj(D) (the
 // accGrad orientation, conj(A) . B).  A: F[t][M][2*kpad], B: F[t][N][2*kpad].
 static void launch_gemm(const float* A, const float* B, float* out, size_t bins, size_t M,
-                        size_t N, size_t kpad, float im_sign, const DevInfo& di,
+                        size_t N, size_t kpad, float im_sign, size_t ldm, const DevInfo& di,
                         cudaStream_t st) {
   const GemmGeom g = gemm_geom(M, N, di);
   CUtensorMap ta = make_operand_map(A, kpad, M, bins, kTileM);
@@ -343,6 +417,7 @@ static void launch_gemm(const float* A, const float* B, float* out, size_t bins,
   p.nc = g.nc;
   p.stages = g.stages;
   p.im_sign = im_sign;
+  p.ldm = (int)ldm;
   smem_optin(cgemm_bins_tcgen05, (int)g.smem);
   const long long tiles = (long long)bins * g.m_tiles * g.n_tiles;
   const int grid = (int)std::min<long long>(tiles, di.sms);
@@ -502,10 +577,10 @@ void run_forward(fftconv_b200_ws* ws, const float* x, size_t S, size_t f, size_t
   const int nl = launch_r2c_both(m, a, b, st, ws->di);
   record(ws, 1, st);  // both forward transforms
   record(ws, 2, st);
-  launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, S, fo, kp, 1.0f, ws->di, st);
+  launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, S, fo, kp, 1.0f, round_up(S, 2), ws->di, st);
   record(ws, 3, st);
   C2RParams c{ws->bufD, y, (long long)(no * no), (long long)(fo * no * no), (int)fo, (int)S,
-              (int)no, 0, 0, 1.0f / (float)(m * m)};
+              (int)no, 0, 0, 1.0f / (float)(m * m), (int)round_up(S, 2)};
   launch_c2r(m, c, st, ws->di);
   record(ws, 4, st);
   ws->last_launches = nl + 2;
@@ -537,10 +612,10 @@ void run_grad_input(fftconv_b200_ws* ws, const float* gy, size_t S, size_t fo, s
   const int nl = launch_r2c_both(m, a, b, st, ws->di);
   record(ws, 1, st);  // both forward transforms
   record(ws, 2, st);
-  launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, S, f, kp, 1.0f, ws->di, st);
+  launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, S, f, kp, 1.0f, round_up(S, 2), ws->di, st);
   record(ws, 3, st);
   C2RParams c{ws->bufD, gx, (long long)(n * n), (long long)(f * n * n), (int)f, (int)S, (int)n,
-              0, 0, 1.0f / (float)(m * m)};
+              0, 0, 1.0f / (float)(m * m), (int)round_up(S, 2)};
   launch_c2r(m, c, st, ws->di);
   record(ws, 4, st);
   ws->last_launches = nl + 2;
@@ -574,10 +649,10 @@ void run_grad_weight(fftconv_b200_ws* ws, const float* gy, size_t Sg, size_t fo,
   const int nl = launch_r2c_both(m, a, b, st, ws->di);
   record(ws, 1, st);  // both forward transforms
   record(ws, 2, st);
-  launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, fo, f, kp, -1.0f, ws->di, st);
+  launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, fo, f, kp, -1.0f, round_up(fo, 2), ws->di, st);
   record(ws, 3, st);
   C2RParams c{ws->bufD, gw, (long long)(k * k), (long long)(f * k * k), (int)f, (int)fo, (int)k,
-              0, 0, 1.0f / (float)(m * m)};
+              0, 0, 1.0f / (float)(m * m), (int)round_up(fo, 2)};
   launch_c2r(m, c, st, ws->di);
   record(ws, 4, st);
   ws->last_launches = nl + 2;
@@ -842,15 +917,15 @@ int fftconv_b200_debug_c2r(const float* in, size_t planes, size_t m, size_t crop
   return guarded(nullptr, [&] {
     if ((m & (m - 1)) || crop > m) throw Error(FFTCONV_B200_PLAN_ERROR, "debug_c2r: bad m");
     // in[p][t] -> P[t][0][p] (R = 1, J = planes)
-    const size_t bins = m * (m / 2 + 1);
+    const size_t bins = m * (m / 2 + 1), ld = round_up(planes, 2);
     float* P = nullptr;
-    FCB_CUDA(cudaMalloc(&P, bins * planes * 2 * sizeof(float)));
+    FCB_CUDA(cudaMalloc(&P, bins * ld * 2 * sizeof(float)));
     for (size_t pl = 0; pl < planes; ++pl)
-      FCB_CUDA(cudaMemcpy2DAsync(P + pl * 2, planes * 2 * sizeof(float), in + pl * bins * 2,
+      FCB_CUDA(cudaMemcpy2DAsync(P + pl * 2, ld * 2 * sizeof(float), in + pl * bins * 2,
                                  2 * sizeof(float), 2 * sizeof(float), bins,
                                  cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
     C2RParams p{P, out, 0, (long long)(crop * crop), 1, (int)planes, (int)crop, 0, 0,
-                1.0f / (float)(m * m)};
+                1.0f / (float)(m * m), (int)round_up(planes, 2)};
     launch_c2r(m, p, (cudaStream_t)stream, dev_info(0));
     FCB_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
     cudaFree(P);
@@ -878,7 +953,7 @@ int fftconv_b200_debug_cgemm(const float* a, const float* b, float* out, size_t 
     if (mode == 1)  // A . B = A . conj(conj(B))
       conj_inplace_kernel<<<256, 256, 0, st>>>(reinterpret_cast<float2*>(B),
                                                (long long)(bins * N * kp));
-    launch_gemm(A, B, out, bins, M, N, kp, mode == 2 ? -1.0f : 1.0f, di, st);
+    launch_gemm(A, B, out, bins, M, N, kp, mode == 2 ? -1.0f : 1.0f, M, di, st);
     FCB_CUDA(cudaStreamSynchronize(st));
     cudaFree(A);
     cudaFree(B);

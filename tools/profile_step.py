@@ -1,6 +1,9 @@
-"""Minimal driver for ncu: `reps` x (fprop, bprop, accGrad) of one layer on
-cuda:0 through the product path, nothing else on the GPU.  Never used for
-reported numbers (a number printed under a profiler is not a measurement)."""
+"""Runs the three operators of one layer `--reps` times (no timing) so ncu
+can capture their kernels.  Development tool:
+
+  ncu --set full --clock-control none --import-source on -k regex:'r2c|cgemm|c2r' \
+      -s <skip> -c <count> -o gpurun_out/prof python tools/profile_step.py --config paper
+"""
 import argparse
 import os
 import sys
@@ -8,7 +11,6 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import bench  # noqa: E402
@@ -29,14 +31,12 @@ def main():
     w = torch.from_numpy(fill_uniform((fo, f, k, k), 1234, 2)).to(dev)
     gy = torch.from_numpy(fill_uniform((S, fo, no, no), 1234, 3)).to(dev)
     ws = ConvWorkspace([LayerConfig(k, n, f, fo, S)], device=0)
-    ops = a.ops.split(",")
+    ops = {"forward": lambda: ws.forward(x, w), "grad_input": lambda: ws.grad_input(gy, w),
+           "grad_weight": lambda: ws.grad_weight(gy, x)}
+    sel = a.ops.split(",")
     for _ in range(a.reps):
-        if "forward" in ops:
-            ws.forward(x, w)
-        if "grad_input" in ops:
-            ws.grad_input(gy, w)
-        if "grad_weight" in ops:
-            ws.grad_weight(gy, x)
+        for name in sel:
+            ops[name]()
     torch.cuda.synchronize()
 
 

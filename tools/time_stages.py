@@ -20,8 +20,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="paper")
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--S", type=int, default=0, help="override the batch")
     a = ap.parse_args()
     (k, n, f, fo, S), label = bench.parse_config(a.config)
+    S = a.S or S
     no = n - k + 1
     dev = torch.device("cuda:0")
     x = torch.from_numpy(fill_uniform((S, f, n, n), 1234, 1)).to(dev)
@@ -43,7 +45,7 @@ def main():
             st.append(ws.stage_ms())
         out[name] = [round(statistics.median(v[i] for v in st) * 1000, 2) for i in range(4)]
     out["total_us"] = round(sum(sum(v) for v in out.values()), 1)
-    print(json.dumps({"config": a.config, "dbg": os.environ.get("FFTCONV_B200_GEMM_DEBUG", "0"),
+    print(json.dumps({"config": a.config, "S": S, "dbg": os.environ.get("FFTCONV_B200_GEMM_DEBUG", "0"),
                       "stage_us[r2cA,r2cB,gemm,c2r]": out}))
 
 
