@@ -29,14 +29,23 @@
 //
 // Pipeline (one CTA per SM, persistent over tiles (t, m-tile, n-tile)):
 //   warp 0      TMA: raw fp32 A (128 x 32) and B (Nc x 32) per K chunk of
-//               16 complex; 128-B swizzle; OOB rows/cols zero-filled
-//   warps 4-7   A converters (thread = row): smem -> regs -> TMEM hi/lo
-//   warps 8-11  B converters: im rows + lo rows in smem, fence.proxy.async
+//               16 complex into a ring of raw stages; 128-B swizzle; OOB
+//               rows/cols zero-filled
+//   warps 4-7   A converters (thread = row): raw stage -> regs -> TMEM hi/lo
+//   warps 8-11  B converters: raw stage -> one of two converted-B buffers
+//               (re = raw, im rows, lo rows, lo-im rows), fence.proxy.async
 //   warp 1      MMA issuer (one thread): 4 K-steps x 3 UMMA (M=128,
 //               N=2Nc, K=8) per chunk, double-buffered TMEM accumulator
-//   warps 12-15 epilogue: tcgen05.ld -> float2 (re, im) stores into the
-//               product spectrum P[t][n][m] (lanes = consecutive m rows)
+//   warps 12-19 epilogue: tcgen05.ld -> float2 (re, im) stores into the
+//               product spectrum P[t][n][m] (lanes = consecutive m rows);
+//               two warps per TMEM lane quadrant split the 16-column blocks
+//               (a tile's 98 KB of stores from 4 warps took longer than its
+//               MMAs and stalled the accumulator double buffer)
 //   warp 2      TMEM allocator
+// Both converter groups release a raw stage as soon as they have read it,
+// so the TMA runs up to RS chunks ahead of the MMAs (the first cut held each
+// stage until its MMAs retired, which capped the loads in flight at ~2
+// chunks and left the tensor pipe ~50% idle at the paper point).
 #pragma once
 #include <cuda.h>
 
@@ -59,13 +68,30 @@ struct GemmParams {
   int ldm;        // output row stride in complex elements (>= m_valid)
 };
 
-constexpr int kGemmThreads = 512;
+constexpr int kGemmThreads = 640;
 constexpr int kTileM = 128;
 constexpr int kChunkBytesA = kTileM * 128;  // 128 rows x 128 B (32 fp32)
 constexpr int kMaxNc = 96;                  // TMEM: 2 x 2*96 accumulator + 2 x 64 A columns
 
-__host__ __device__ inline int gemm_stage_bytes(int nc) {
-  return kChunkBytesA + 4 * nc * 128;  // raw A | B hi (re, im rows) | B lo (re, im rows)
+// FCB_GEMM_TRACE: per-chunk clock64 timeline of CTA 0, printed at exit
+// (development builds only).
+#ifdef FCB_GEMM_TRACE
+__device__ long long g_gemm_trace[6][64];
+#define GTRACE(ev, idx)                                                      \
+  do {                                                                       \
+    if (blockIdx.x == 0 && (idx) < 64) g_gemm_trace[ev][idx] = clock64();    \
+  } while (0)
+#else
+#define GTRACE(ev, idx) \
+  do {                  \
+  } while (0)
+#endif
+
+__host__ __device__ inline int gemm_raw_stage_bytes(int nc) {
+  return kChunkBytesA + nc * 128;  // raw A | raw B
+}
+__host__ __device__ inline int gemm_bbuf_bytes(int nc) {
+  return 4 * nc * 128;  // B re (= raw) | B im | B lo re | B lo im
 }
 
 __global__ void __launch_bounds__(kGemmThreads, 1)
@@ -76,18 +102,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   // pointer so the converters' accesses compile to LDS/STS.
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int nc = p.nc;
-  const int S = p.stages;
+  const int RS = p.stages;  // raw stages
   const int rowsB = nc * 128;  // bytes of nc rows
-  const int stageBytes = gemm_stage_bytes(nc);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * stageBytes);
-  uint64_t* full = bars;              // TMA -> converters           [S]
-  uint64_t* aready = bars + S;        // A converters -> MMA         [S]
-  uint64_t* bready = bars + 2 * S;    // B converters -> MMA         [S]
-  uint64_t* empty = bars + 3 * S;     // MMA -> TMA                  [S]
-  uint64_t* atfree = bars + 4 * S;    // MMA -> A converters (TMEM)  [2]
-  uint64_t* tfull = bars + 4 * S + 2;   // MMA -> epilogue           [2]
-  uint64_t* tempty = bars + 4 * S + 4;  // epilogue -> MMA           [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 * S + 6);
+  const int rawBytes = gemm_raw_stage_bytes(nc);
+  uint8_t* bbuf0 = smem + RS * rawBytes;  // 2 converted-B buffers
+  const int bbufBytes = gemm_bbuf_bytes(nc);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(bbuf0 + 2 * bbufBytes);
+  uint64_t* rfull = bars;               // TMA -> converters          [RS]
+  uint64_t* rempty = bars + RS;         // converters -> TMA          [RS]
+  uint64_t* aready = bars + 2 * RS;     // A converters -> MMA        [2]
+  uint64_t* bready = aready + 2;        // B converters -> MMA        [2]
+  uint64_t* atfree = bready + 2;        // MMA -> A converters (TMEM) [2]
+  uint64_t* bfree = atfree + 2;         // MMA -> B converters (smem) [2]
+  uint64_t* tfull = bfree + 2;          // MMA -> epilogue            [2]
+  uint64_t* tempty = tfull + 2;         // epilogue -> MMA            [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -95,16 +124,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t a_col0 = 4 * nc;  // A staging: 2 buffers x (32 hi + 32 lo) columns
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&aready[s], 128);
-      mbar_init(&bready[s], 128);
-      mbar_init(&empty[s], 1);
+    for (int s = 0; s < RS; ++s) {
+      mbar_init(&rfull[s], 1);
+      mbar_init(&rempty[s], 256);  // every A and B converter thread
     }
     for (int a = 0; a < 2; ++a) {
+      mbar_init(&aready[a], 128);
+      mbar_init(&bready[a], 128);
       mbar_init(&atfree[a], 1);
+      mbar_init(&bfree[a], 1);
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], 256);
     }
     fence_barrier_init();
   }
@@ -130,41 +160,28 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       int s = 0;
       uint32_t ph = 0;
       const uint32_t tx = kChunkBytesA + rowsB;
-      // L2 prefetch runs kPrefetch chunks ahead of the smem ring, so more
-      // bytes are in flight than the stages alone can hold.
-      constexpr int kPrefetch = 6;
-      int pf_tile = blockIdx.x, pf_kc = 0;
-      auto prefetch_next = [&]() {
-        if (pf_tile >= total_tiles) return;
-        const int t = pf_tile / tiles_per_bin;
-        const int rem = pf_tile - t * tiles_per_bin;
-        const int mt = rem / p.n_tiles, nt = rem - mt * p.n_tiles;
-        tma_prefetch_l2_3d(&tmA, pf_kc * 32, mt * kTileM, t);
-        tma_prefetch_l2_3d(&tmB, pf_kc * 32, nt * nc, t);
-        if (++pf_kc == kc_n) { pf_kc = 0; pf_tile += gridDim.x; }
-      };
-      for (int i = 0; i < kPrefetch; ++i) prefetch_next();
+      int gi = 0;
+      (void)gi;
       for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
         const int t = tile / tiles_per_bin;
         const int rem = tile - t * tiles_per_bin;
         const int mt = rem / p.n_tiles, nt = rem - mt * p.n_tiles;
         for (int kc = 0; kc < kc_n; ++kc) {
-          prefetch_next();
-          mbar_wait(&empty[s], ph ^ 1);
-          uint8_t* st = smem + s * stageBytes;
-          mbar_arrive_expect_tx(&full[s], tx);
-          tma_load_3d(st, &tmA, &full[s], kc * 32, mt * kTileM, t);
-          tma_load_3d(st + kChunkBytesA, &tmB, &full[s], kc * 32, nt * nc, t);
-          if (++s == S) { s = 0; ph ^= 1; }
+          mbar_wait(&rempty[s], ph ^ 1);
+          GTRACE(0, gi);
+          ++gi;
+          uint8_t* st = smem + s * rawBytes;
+          mbar_arrive_expect_tx(&rfull[s], tx);
+          tma_load_3d(st, &tmA, &rfull[s], kc * 32, mt * kTileM, t);
+          tma_load_3d(st + kChunkBytesA, &tmB, &rfull[s], kc * 32, nt * nc, t);
+          if (++s == RS) { s = 0; ph ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
     const uint32_t idesc = umma_idesc_tf32(kTileM, 2 * nc);
-    int s = 0;
-    uint32_t ph = 0;
-    uint32_t g = 0;  // global chunk counter (TMEM A buffer = g & 1)
+    uint32_t g = 0;  // global chunk counter (TMEM A buffer / B buffer = g & 1)
     int local = 0;
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++local) {
       const int a = local & 1;
@@ -172,13 +189,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + a * (2 * nc);
       for (int kc = 0; kc < kc_n; ++kc, ++g) {
-        mbar_wait(&aready[s], ph);
-        mbar_wait(&bready[s], ph);
+        const int b = g & 1;
+        mbar_wait(&aready[b], (g >> 1) & 1);
+        mbar_wait(&bready[b], (g >> 1) & 1);
         tc_fence_after();
+        if (lane == 0) GTRACE(4, g);
         if (lane == 0) {
-          const uint32_t a_hi = tmem_base + a_col0 + (g & 1) * 64;
+          const uint32_t a_hi = tmem_base + a_col0 + b * 64;
           const uint32_t a_lo = a_hi + 32;
-          const uint32_t b_hi = smem_u32(smem + s * stageBytes + kChunkBytesA);
+          const uint32_t b_hi = smem_u32(bbuf0 + b * bbufBytes);
           const uint32_t b_lo = b_hi + 2 * rowsB;
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
@@ -188,16 +207,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             umma_tf32_ts(d_tmem, a_hi + kk * 8, dbl, idesc, 1u);
             umma_tf32_ts(d_tmem, a_lo + kk * 8, dbh, idesc, 1u);
           }
-          umma_commit(&empty[s]);
-          umma_commit(&atfree[g & 1]);
+          umma_commit(&atfree[b]);
+          umma_commit(&bfree[b]);
           if (kc == kc_n - 1) umma_commit(&tfull[a]);
         }
         __syncwarp();
-        if (++s == S) { s = 0; ph ^= 1; }
       }
     }
   } else if (warp >= 4 && warp < 8) {
-    // ------------------------------------------------ A converters: smem -> TMEM hi/lo
+    // ------------------------------------------------ A converters: raw -> TMEM hi/lo
     const int q = warp & 3;        // TMEM lane quadrant of this warp
     const int m = q * 32 + lane;   // A row
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
@@ -206,8 +224,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint32_t g = 0;
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
       for (int kc = 0; kc < kc_n; ++kc, ++g) {
-        mbar_wait(&full[s], ph);
-        const uint8_t* arow = smem + s * stageBytes + (m >> 3) * 1024 + (m & 7) * 128;
+        mbar_wait(&rfull[s], ph);
+        if (threadIdx.x == 128) GTRACE(1, g);
+        const uint8_t* arow = smem + s * rawBytes + (m >> 3) * 1024 + (m & 7) * 128;
         float x[32], lo[32];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {  // 16-B chunk c of the row sits at c ^ (m & 7)
@@ -217,6 +236,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           x[4 * c + 2] = v.z;
           x[4 * c + 3] = v.w;
         }
+        mbar_arrive(&rempty[s]);  // raw A read: the TMA may refill the stage
 #pragma unroll
         for (int i = 0; i < 32; ++i) lo[i] = tf32_lo(x[i]);
         mbar_wait(&atfree[g & 1], ((g >> 1) & 1) ^ 1);  // MMAs of chunk g-2 done with it
@@ -226,40 +246,55 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tmem_st_32x32b_x32(ta + 32, lo);
         tmem_st_wait();
         tc_fence_before();
-        mbar_arrive(&aready[s]);
-        if (++s == S) { s = 0; ph ^= 1; }
+        mbar_arrive(&aready[g & 1]);
+        if (threadIdx.x == 128) GTRACE(2, g);
+        if (++s == RS) { s = 0; ph ^= 1; }
       }
     }
   } else if (warp >= 8 && warp < 12) {
-    // ------------------------------------------------ B converters: im rows, lo rows
+    // ------------------------------------------------ B converters: raw -> re, im, lo, lo-im
     const int ct = threadIdx.x - 256;  // 0..127
     const int nb = nc * 8;             // float4 per raw B tile
     int s = 0;
     uint32_t ph = 0;
+    uint32_t g = 0;
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-      for (int kc = 0; kc < kc_n; ++kc) {
-        mbar_wait(&full[s], ph);
-        uint8_t* bh = smem + s * stageBytes + kChunkBytesA;
-        const float4* bre = reinterpret_cast<const float4*>(bh);
-        float4* bim = reinterpret_cast<float4*>(bh + rowsB);
-        float4* blr = reinterpret_cast<float4*>(bh + 2 * rowsB);
-        float4* bli = reinterpret_cast<float4*>(bh + 3 * rowsB);
-#pragma unroll 3
-        for (int i = ct; i < nb; i += 128) {
-          const float4 v = bre[i];  // (p0, q0, p1, q1): re rows are the raw rows
-          bim[i] = make_float4(-v.y, v.x, -v.w, v.z);
-          const float4 l = make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
-          blr[i] = l;
-          bli[i] = make_float4(-l.y, l.x, -l.w, l.z);
+      for (int kc = 0; kc < kc_n; ++kc, ++g) {
+        mbar_wait(&rfull[s], ph);
+        const float4* braw = reinterpret_cast<const float4*>(smem + s * rawBytes + kChunkBytesA);
+        float4 v[6];  // nb / 128 <= 6 (nc <= 96)
+#pragma unroll
+        for (int k = 0; k < 6; ++k)
+          if (ct + k * 128 < nb) v[k] = braw[ct + k * 128];
+        mbar_arrive(&rempty[s]);
+        mbar_wait(&bfree[g & 1], ((g >> 1) & 1) ^ 1);  // MMAs of chunk g-2 done with it
+        uint8_t* bb = bbuf0 + (g & 1) * bbufBytes;
+        float4* bre = reinterpret_cast<float4*>(bb);
+        float4* bim = reinterpret_cast<float4*>(bb + rowsB);
+        float4* blr = reinterpret_cast<float4*>(bb + 2 * rowsB);
+        float4* bli = reinterpret_cast<float4*>(bb + 3 * rowsB);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+          const int i = ct + k * 128;
+          if (i < nb) {
+            const float4 w = v[k];  // (p0, q0, p1, q1): re rows are the raw rows
+            bre[i] = w;
+            bim[i] = make_float4(-w.y, w.x, -w.w, w.z);
+            const float4 l = make_float4(tf32_lo(w.x), tf32_lo(w.y), tf32_lo(w.z), tf32_lo(w.w));
+            blr[i] = l;
+            bli[i] = make_float4(-l.y, l.x, -l.w, l.z);
+          }
         }
         fence_proxy_async_smem();
-        mbar_arrive(&bready[s]);
-        if (++s == S) { s = 0; ph ^= 1; }
+        mbar_arrive(&bready[g & 1]);
+        if (threadIdx.x == 256) GTRACE(3, g);
+        if (++s == RS) { s = 0; ph ^= 1; }
       }
     }
   } else if (warp >= 12) {
     // ------------------------------------------------ epilogue
-    const int q = warp & 3;
+    const int q = warp & 3;              // TMEM lane quadrant
+    const int half = (warp - 12) >> 2;   // which 16-column blocks
     const int row = q * 32 + lane;
     const float im_sign = p.im_sign;
     int local = 0;
@@ -274,7 +309,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const bool mok = m < p.m_valid;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + a * (2 * nc);
       float2* out = reinterpret_cast<float2*>(p.out) + (long long)t * p.n_valid * p.ldm + m;
-      for (int nb = 0; nb < nc; nb += 16) {
+      for (int nb = half * 16; nb < nc; nb += 32) {
         float re[16], im[16];
         tmem_ld_32x32b_x16(tbase + nb, re);
         tmem_ld_32x32b_x16(tbase + nc + nb, im);
@@ -289,6 +324,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(&tempty[a]);
+      if (threadIdx.x == 384) GTRACE(5, local);  // first epilogue warp
     }
   }
 
@@ -297,6 +333,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tc_fence_after();
     tmem_dealloc(tmem_base, kTmemCols);
   }
+#ifdef FCB_GEMM_TRACE
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const long long t0 = g_gemm_trace[0][0];
+    for (int i = 0; i < 30; ++i)
+      printf("chunk %2d tma %7lld arawfull %7lld aready %7lld bready %7lld mma %7lld | tile %d epi_done %7lld\n", i,
+             g_gemm_trace[0][i] - t0, g_gemm_trace[1][i] - t0, g_gemm_trace[2][i] - t0,
+             g_gemm_trace[3][i] - t0, g_gemm_trace[4][i] - t0, i, g_gemm_trace[5][i] - t0);
+  }
+#endif
 }
 
 }  // namespace fcb

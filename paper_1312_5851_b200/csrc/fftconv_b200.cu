@@ -390,11 +390,13 @@ static GemmGeom gemm_geom(size_t M, size_t N, const DevInfo& di) {
   g.n_tiles = (int)((n16 + kMaxNc - 1) / kMaxNc);
   g.nc = (int)round_up((n16 + g.n_tiles - 1) / g.n_tiles, 16);
   g.m_tiles = (int)((M + kTileM - 1) / kTileM);
-  const int sb = gemm_stage_bytes(g.nc);
-  const int budget = di.max_smem_optin - 1024 - 256;
-  g.stages = std::min(6, budget / sb);
+  // raw TMA stages (A + B chunks) fill what the two converted-B buffers leave
+  const int sb = gemm_raw_stage_bytes(g.nc);
+  const int fixed = 2 * gemm_bbuf_bytes(g.nc);
+  const int budget = di.max_smem_optin - 1024 - 256 - fixed;
+  g.stages = std::min(8, budget / sb);
   if (g.stages < 2) throw Error(FFTCONV_B200_CUDA_ERROR, "gemm tile does not fit shared memory");
-  g.smem = (size_t)g.stages * sb + 1024 + 256;
+  g.smem = (size_t)g.stages * sb + fixed + 1024 + 256;
   return g;
 }
 
