@@ -39,20 +39,53 @@ __host__ __device__ constexpr int ceil32_i(int a) { return (a + 31) / 32 * 32; }
 
 constexpr int kTmaSmemBudget = 220 * 1024;
 // Development switch for bottleneck experiments (default 0 = real kernel):
-// 1 skips the FFT arithmetic, 2 skips the HBM stores, 3 skips the HBM loads,
-// 4 = stores only, 5 = stores only into a group-contiguous layout.
+// 1 skips the FFT arithmetic, 2 skips the HBM stores, 3 skips the HBM loads.
 #ifndef FCB_XFORM_EXP
 #define FCB_XFORM_EXP 0
 #endif
-constexpr int kConsumers = 2;  // consumer groups per CTA (named barriers 1, 2)
+constexpr int kConsumers = 2;
+
+// FCB_XFORM_TRACE: per-group clock64 timeline of CTA 0 (development builds)
+#ifdef FCB_XFORM_TRACE
+__device__ long long g_xform_trace[6][64];
+#define XTRACE(ev, idx)                                                     \
+  do {                                                                      \
+    if (blockIdx.x == 0 && (idx) < 64) g_xform_trace[ev][idx] = clock64();  \
+  } while (0)
+#else
+#define XTRACE(ev, idx) \
+  do {                  \
+  } while (0)
+#endif
+
+// smallest box count >= bins/256 that divides the bins (TMA box dims <= 256)
+__host__ __device__ constexpr int nbox_for(int bins, int n = 0) {
+  return n == 0 ? nbox_for(bins, (bins + 255) / 256) : (bins % n == 0 ? n : nbox_for(bins, n + 1));
+}  // consumer groups per CTA (named barriers 1, 2)
 
 // ---------------------------------------------------------------- K1: r2c
+//
+// Warp roles (stores never stall a compute warp: the measured bottleneck of
+// the earlier cuts was warps issuing the 93.5 MB of scattered spectrum
+// stores between FFTs):
+//   warp 0         copy engine: bulk-loads plane groups into the stage ring
+//                  and drains finished stages to HBM with TMA tensor stores
+//   pass-1 warps   FULL[s] -> real column FFTs (dense (plane, column-pair)
+//                  items) -> intermediate in place -> MID[s]
+//   pass-2 warps   MID[s] -> complex row FFTs -> the spectrum rows written
+//                  back into the same stage in the output tile layout
+//                  [bin][plane] -> OUT[s]; the copy engine stores the tile
+//                  and refills the stage once the store has read it
 template <int M>
 struct TR2C {
   static constexpr bool BIG = (M == 64);
-  static constexpr int G = BIG ? 4 : 16;  // planes (K indices) per group
+  // planes (K indices) per group: 8 (64-B spectrum segments; a 16-plane
+  // group made 72-KB stages, only 3 of which fit, too shallow to hide the
+  // ~4.5k-cycle load latency under load), 4 at m = 64
+  static constexpr int G = BIG ? 4 : 8;
   static constexpr int PC = M / 2 + 1;
   static constexpr int CP = M + 1;        // intermediate row stride (float2)
+  static constexpr int BINS = M * PC;
   // raw plane incl. 16-B alignment slack, in float2
   static constexpr int RAWF2 = (M * M * 4 + 16 + 7) / 8;
   static constexpr int PS0 = cmax_i(PC * CP, RAWF2 + 1);
@@ -60,15 +93,21 @@ struct TR2C {
   // reads in pass 2 hit distinct banks.  m = 64: 4 (mod 16), so the
   // (plane, u) pairs of a warp are spread over the banks.
   static constexpr int PS = BIG ? PS0 + ((4 - PS0 % 16) + 16) % 16 : (PS0 | 1);
-  static constexpr int STAGE = round_up_i(G * PS * 8 + 8, 128);
+  static constexpr int STAGE = round_up_i(cmax_i(G * PS * 8 + 8, BINS * G * 8), 128);
   static constexpr int S = cmin_i(8, kTmaSmemBudget / STAGE);
-  // threads per consumer group = work items per pass (m = 64: one column /
-  // half-row per thread)
   static constexpr int P1 = BIG ? G * M : G * (M / 2);  // column (pair) items
-  static constexpr int P2 = BIG ? G * PC * 2 : G * PC;  // (plane, u[, half]) row items
-  static constexpr int CT = ceil32_i(cmax_i(P1, P2));   // threads per consumer group
-  static constexpr int THREADS = kConsumers * CT;
-  static constexpr int SMEM = S * STAGE + 2 * S * 8 + 128;
+  static constexpr int P2 = BIG ? G * PC * 2 : G * PC;  // row items
+  static constexpr int P1W = ceil32_i(P1), P2W = ceil32_i(P2);
+  // independent pass-1/pass-2 pipelines on alternating groups (an even
+  // stage count keeps every stage in one parity class, so no mbarrier
+  // phase is ever shared between the pipelines)
+  static constexpr int NPIPE = (!BIG && S % 2 == 0) ? 2 : 1;
+  static constexpr int THREADS = 32 + NPIPE * (P1W + P2W);
+  static constexpr int SMEM = S * STAGE + 3 * S * 8 + 128;
+  // output tile stores: NBOX boxes of BT bins x G planes
+  static constexpr int NBOX = nbox_for(BINS);
+  static constexpr int BT = BINS / NBOX;
+  static_assert(BT * NBOX == BINS && BT <= 256, "output box must tile the bins");
 };
 
 // byte offset of plane jl's raw copy inside a stage (16-B aligned, at or
@@ -77,7 +116,7 @@ __device__ __forceinline__ int r2c_raw_off(int jl, int ps) { return (jl * ps * 8
 
 struct GroupRef {
   const R2CParams* p;
-  int r, j0;
+  int which, r, j0;
 };
 
 template <int G>
@@ -86,229 +125,261 @@ __device__ __forceinline__ GroupRef r2c_group(const R2CPair& P, int ngA, int g) 
   const R2CParams& p = P.op[which];
   const int gl = g - which * ngA, ngj = p.kpad / G;
   const int r = gl / ngj;
-  return {&p, r, (gl - r * ngj) * G};
+  return {&p, which, r, (gl - r * ngj) * G};
 }
 
-// Stores one spectrum row (bin-major, stride bstride) with the conjugation
-// sign of the operand.
+// Stores one spectrum row into the output tile (stride in float2).
 template <int N>
-__device__ __forceinline__ void store_row(float2* o, long long stride, const float2 (&w)[N], float csign) {
+__device__ __forceinline__ void tile_row(float2* o, int stride, const float2 (&w)[N], float csign) {
 #pragma unroll
-  for (int v = 0; v < N; ++v) {
-    *o = make_float2(w[v].x, csign * w[v].y);
-    o += stride;
-  }
+  for (int v = 0; v < N; ++v) o[v * stride] = make_float2(w[v].x, csign * w[v].y);
 }
 
 // grid = persistent (<= groups), block = THREADS, smem = SMEM.
+// tmo[i]: 3-D fp32 map over operand i's spectrum F[t][R][2*kpad], box
+// {2G floats, 1 row, BT bins}.
 template <int M>
-__global__ void __launch_bounds__(TR2C<M>::THREADS, 1) r2c_tma_kernel(const __grid_constant__ R2CPair P) {
+__global__ void __launch_bounds__(TR2C<M>::THREADS, 1)
+    r2c_tma_kernel(const __grid_constant__ R2CPair P, const __grid_constant__ CUtensorMap tmo0,
+                   const __grid_constant__ CUtensorMap tmo1) {
   using T = TR2C<M>;
-  constexpr int G = T::G, PC = T::PC, CP = T::CP, PS = T::PS, S = T::S, CT = T::CT;
+  constexpr int G = T::G, PC = T::PC, CP = T::CP, PS = T::PS, S = T::S;
   extern __shared__ __align__(128) uint8_t smem[];
-  // FULL[s]: the group's copies landed.  EMPTY[s]: the previous user of the
-  // stage released it.  With two consumers a group's consumer may reach its
-  // FULL wait before the previous use of the stage has even completed; it
-  // waits EMPTY first so the FULL parity it waits on cannot alias.
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * T::STAGE);
-  uint64_t* empty = full + S;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * T::STAGE);  // loads landed
+  uint64_t* mid = full + S;                                           // intermediate written
+  uint64_t* outb = mid + S;                                           // output tile written
   const int ngA = P.op[0].R * (P.op[0].kpad / G);
   const int ngroups = ngA + (P.n > 1 ? P.op[1].R * (P.op[1].kpad / G) : 0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&mid[s], T::P1W);
+      mbar_init(&outb[s], T::P2W);
     }
     fence_barrier_init();
+    tma_prefetch_desc(&tmo0);
+    tma_prefetch_desc(&tmo1);
   }
   __syncthreads();
   pdl_wait();
   pdl_trigger();
 
-  // copies of this CTA's i-th group into stage i % S (one thread)
-  auto issue = [&](int i) {
-    const int g = blockIdx.x + i * gridDim.x;
-    if (g >= ngroups) return;
-    const uint64_t pol = l2_policy_evict_first();
-    const int s = i % S;
-    const GroupRef q = r2c_group<G>(P, ngA, g);
-    const R2CParams& p = *q.p;
-    const int jv = min(G, p.J - q.j0);  // <= 0: a pure K-padding group
-    const uint32_t pb = (uint32_t)(p.src * p.src) * 4u;
-    const float* base = p.in + (long long)q.r * p.in_sr + (long long)q.j0 * p.in_sj;
-    uint32_t total = 0;
-    const int jv_copy = (FCB_XFORM_EXP == 3 || FCB_XFORM_EXP >= 4) ? 0 : jv;
-    for (int jl = 0; jl < jv_copy; ++jl) {
-      const uintptr_t a = reinterpret_cast<uintptr_t>(base + (long long)jl * p.in_sj);
-      total += ((uint32_t)(a & 15) + pb + 15) & ~15u;
-    }
-    mbar_arrive_expect_tx(&full[s], total);
-    uint8_t* st = smem + s * T::STAGE;
-    for (int jl = 0; jl < jv_copy; ++jl) {
-      // the plane's enclosing 16-B aligned range (planes need not be aligned)
-      const uintptr_t a = reinterpret_cast<uintptr_t>(base + (long long)jl * p.in_sj);
-      const uint32_t sz = ((uint32_t)(a & 15) + pb + 15) & ~15u;
-      bulk_load(st + r2c_raw_off(jl, PS), reinterpret_cast<const void*>(a & ~uintptr_t(15)), sz,
-                &full[s], pol);
-    }
-  };
-  if (threadIdx.x == 0) {
-#pragma unroll 1
-    for (int i = 0; i < S; ++i) issue(i);
-  }
-
-  const int cg = threadIdx.x / CT;  // consumer group
-  const int t = threadIdx.x - cg * CT;
-  const int bar = 1 + cg;
-#pragma unroll 1
-  for (int i = cg;; i += kConsumers) {
-    const int g = blockIdx.x + i * gridDim.x;
-    if (g >= ngroups) break;
-    const int s = i % S;
-    const GroupRef q = r2c_group<G>(P, ngA, g);
-    const R2CParams& p = *q.p;
-    const int src = p.src;
-    const int jv = max(0, min(G, p.J - q.j0));
-    uint8_t* st = smem + s * T::STAGE;
-    if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
-    mbar_wait(&full[s], (i / S) & 1);
-
-    // ---------------- pass 1: real column FFTs over the src non-zero columns
-    // of the valid planes, (plane, column[-pair]) items packed densely.
-    // Each specialisation keeps its own register arrays (a branch that
-    // writes one array from two paths demotes it to local memory).
-    if constexpr (!T::BIG) {
-      // column pairs (c, c + H) packed as one complex FFT
-      const int H = (src + 1) >> 1;
-      const bool act = t < jv * H;
-      const int jl = act ? t / H : 0, c = t - jl * H;
-      const bool hb = c + H < src;
-      const float* pin = p.in + (long long)q.r * p.in_sr + (long long)(q.j0 + jl) * p.in_sj;
-      const float* raw = reinterpret_cast<const float*>(st + r2c_raw_off(jl, PS)) +
-                         ((reinterpret_cast<uintptr_t>(pin) & 15) >> 2) + c;
-      float2* dst = reinterpret_cast<float2*>(st + jl * PS * 8) + c;
-      auto pass1 = [&](auto full_tag) {
-        constexpr bool FULL = decltype(full_tag)::value;
-        float2 z[M];
-#pragma unroll
-        for (int row = 0; row < M; ++row) {
-          if constexpr (FULL) {  // full plane: constant offsets, no predicates
-            z[row].x = act ? raw[row * M] : 0.f;
-            z[row].y = act ? raw[row * M + M / 2] : 0.f;
-          } else {
-            const bool ok = act && row < src;
-            z[row].x = ok ? raw[0] : 0.f;
-            z[row].y = (ok && hb) ? raw[H] : 0.f;
-            raw += src;
-          }
+  if (threadIdx.x < 32) {
+    // ------------------------------------------------ copy engine
+    if (threadIdx.x == 0) {
+      const uint64_t pol = l2_policy_evict_first();
+      auto issue_load = [&](int i) {
+        const int g = blockIdx.x + i * gridDim.x;
+        if (g >= ngroups) return;
+        XTRACE(0, i);
+        const int s = i % S;
+        const GroupRef q = r2c_group<G>(P, ngA, g);
+        const R2CParams& p = *q.p;
+        const int jv = FCB_XFORM_EXP == 3 ? 0 : min(G, p.J - q.j0);  // <= 0: pure K padding
+        const uint32_t pb = (uint32_t)(p.src * p.src) * 4u;
+        const float* base = p.in + (long long)q.r * p.in_sr + (long long)q.j0 * p.in_sj;
+        uint32_t total = 0;
+        for (int jl = 0; jl < jv; ++jl) {
+          const uintptr_t a = reinterpret_cast<uintptr_t>(base + (long long)jl * p.in_sj);
+          total += ((uint32_t)(a & 15) + pb + 15) & ~15u;
         }
-        named_bar_sync(bar, CT);  // every raw plane is read: overwrite in place
-        if (act) {
-          if (FCB_XFORM_EXP != 1 && FCB_XFORM_EXP < 4) fft_reg<M, false>(z);
-          static_for<0, PC>([&](auto U) {
-            constexpr int u = decltype(U)::value;
-            const float2 zu = z[u];
-            const float2 zc = cconj(z[(M - u) % M]);
-            dst[u * CP] = make_float2(0.5f * (zu.x + zc.x), 0.5f * (zu.y + zc.y));
-            if (FULL || hb) {
-              const float2 d = csub(zu, zc);
-              dst[u * CP + (FULL ? M / 2 : H)] = make_float2(0.5f * d.y, -0.5f * d.x);  // (zu - zc) / (2i)
+        mbar_arrive_expect_tx(&full[s], total);
+        uint8_t* st = smem + s * T::STAGE;
+        for (int jl = 0; jl < jv; ++jl) {
+          // the plane's enclosing 16-B aligned range (planes need not be aligned)
+          const uintptr_t a = reinterpret_cast<uintptr_t>(base + (long long)jl * p.in_sj);
+          const uint32_t sz = ((uint32_t)(a & 15) + pb + 15) & ~15u;
+          bulk_load(st + r2c_raw_off(jl, PS), reinterpret_cast<const void*>(a & ~uintptr_t(15)), sz,
+                    &full[s], pol);
+        }
+      };
+#pragma unroll 1
+      for (int i = 0; i < S; ++i) issue_load(i);
+#pragma unroll 1
+      for (int i = 0;; ++i) {
+        const int g = blockIdx.x + i * gridDim.x;
+        if (g >= ngroups) break;
+        const int s = i % S;
+        mbar_wait(&outb[s], (i / S) & 1);
+        XTRACE(4, i);
+        const GroupRef q = r2c_group<G>(P, ngA, g);
+        const CUtensorMap* tm = q.which ? &tmo1 : &tmo0;
+        const uint8_t* st = smem + s * T::STAGE;
+        if (FCB_XFORM_EXP != 2)
+          for (int k = 0; k < T::NBOX; ++k)
+            tma_store_3d(tm, st + k * T::BT * G * 8, 2 * q.j0, q.r, k * T::BT);
+        bulk_commit_group();
+        bulk_wait_group_read<0>();  // the store has read the tile: refill the stage
+        XTRACE(5, i);
+        issue_load(i + S);
+      }
+      bulk_wait_group<0>();  // spectra written before the grid completes
+    }
+  } else if (threadIdx.x < 32 + T::NPIPE * T::P1W) {
+    // ------------------------------------------------ pass 1: real column FFTs
+    const int pipe = (threadIdx.x - 32) / T::P1W;
+    const int t = threadIdx.x - 32 - pipe * T::P1W;
+    const int bar = 1 + pipe;
+#pragma unroll 1
+    for (int i = pipe;; i += T::NPIPE) {
+      const int g = blockIdx.x + i * gridDim.x;
+      if (g >= ngroups) break;
+      const int s = i % S;
+      const GroupRef q = r2c_group<G>(P, ngA, g);
+      const R2CParams& p = *q.p;
+      const int src = p.src;
+      const int jv = max(0, min(G, p.J - q.j0));
+      uint8_t* st = smem + s * T::STAGE;
+      mbar_wait(&full[s], (i / S) & 1);
+      if (t == 0) XTRACE(1, i);
+      // (plane, column[-pair]) items packed densely over the valid planes and
+      // their src non-zero columns.  Each specialisation keeps its own
+      // register arrays (a branch writing one array from two paths demotes
+      // it to local memory).
+      if constexpr (!T::BIG) {
+        const int H = (src + 1) >> 1;  // column pairs (c, c + H): one complex FFT
+        const bool act = t < jv * H;
+        const int jl = act ? t / H : 0, c = t - jl * H;
+        const bool hb = c + H < src;
+        const float* pin = p.in + (long long)q.r * p.in_sr + (long long)(q.j0 + jl) * p.in_sj;
+        const float* raw = reinterpret_cast<const float*>(st + r2c_raw_off(jl, PS)) +
+                           ((reinterpret_cast<uintptr_t>(pin) & 15) >> 2) + c;
+        float2* dst = reinterpret_cast<float2*>(st + jl * PS * 8) + c;
+        auto pass1 = [&](auto full_tag) {
+          constexpr bool FULL = decltype(full_tag)::value;
+          float2 z[M];
+#pragma unroll
+          for (int row = 0; row < M; ++row) {
+            if constexpr (FULL) {  // full plane: constant offsets, no predicates
+              z[row].x = act ? raw[row * M] : 0.f;
+              z[row].y = act ? raw[row * M + M / 2] : 0.f;
+            } else {
+              const bool ok = act && row < src;
+              z[row].x = ok ? raw[0] : 0.f;
+              z[row].y = (ok && hb) ? raw[H] : 0.f;
+              raw += src;
             }
-          });
-        }
-      };
-      if (src == M) pass1(std::true_type{});
-      else pass1(std::false_type{});
-    } else {
-      // m = 64: one real column per thread (half-length complex FFT)
-      const bool act = t < jv * src;
-      const int jl = act ? t / src : 0, c = t - jl * src;
-      const float* pin = p.in + (long long)q.r * p.in_sr + (long long)(q.j0 + jl) * p.in_sj;
-      const float* raw = reinterpret_cast<const float*>(st + r2c_raw_off(jl, PS)) +
-                         ((reinterpret_cast<uintptr_t>(pin) & 15) >> 2) + c;
-      float2* dst = reinterpret_cast<float2*>(st + jl * PS * 8) + c;
-      auto pass1 = [&](auto full_tag) {
-        constexpr bool FULL = decltype(full_tag)::value;
-        float2 z[M / 2];  // (even, odd) rows packed for the half-length FFT
-#pragma unroll
-        for (int i2 = 0; i2 < M / 2; ++i2) {
-          if constexpr (FULL) {
-            z[i2].x = act ? raw[(2 * i2) * M] : 0.f;
-            z[i2].y = act ? raw[(2 * i2 + 1) * M] : 0.f;
-          } else {
-            z[i2].x = (act && 2 * i2 < src) ? raw[(2 * i2) * src] : 0.f;
-            z[i2].y = (act && 2 * i2 + 1 < src) ? raw[(2 * i2 + 1) * src] : 0.f;
           }
-        }
-        named_bar_sync(bar, CT);  // a plane spans two warps
-        if (act) rfft_packed_emit<M>(z, [&](int u, float2 v) { dst[u * CP] = v; });
-      };
-      if (src == M) pass1(std::true_type{});
-      else pass1(std::false_type{});
-    }
-    named_bar_sync(bar, CT);  // intermediate complete
-
-    // ---------------- pass 2: complex row FFTs -> bin-major HBM
-    const long long bstride = (long long)p.R * p.kpad;  // float2 per bin
-    const float csign = p.conj ? -1.f : 1.f;
-    float2* obase = reinterpret_cast<float2*>(p.out) + (long long)q.r * p.kpad + q.j0;
-    if constexpr (!T::BIG) {
-      const int jl = t % G, u = t / G;
-      const bool act = t < T::P2;
-      const bool valid = act && jl < jv;
-      const float2* row = reinterpret_cast<const float2*>(st + jl * PS * 8) + u * CP;
-      float2* o = obase + jl + (long long)(u * M) * bstride;
-#if FCB_XFORM_EXP == 5
-      o = reinterpret_cast<float2*>(p.out) + (long long)(q.r * (p.kpad / G) + q.j0 / G) * (M * PC * G) + (u * M) * G + jl;
-      const long long bstride_e = G;
-#else
-      const long long bstride_e = bstride;
-#endif
-      auto pass2 = [&](auto full_tag) {
-        constexpr bool FULL = decltype(full_tag)::value;
-        float2 w[M];
+          named_bar_sync(bar, T::P1W);  // every raw plane is read: overwrite in place
+          if (act) {
+            if (FCB_XFORM_EXP != 1) fft_reg<M, false>(z);
+            static_for<0, PC>([&](auto U) {
+              constexpr int u = decltype(U)::value;
+              const float2 zu = z[u];
+              const float2 zc = cconj(z[(M - u) % M]);
+              dst[u * CP] = make_float2(0.5f * (zu.x + zc.x), 0.5f * (zu.y + zc.y));
+              if (FULL || hb) {
+                const float2 d = csub(zu, zc);
+                dst[u * CP + (FULL ? M / 2 : H)] = make_float2(0.5f * d.y, -0.5f * d.x);  // (zu - zc) / (2i)
+              }
+            });
+          }
+        };
+        if (src == M) pass1(std::true_type{});
+        else pass1(std::false_type{});
+      } else {
+        // m = 64: one real column per thread (half-length complex FFT)
+        const bool act = t < jv * src;
+        const int jl = act ? t / src : 0, c = t - jl * src;
+        const float* pin = p.in + (long long)q.r * p.in_sr + (long long)(q.j0 + jl) * p.in_sj;
+        const float* raw = reinterpret_cast<const float*>(st + r2c_raw_off(jl, PS)) +
+                           ((reinterpret_cast<uintptr_t>(pin) & 15) >> 2) + c;
+        float2* dst = reinterpret_cast<float2*>(st + jl * PS * 8) + c;
+        auto pass1 = [&](auto full_tag) {
+          constexpr bool FULL = decltype(full_tag)::value;
+          float2 z[M / 2];  // (even, odd) rows packed for the half-length FFT
 #pragma unroll
-        for (int cc = 0; cc < M; ++cc)
-          w[cc] = (valid && (FULL || cc < src)) ? row[cc] : make_float2(0.f, 0.f);
-        named_bar_sync(bar, CT);  // the stage is free: refill it S groups ahead
-        if (t == 0) {
-          mbar_arrive(&empty[s]);
-          issue(i + S);
-        }
-        if (act) {  // K padding (invalid planes) stores exact zeros
-          if (FCB_XFORM_EXP != 1 && FCB_XFORM_EXP < 4) fft_reg<M, false>(w);
-          if (FCB_XFORM_EXP != 2) store_row<M>(o, bstride_e, w, csign);
-        }
-      };
-      if (src == M) pass2(std::true_type{});
-      else pass2(std::false_type{});
-    } else {
-      // (plane, u, half): one decimation-in-frequency stage splits the
-      // 64-point row FFT into two 32-point halves, outputs v = 2k + h
-      const int jl = t % G, h = (t / G) & 1, u = t / (2 * G);
-      const bool act = t < T::P2;
-      const bool valid = act && jl < jv;
-      const float2* row = reinterpret_cast<const float2*>(st + jl * PS * 8) + u * CP;
-      float2 z[32];
-      static_for<0, 32>([&](auto Cc) {
-        constexpr int cc = decltype(Cc)::value;
-        const float2 a0 = (valid && cc < src) ? row[cc] : make_float2(0.f, 0.f);
-        const float2 a1 = (valid && cc + 32 < src) ? row[cc + 32] : make_float2(0.f, 0.f);
-        const float2 d = csub(a0, a1);
-        if constexpr (cc == 0) z[cc] = h ? d : cadd(a0, a1);
-        else z[cc] = h ? cmul(d, tw128c<false, cc * 2>()) : cadd(a0, a1);
-      });
-      named_bar_sync(bar, CT);
-      if (t == 0) {
-        mbar_arrive(&empty[s]);
-        issue(i + S);
+          for (int i2 = 0; i2 < M / 2; ++i2) {
+            if constexpr (FULL) {
+              z[i2].x = act ? raw[(2 * i2) * M] : 0.f;
+              z[i2].y = act ? raw[(2 * i2 + 1) * M] : 0.f;
+            } else {
+              z[i2].x = (act && 2 * i2 < src) ? raw[(2 * i2) * src] : 0.f;
+              z[i2].y = (act && 2 * i2 + 1 < src) ? raw[(2 * i2 + 1) * src] : 0.f;
+            }
+          }
+          named_bar_sync(bar, T::P1W);  // a plane spans two warps
+          if (act) rfft_packed_emit<M>(z, [&](int u, float2 v) { dst[u * CP] = v; });
+        };
+        if (src == M) pass1(std::true_type{});
+        else pass1(std::false_type{});
       }
-      if (act) {
-        fft_reg<32, false>(z);
-        store_row<32>(obase + jl + (long long)(u * M + h) * bstride, 2 * bstride, z, csign);
+      mbar_arrive(&mid[s]);
+      if (t == 0) XTRACE(2, i);
+    }
+  } else {
+    // ------------------------------------------------ pass 2: complex row FFTs -> output tile
+    const int pipe = (threadIdx.x - 32 - T::NPIPE * T::P1W) / T::P2W;
+    const int t = threadIdx.x - 32 - T::NPIPE * T::P1W - pipe * T::P2W;
+    const int bar = 1 + T::NPIPE + pipe;
+    const bool act = t < T::P2;
+#pragma unroll 1
+    for (int i = pipe;; i += T::NPIPE) {
+      const int g = blockIdx.x + i * gridDim.x;
+      if (g >= ngroups) break;
+      const int s = i % S;
+      const GroupRef q = r2c_group<G>(P, ngA, g);
+      const R2CParams& p = *q.p;
+      const int src = p.src;
+      const int jv = max(0, min(G, p.J - q.j0));
+      const float csign = p.conj ? -1.f : 1.f;
+      uint8_t* st = smem + s * T::STAGE;
+      float2* tile = reinterpret_cast<float2*>(st);  // [bin][G planes]
+      mbar_wait(&mid[s], (i / S) & 1);
+      if constexpr (!T::BIG) {
+        const int jl = t % G, u = t / G;
+        const bool valid = act && jl < jv;
+        const float2* row = reinterpret_cast<const float2*>(st + jl * PS * 8) + u * CP;
+        auto pass2 = [&](auto full_tag) {
+          constexpr bool FULL = decltype(full_tag)::value;
+          float2 w[M];
+#pragma unroll
+          for (int cc = 0; cc < M; ++cc)
+            w[cc] = (valid && (FULL || cc < src)) ? row[cc] : make_float2(0.f, 0.f);
+          named_bar_sync(bar, T::P2W);  // the intermediate is read: reuse the stage as the tile
+          if (act) {  // invalid (K padding) planes store exact zeros
+            if (FCB_XFORM_EXP != 1) fft_reg<M, false>(w);
+            tile_row<M>(tile + (u * M) * G + jl, G, w, csign);
+          }
+        };
+        if (src == M) pass2(std::true_type{});
+        else pass2(std::false_type{});
+      } else {
+        // (plane, u, half): one decimation-in-frequency stage splits the
+        // 64-point row FFT into two 32-point halves, outputs v = 2k + h
+        const int jl = t % G, h = (t / G) & 1, u = t / (2 * G);
+        const bool valid = act && jl < jv;
+        const float2* row = reinterpret_cast<const float2*>(st + jl * PS * 8) + u * CP;
+        float2 z[32];
+        static_for<0, 32>([&](auto Cc) {
+          constexpr int cc = decltype(Cc)::value;
+          const float2 a0 = (valid && cc < src) ? row[cc] : make_float2(0.f, 0.f);
+          const float2 a1 = (valid && cc + 32 < src) ? row[cc + 32] : make_float2(0.f, 0.f);
+          const float2 d = csub(a0, a1);
+          if constexpr (cc == 0) z[cc] = h ? d : cadd(a0, a1);
+          else z[cc] = h ? cmul(d, tw128c<false, cc * 2>()) : cadd(a0, a1);
+        });
+        named_bar_sync(bar, T::P2W);
+        if (act) {
+          if (FCB_XFORM_EXP != 1) fft_reg<32, false>(z);
+          tile_row<32>(tile + (u * M + h) * G + jl, 2 * G, z, csign);
+        }
       }
+      fence_proxy_async_smem();  // the tile is read by the TMA store (async proxy)
+      mbar_arrive(&outb[s]);
+      if (t == 0) XTRACE(3, i);
     }
   }
+#ifdef FCB_XFORM_TRACE
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const long long t0 = g_xform_trace[0][0];
+    for (int i = 0; i < 12; ++i)
+      printf("grp %2d load %7lld full %7lld p1done %7lld p2done %7lld store %7lld refill %7lld\n", i,
+             g_xform_trace[0][i] - t0, g_xform_trace[1][i] - t0, g_xform_trace[2][i] - t0,
+             g_xform_trace[3][i] - t0, g_xform_trace[4][i] - t0, g_xform_trace[5][i] - t0);
+  }
+#endif
 }
 
 // ---------------------------------------------------------------- K4: c2r

@@ -224,6 +224,24 @@ static bool legacy_xform() {
   return v;
 }
 
+// 3-D fp32 map over a bin-major spectrum X[t][R][2*ld] (complex, ld even)
+// with box {2g floats, 1 row, bt bins}: the transform kernels' tiles.
+static CUtensorMap make_bin_map(const float* base, size_t ld, size_t R, size_t bins, uint32_t g,
+                                uint32_t bt) {
+  CUtensorMap t;
+  const cuuint64_t dims[3] = {2 * ld, R, bins};
+  const cuuint64_t strides[2] = {2 * ld * sizeof(float), R * 2 * ld * sizeof(float)};
+  const cuuint32_t box[3] = {2 * g, 1, bt};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&t, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw Error(FFTCONV_B200_CUDA_ERROR, "cuTensorMapEncodeTiled (spectrum) failed: " + std::to_string(r));
+  return t;
+}
+
 template <int M>
 static void launch_r2c_tma(const R2CPair& P, const DevInfo& di, cudaStream_t st) {
   using T = TR2C<M>;
@@ -232,7 +250,13 @@ static void launch_r2c_tma(const R2CPair& P, const DevInfo& di, cudaStream_t st)
   int groups = 0;
   for (int i = 0; i < P.n; ++i) groups += P.op[i].R * (P.op[i].kpad / T::G);
   const int grid = std::max(1, std::min(groups, di.sms));
-  launch_pdl(kern, dim3(grid), dim3(T::THREADS), T::SMEM, st, P);
+  const size_t bins = (size_t)T::BINS;
+  CUtensorMap tm[2];
+  for (int i = 0; i < 2; ++i) {
+    const R2CParams& p = P.op[i < P.n ? i : 0];
+    tm[i] = make_bin_map(p.out, p.kpad, p.R, bins, T::G, T::BT);
+  }
+  launch_pdl(kern, dim3(grid), dim3(T::THREADS), T::SMEM, st, P, tm[0], tm[1]);
 }
 
 static void launch_r2c_group(size_t m, const R2CPair& P, cudaStream_t st, const DevInfo& di) {
@@ -312,30 +336,13 @@ static void launch_c2r_ws(const C2RParams& p, const DevInfo& di, cudaStream_t st
   launch_pdl(kern, dim3(grid), dim3(Tr::THREADS), Tr::SMEM, st, p);
 }
 
-// 3-D fp32 map over P[t][R][2*ld]; box {2G floats, 1, m bins} = one u row.
-static CUtensorMap make_spectrum_map(const float* base, size_t ld, size_t R, size_t bins,
-                                     uint32_t g, uint32_t m) {
-  CUtensorMap t;
-  const cuuint64_t dims[3] = {2 * ld, R, bins};
-  const cuuint64_t strides[2] = {2 * ld * sizeof(float), R * 2 * ld * sizeof(float)};
-  const cuuint32_t box[3] = {2 * g, 1, m};
-  const cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = encode_fn()(&t, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims,
-                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS)
-    throw Error(FFTCONV_B200_CUDA_ERROR, "cuTensorMapEncodeTiled (spectrum) failed: " + std::to_string(r));
-  return t;
-}
-
 template <int M>
 static void launch_c2r_tma(const C2RParams& p, const DevInfo& di, cudaStream_t st) {
   using T = TC2R<M>;
   auto kern = c2r_tma_kernel<M>;
   smem_optin(kern, T::SMEM);
   const size_t bins = (size_t)M * (M / 2 + 1);
-  const CUtensorMap tm = make_spectrum_map(p.in, p.ld, p.R, bins, T::G, M);
+  const CUtensorMap tm = make_bin_map(p.in, p.ld, p.R, bins, T::G, M);
   const int groups = p.R * ((p.J + T::G - 1) / T::G);
   const int grid = std::max(1, std::min(groups, di.sms));
   launch_pdl(kern, dim3(grid), dim3(T::THREADS), T::SMEM, st, tm, p);
