@@ -56,7 +56,8 @@
 namespace fcb {
 
 struct GemmParams {
-  float* out;     // P[t][n][ldm] complex
+  float* out;     // product spectrum, complex element (t, n, m) at
+                  // t*s_t + (m/16)*s_mg + n*s_n + m%16 (see OutLayout)
   int bins;
   int m_valid;    // A rows (M)
   int n_valid;    // complex output columns (N)
@@ -65,7 +66,7 @@ struct GemmParams {
   int nc;         // complex columns per N tile (multiple of 16, <= 96)
   int stages;
   float im_sign;  // +1 (fprop, bprop) or -1 (accGrad)
-  int ldm;        // output row stride in complex elements (>= m_valid)
+  long long s_t, s_mg, s_n;  // output strides in complex elements
 };
 
 constexpr int kGemmThreads = 640;
@@ -308,7 +309,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int m = mt * kTileM + row;
       const bool mok = m < p.m_valid;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + a * (2 * nc);
-      float2* out = reinterpret_cast<float2*>(p.out) + (long long)t * p.n_valid * p.ldm + m;
+      float2* out = reinterpret_cast<float2*>(p.out) + (long long)t * p.s_t + (m >> 4) * p.s_mg + (m & 15);
       for (int nb = half * 16; nb < nc; nb += 32) {
         float re[16], im[16];
         tmem_ld_32x32b_x16(tbase + nb, re);
@@ -319,7 +320,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int i = 0; i < 16; ++i) {
           const int n = n0 + i;
           if (mok && n < p.n_valid)
-            out[(long long)n * p.ldm] = make_float2(re[i], im_sign * im[i]);
+            out[(long long)n * p.s_n] = make_float2(re[i], im_sign * im[i]);
         }
       }
       tc_fence_before();

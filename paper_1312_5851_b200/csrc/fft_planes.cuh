@@ -388,6 +388,8 @@ struct C2RParams {
   int ccpad;    // odd smem stride >= cc
   float scale;  // 1 / m^2 (negated to fold a sign flip of the product)
   int ld;       // row stride of P in complex elements (>= J, even)
+  int bulk;     // 1: output planes 16-B aligned -> staged + bulk-stored (K4 TMA kernel)
+  int gm;       // 1: P is group-major P[r][J/16][t][16] (K4 TMA kernel, m <= 32)
 };
 
 // grid = (ceil(J/G), R, ceil(crop/cc)), block = PlaneTraits<M>::THREADS.

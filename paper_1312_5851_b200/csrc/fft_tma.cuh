@@ -58,6 +58,10 @@ __device__ long long g_xform_trace[6][64];
   } while (0)
 #endif
 
+#ifndef FCB_C2R_G
+#define FCB_C2R_G 16  // planes per K4 group at m <= 32
+#endif
+
 // smallest box count >= bins/256 that divides the bins (TMA box dims <= 256)
 __host__ __device__ constexpr int nbox_for(int bins, int n = 0) {
   return n == 0 ? nbox_for(bins, (bins + 255) / 256) : (bins % n == 0 ? n : nbox_for(bins, n + 1));
@@ -383,10 +387,23 @@ __global__ void __launch_bounds__(TR2C<M>::THREADS, 1)
 }
 
 // ---------------------------------------------------------------- K4: c2r
+//
+// Warp roles, as for K1:
+//   warp 0         copy engine: TMA tensor loads of the product spectrum
+//                  (one box of m bins x G planes per u row) into the stage
+//                  ring; refills a stage once pass 2 has read it
+//   pass-1 warps   FULL[s] -> inverse row FFTs over v, cropped columns
+//                  written in place -> MID[s]
+//   pass-2 warps   MID[s] -> Hermitian column c2r (dense (plane,
+//                  column-pair) items) -> the cropped planes written into
+//                  the same stage -> OUT[s]; the copy engine bulk-stores them
+//                  and refills the stage once the stores have read it.
+//                  Planes that are not 16-B aligned (odd crops) are stored
+//                  directly from registers instead (EMPTY[s] after the reads).
 template <int M>
 struct TC2R {
   static constexpr bool BIG = (M == 64);
-  static constexpr int G = BIG ? 4 : 16;
+  static constexpr int G = BIG ? 4 : FCB_C2R_G;
   static constexpr int PC = M / 2 + 1;
   static constexpr int CP = M + 1;  // intermediate row stride (float2), >= crop
   static constexpr int PS = BIG ? PC * CP + ((4 - (PC * CP) % 16) + 16) % 16 : ((PC * CP) | 1);
@@ -399,10 +416,12 @@ struct TC2R {
   static constexpr int S = cmin_i(8, kTmaSmemBudget / STAGE);
   static constexpr int P1 = BIG ? G * PC * 2 : G * PC;  // (plane, u[, half]) row items
   static constexpr int P2 = BIG ? G * M : G * (M / 2);  // column (pair) items
-  static constexpr int CT = ceil32_i(cmax_i(P1, P2));
-  static constexpr int THREADS = kConsumers * CT;
-  static constexpr int SMEM = S * STAGE + 2 * S * 8 + 128;
+  static constexpr int P1W = ceil32_i(P1), P2W = ceil32_i(P2);
+  static constexpr int NPIPE = (!BIG && S % 2 == 0) ? 2 : 1;
+  static constexpr int THREADS = 32 + NPIPE * (P1W + P2W);
+  static constexpr int SMEM = S * STAGE + 4 * S * 8 + 128;
   static constexpr uint32_t BOX_BYTES = 2 * G * 4 * M;  // one u row
+  static_assert(G * M * M * 4 <= STAGE, "a staged output tile must fit a stage");
 };
 
 // tm: 3-D fp32 map over the product spectrum P[t][r][2*ld] with box
@@ -411,21 +430,21 @@ template <int M>
 __global__ void __launch_bounds__(TC2R<M>::THREADS, 1)
     c2r_tma_kernel(const __grid_constant__ CUtensorMap tm, const C2RParams p) {
   using T = TC2R<M>;
-  constexpr int G = T::G, PC = T::PC, CP = T::CP, PS = T::PS, RS = T::RS, S = T::S, CT = T::CT;
+  constexpr int G = T::G, PC = T::PC, CP = T::CP, PS = T::PS, RS = T::RS, S = T::S;
   extern __shared__ __align__(128) uint8_t smem[];
-  // FULL[s]: the group's copies landed.  EMPTY[s]: the previous user of the
-  // stage released it.  With two consumers a group's consumer may reach its
-  // FULL wait before the previous use of the stage has even completed; it
-  // waits EMPTY first so the FULL parity it waits on cannot alias.
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * T::STAGE);
-  uint64_t* empty = full + S;
+  uint64_t* mid = full + S;
+  uint64_t* empty = mid + S;  // pass 2 read the stage (direct-store mode)
+  uint64_t* outb = empty + S;  // pass 2 wrote the output tile (bulk mode)
   const int ngj = (p.J + G - 1) / G;
   const int ngroups = p.R * ngj;
   const int crop = p.crop;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&mid[s], T::P1W);
+      mbar_init(&empty[s], T::P2W);
+      mbar_init(&outb[s], T::P2W);
     }
     fence_barrier_init();
     tma_prefetch_desc(&tm);
@@ -434,157 +453,239 @@ __global__ void __launch_bounds__(TC2R<M>::THREADS, 1)
   pdl_wait();
   pdl_trigger();
 
-  auto issue = [&](int i) {
-    const int g = blockIdx.x + i * gridDim.x;
-    if (g >= ngroups) return;
-    const uint64_t pol = l2_policy_evict_first();
-    const int s = i % S;
-    const int r = g / ngj, j0 = (g - r * ngj) * G;
-    mbar_arrive_expect_tx(&full[s], PC * T::BOX_BYTES);
-    uint8_t* st = smem + s * T::STAGE;
-    for (int u = 0; u < PC; ++u) tma_load_3d_hint(st + u * RS * 8, &tm, &full[s], 2 * j0, r, u * M, pol);
-  };
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
+    // ------------------------------------------------ copy engine
+    if (threadIdx.x == 0) {
+      const uint64_t pol = l2_policy_evict_first();
+      const uint32_t plane_bytes = (uint32_t)(crop * crop) * 4u;
+      auto issue_load = [&](int i) {
+        const int g = blockIdx.x + i * gridDim.x;
+        if (g >= ngroups) return;
+        const int s = i % S;
+        const int r = g / ngj, j0 = (g - r * ngj) * G;
+        XTRACE(0, i);
+        mbar_arrive_expect_tx(&full[s], PC * T::BOX_BYTES);
+        uint8_t* st = smem + s * T::STAGE;
+        if (p.gm) {  // group-major product: the group is one contiguous block
+          const float* src = p.in + (long long)(r * ngj + j0 / G) * (PC * T::BOX_BYTES / 4);
+          bulk_load(st, src, PC * T::BOX_BYTES, &full[s], pol);
+        } else {
+          for (int u = 0; u < PC; ++u) tma_load_3d_hint(st + u * RS * 8, &tm, &full[s], 2 * j0, r, u * M, pol);
+        }
+      };
 #pragma unroll 1
-    for (int i = 0; i < S; ++i) issue(i);
-  }
-
-  const int cg = threadIdx.x / CT;
-  const int t = threadIdx.x - cg * CT;
-  const int bar = 1 + cg;
-  const float scale = p.scale;
+      for (int i = 0; i < S; ++i) issue_load(i);
 #pragma unroll 1
-  for (int i = cg;; i += kConsumers) {
-    const int g = blockIdx.x + i * gridDim.x;
-    if (g >= ngroups) break;
-    const int s = i % S;
-    const int r = g / ngj, j0 = (g - r * ngj) * G;
-    const int jv = min(G, p.J - j0);
-    uint8_t* st = smem + s * T::STAGE;
-    const float2* raw = reinterpret_cast<const float2*>(st);
-    float2* inter = reinterpret_cast<float2*>(st);
-    if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
-    mbar_wait(&full[s], (i / S) & 1);
-
-    // ---------------- pass 1: inverse row FFTs over v, cropped columns kept
+      for (int i = 0;; ++i) {
+        const int g = blockIdx.x + i * gridDim.x;
+        if (g >= ngroups) break;
+        const int s = i % S;
+        if (p.bulk) {
+          mbar_wait(&outb[s], (i / S) & 1);
+          const int r = g / ngj, j0 = (g - r * ngj) * G;
+          const int jv = min(G, p.J - j0);
+          const uint8_t* tile = smem + s * T::STAGE;
+          if (FCB_XFORM_EXP != 2)
+            for (int jl = 0; jl < jv; ++jl)
+              bulk_store(p.out + (long long)r * p.out_sr + (long long)(j0 + jl) * p.out_sj,
+                         tile + jl * plane_bytes, plane_bytes);
+          bulk_commit_group();
+          bulk_wait_group_read<0>();  // the stores have read the tile: refill the stage
+        } else {
+          mbar_wait(&empty[s], (i / S) & 1);
+        }
+        issue_load(i + S);
+      }
+      if (p.bulk) bulk_wait_group<0>();
+    }
+  } else if (threadIdx.x < 32 + T::NPIPE * T::P1W) {
+    // ------------------------------------------------ pass 1: inverse row FFTs over v
+    const int pipe = (threadIdx.x - 32) / T::P1W;
+    const int t = threadIdx.x - 32 - pipe * T::P1W;
+    const int bar = 1 + pipe;
     const bool act1 = t < T::P1;
-    if constexpr (!T::BIG) {
-      const int jl = t % G, u = t / G;
-      const float2* src = raw + u * RS + jl;
-      float2 z[M];
+#pragma unroll 1
+    for (int i = pipe;; i += T::NPIPE) {
+      const int g = blockIdx.x + i * gridDim.x;
+      if (g >= ngroups) break;
+      const int s = i % S;
+      const int r = g / ngj, j0 = (g - r * ngj) * G;
+      const int jv = min(G, p.J - j0);
+      uint8_t* st = smem + s * T::STAGE;
+      const float2* raw = reinterpret_cast<const float2*>(st);
+      float2* inter = reinterpret_cast<float2*>(st);
+      (void)r;
+      mbar_wait(&full[s], (i / S) & 1);
+      if (t == 0) XTRACE(1, i);
+      if constexpr (!T::BIG) {
+        const int jl = t % G, u = t / G;
+        const float2* src = raw + u * RS + jl;
+        float2 z[M];
 #pragma unroll
-      for (int v = 0; v < M; ++v) z[v] = act1 ? src[v * G] : make_float2(0.f, 0.f);
-      named_bar_sync(bar, CT);  // the whole stage is read: overwrite in place
-      if (act1 && jl < jv) {
-        fft_reg<M, true>(z);
-        float2* dst = inter + jl * PS + u * CP;
+        for (int v = 0; v < M; ++v) z[v] = act1 ? src[v * G] : make_float2(0.f, 0.f);
+        named_bar_sync(bar, T::P1W);  // the whole stage is read: overwrite in place
+        if (act1 && jl < jv) {
+          if (FCB_XFORM_EXP != 1) fft_reg<M, true>(z);
+          float2* dst = inter + jl * PS + u * CP;
 #pragma unroll
-        for (int c = 0; c < M; ++c)
-          if (c < crop) dst[c] = z[c];
-      }
-    } else {
-      const int jl = t % G, h = (t / G) & 1, u = t / (2 * G);
-      const float2* src = raw + u * RS + jl;
-      float2 z[32];
-      static_for<0, 32>([&](auto Vv) {
-        constexpr int v = decltype(Vv)::value;
-        const float2 a0 = act1 ? src[v * G] : make_float2(0.f, 0.f);
-        const float2 a1 = act1 ? src[(v + 32) * G] : make_float2(0.f, 0.f);
-        const float2 d = csub(a0, a1);
-        if constexpr (v == 0) z[v] = h ? d : cadd(a0, a1);
-        else z[v] = h ? cmul(d, tw128c<true, v * 2>()) : cadd(a0, a1);
-      });
-      named_bar_sync(bar, CT);
-      if (act1 && jl < jv) {
-        fft_reg<32, true>(z);
-        float2* dst = inter + jl * PS + u * CP + h;
-#pragma unroll
-        for (int k = 0; k < 32; ++k)
-          if (2 * k + h < crop) dst[2 * k] = z[k];
-      }
-    }
-    named_bar_sync(bar, CT);  // intermediate complete
-
-    // ---------------- pass 2: Hermitian c2r over u -> HBM, (plane, column[-pair])
-    // items packed densely over the valid planes
-    if constexpr (!T::BIG) {
-      // column pairs (c, c + H) packed as one complex inverse FFT
-      const int H = (crop + 1) >> 1;
-      const bool act = t < jv * H;
-      const int jl = act ? t / H : 0, c = t - jl * H;
-      const bool hb = c + H < crop;
-      float2 zz[M];
-      {
-        const float2* col = inter + jl * PS + c;
-        static_for<0, PC>([&](auto U) {
-          constexpr int uu = decltype(U)::value;
-          float2 a = act ? col[uu * CP] : make_float2(0.f, 0.f);
-          float2 b = (act && hb) ? col[uu * CP + H] : make_float2(0.f, 0.f);
-          if constexpr (uu == 0 || 2 * uu == M) {  // c2r ignores these imaginary parts
-            a.y = 0.f;
-            b.y = 0.f;
-          }
-          zz[uu] = make_float2(a.x - b.y, a.y + b.x);  // a + i b
-          if constexpr (uu != 0 && 2 * uu != M) zz[M - uu] = make_float2(a.x + b.y, b.x - a.y);
+          for (int c = 0; c < M; ++c)
+            if (c < crop) dst[c] = z[c];
+        }
+      } else {
+        const int jl = t % G, h = (t / G) & 1, u = t / (2 * G);
+        const float2* src = raw + u * RS + jl;
+        float2 z[32];
+        static_for<0, 32>([&](auto Vv) {
+          constexpr int v = decltype(Vv)::value;
+          const float2 a0 = act1 ? src[v * G] : make_float2(0.f, 0.f);
+          const float2 a1 = act1 ? src[(v + 32) * G] : make_float2(0.f, 0.f);
+          const float2 d = csub(a0, a1);
+          if constexpr (v == 0) z[v] = h ? d : cadd(a0, a1);
+          else z[v] = h ? cmul(d, tw128c<true, v * 2>()) : cadd(a0, a1);
         });
-      }
-      named_bar_sync(bar, CT);  // the stage is free: refill it S groups ahead
-      if (t == 0) {
-        mbar_arrive(&empty[s]);
-        issue(i + S);
-      }
-      if (act) {
-        fft_reg<M, true>(zz);
-        float* dst = p.out + (long long)r * p.out_sr + (long long)(j0 + jl) * p.out_sj + c;
+        named_bar_sync(bar, T::P1W);
+        if (act1 && jl < jv) {
+          if (FCB_XFORM_EXP != 1) fft_reg<32, true>(z);
+          float2* dst = inter + jl * PS + u * CP + h;
 #pragma unroll
-        for (int row = 0; row < M; ++row) {
-          if (row < crop) {
-            dst[0] = zz[row].x * scale;
-            if (hb) dst[H] = zz[row].y * scale;
-            dst += crop;
-          }
+          for (int k = 0; k < 32; ++k)
+            if (2 * k + h < crop) dst[2 * k] = z[k];
         }
       }
-    } else {
-      // one Hermitian column per thread: the half-length pre-twiddle is
-      // formed straight from shared memory (X[k], X[H-k] pairs), so the
-      // 33-entry column is never held whole in registers
-      const bool act = t < jv * crop;
-      const int jl = act ? t / crop : 0, c = t - jl * crop;
-      constexpr int H = M / 2;
-      float2 z[H];
-      {
-        const float2* col = inter + jl * PS + c;
-        static_for<0, H>([&](auto K) {
-          constexpr int k = decltype(K)::value;
-          float2 xk = act ? col[k * CP] : make_float2(0.f, 0.f);
-          float2 xc = cconj(act ? col[(H - k) * CP] : make_float2(0.f, 0.f));
-          if constexpr (k == 0) {  // c2r ignores Im X[0] and Im X[H]
-            xk.y = 0.f;
-            xc.y = 0.f;
-          }
-          const float2 e = cadd(xk, xc);
-          float2 o = csub(xk, xc);
-          if constexpr (k != 0) o = cmul(o, tw128c<true, k * (128 / M)>());
-          z[k] = make_float2(e.x - o.y, e.y + o.x);  // e + i*o
-        });
-      }
-      named_bar_sync(bar, CT);
-      if (t == 0) {
-        mbar_arrive(&empty[s]);
-        issue(i + S);
-      }
-      if (act) {
-        fft_reg<H, true>(z);
-        float* dst = p.out + (long long)r * p.out_sr + (long long)(j0 + jl) * p.out_sj + c;
+      mbar_arrive(&mid[s]);
+      if (t == 0) XTRACE(2, i);
+    }
+  } else {
+    // ------------------------------------------------ pass 2: Hermitian c2r over u -> HBM
+    const int pipe = (threadIdx.x - 32 - T::NPIPE * T::P1W) / T::P2W;
+    const int t = threadIdx.x - 32 - T::NPIPE * T::P1W - pipe * T::P2W;
+    const float scale = p.scale;
+#pragma unroll 1
+    for (int i = pipe;; i += T::NPIPE) {
+      const int g = blockIdx.x + i * gridDim.x;
+      if (g >= ngroups) break;
+      const int s = i % S;
+      const int r = g / ngj, j0 = (g - r * ngj) * G;
+      const int jv = min(G, p.J - j0);
+      const float2* inter = reinterpret_cast<const float2*>(smem + s * T::STAGE);
+      mbar_wait(&mid[s], (i / S) & 1);
+      if constexpr (!T::BIG) {
+        // (plane, column-pair) items packed densely over the valid planes;
+        // columns (c, c + H) form one complex inverse FFT
+        const int H = (crop + 1) >> 1;
+        const bool act = t < jv * H;
+        const int jl = act ? t / H : 0, c = t - jl * H;
+        const bool hb = c + H < crop;
+        float2 zz[M];
+        {
+          const float2* col = inter + jl * PS + c;
+          static_for<0, PC>([&](auto U) {
+            constexpr int uu = decltype(U)::value;
+            float2 a = act ? col[uu * CP] : make_float2(0.f, 0.f);
+            float2 b = (act && hb) ? col[uu * CP + H] : make_float2(0.f, 0.f);
+            if constexpr (uu == 0 || 2 * uu == M) {  // c2r ignores these imaginary parts
+              a.y = 0.f;
+              b.y = 0.f;
+            }
+            zz[uu] = make_float2(a.x - b.y, a.y + b.x);  // a + i b
+            if constexpr (uu != 0 && 2 * uu != M) zz[M - uu] = make_float2(a.x + b.y, b.x - a.y);
+          });
+        }
+        if (p.bulk) {
+          named_bar_sync(1 + T::NPIPE + pipe, T::P2W);  // stage read: reuse it as the output tile
+          if (act) {
+            if (FCB_XFORM_EXP != 1) fft_reg<M, true>(zz);
+            float* tile = reinterpret_cast<float*>(smem + s * T::STAGE) + jl * crop * crop + c;
 #pragma unroll
-        for (int i2 = 0; i2 < H; ++i2) {
-          if (2 * i2 < crop) dst[(2 * i2) * crop] = z[i2].x * scale;
-          if (2 * i2 + 1 < crop) dst[(2 * i2 + 1) * crop] = z[i2].y * scale;
+            for (int row = 0; row < M; ++row) {
+              if (row < crop) {
+                tile[0] = zz[row].x * scale;
+                if (hb) tile[H] = zz[row].y * scale;
+              }
+              tile += crop;
+            }
+          }
+          fence_proxy_async_smem();  // the tile is read by the bulk store (async proxy)
+          mbar_arrive(&outb[s]);
+        } else {
+          mbar_arrive(&empty[s]);  // operands in registers: the stage may be refilled
+          if (t == 0) XTRACE(3, i);
+          if (act) {
+            if (FCB_XFORM_EXP != 1) fft_reg<M, true>(zz);
+            float* dst = p.out + (long long)r * p.out_sr + (long long)(j0 + jl) * p.out_sj + c;
+#pragma unroll
+            for (int row = 0; row < M; ++row) {
+              if (row < crop && FCB_XFORM_EXP != 2) {
+                dst[0] = zz[row].x * scale;
+                if (hb) dst[H] = zz[row].y * scale;
+              }
+              dst += crop;
+            }
+          }
+        }
+        if (t == 0) XTRACE(4, i);
+      } else {
+        // one Hermitian column per thread: the half-length pre-twiddle is
+        // formed straight from shared memory (X[k], X[H-k] pairs), so the
+        // 33-entry column is never held whole in registers
+        const bool act = t < jv * crop;
+        const int jl = act ? t / crop : 0, c = t - jl * crop;
+        constexpr int H = M / 2;
+        float2 z[H];
+        {
+          const float2* col = inter + jl * PS + c;
+          static_for<0, H>([&](auto K) {
+            constexpr int k = decltype(K)::value;
+            float2 xk = act ? col[k * CP] : make_float2(0.f, 0.f);
+            float2 xc = cconj(act ? col[(H - k) * CP] : make_float2(0.f, 0.f));
+            if constexpr (k == 0) {  // c2r ignores Im X[0] and Im X[H]
+              xk.y = 0.f;
+              xc.y = 0.f;
+            }
+            const float2 e = cadd(xk, xc);
+            float2 o = csub(xk, xc);
+            if constexpr (k != 0) o = cmul(o, tw128c<true, k * (128 / M)>());
+            z[k] = make_float2(e.x - o.y, e.y + o.x);  // e + i*o
+          });
+        }
+        if (p.bulk) {
+          named_bar_sync(1 + T::NPIPE + pipe, T::P2W);
+          if (act) {
+            if (FCB_XFORM_EXP != 1) fft_reg<H, true>(z);
+            float* tile = reinterpret_cast<float*>(smem + s * T::STAGE) + jl * crop * crop + c;
+#pragma unroll
+            for (int i2 = 0; i2 < H; ++i2) {
+              if (2 * i2 < crop) tile[(2 * i2) * crop] = z[i2].x * scale;
+              if (2 * i2 + 1 < crop) tile[(2 * i2 + 1) * crop] = z[i2].y * scale;
+            }
+          }
+          fence_proxy_async_smem();
+          mbar_arrive(&outb[s]);
+        } else {
+          mbar_arrive(&empty[s]);
+          if (act) {
+            if (FCB_XFORM_EXP != 1) fft_reg<H, true>(z);
+            float* dst = p.out + (long long)r * p.out_sr + (long long)(j0 + jl) * p.out_sj + c;
+#pragma unroll
+            for (int i2 = 0; i2 < H; ++i2) {
+              if (2 * i2 < crop) dst[(2 * i2) * crop] = z[i2].x * scale;
+              if (2 * i2 + 1 < crop) dst[(2 * i2 + 1) * crop] = z[i2].y * scale;
+            }
+          }
         }
       }
     }
   }
+#ifdef FCB_XFORM_TRACE
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const long long t0 = g_xform_trace[0][0];
+    for (int i = 0; i < 14; ++i)
+      printf("c2r grp %2d load %7lld full %7lld p1done %7lld p2read %7lld p2done %7lld\n", i,
+             g_xform_trace[0][i] - t0, g_xform_trace[1][i] - t0, g_xform_trace[2][i] - t0,
+             g_xform_trace[3][i] - t0, g_xform_trace[4][i] - t0);
+  }
+#endif
 }
 
 }  // namespace fcb

@@ -73,15 +73,23 @@ static PassNeed pass_need(Pass pass, size_t S, size_t f, size_t fo, size_t m) {
   switch (pass) {
     case kFprop:
       return {bins * S * 2 * round_up(f, 16), bins * fo * 2 * round_up(f, 16),
-              bins * fo * 2 * round_up(S, 2)};
+              bins * fo * 2 * round_up(S, 16)};
     case kBprop:
       return {bins * S * 2 * round_up(fo, 16), bins * f * 2 * round_up(fo, 16),
-              bins * f * 2 * round_up(S, 2)};
+              bins * f * 2 * round_up(S, 16)};
     default:
       return {bins * fo * 2 * round_up(S, 16), bins * f * 2 * round_up(S, 16),
-              bins * f * 2 * round_up(fo, 2)};
+              bins * f * 2 * round_up(fo, 16)};
   }
 }
+
+// Product-spectrum layouts written by the GEMM epilogue:
+//   kBinMajor   P[t][n][ld]         (ld >= M, even) -- m = 64 K4 and the
+//                                    debug hook
+//   kGroupMajor P[n][m/16][t][16]   every 16-plane K4 group is one
+//                                    contiguous bins x 128-B block (one bulk
+//                                    load instead of bins scattered rows)
+enum OutLayout { kBinMajor = 0, kGroupMajor = 1 };
 
 // ------------------------------------------------------------ driver API
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -336,9 +344,22 @@ static void launch_c2r_ws(const C2RParams& p, const DevInfo& di, cudaStream_t st
   launch_pdl(kern, dim3(grid), dim3(Tr::THREADS), Tr::SMEM, st, p);
 }
 
+static_assert(FCB_C2R_G == 16, "group-major products hold 16-plane K4 groups");
+
+// Layout the GEMM writes for K4 at fft size m (group-major where the TMA K4
+// kernel groups 16 planes).
+static OutLayout c2r_layout(size_t m) {
+  return (m >= 4 && m <= 32 && !legacy_xform()) ? kGroupMajor : kBinMajor;
+}
+
 template <int M>
-static void launch_c2r_tma(const C2RParams& p, const DevInfo& di, cudaStream_t st) {
+static void launch_c2r_tma(C2RParams p, const DevInfo& di, cudaStream_t st) {
   using T = TC2R<M>;
+  // staged output tiles go out as 1-D bulk stores: planes must be 16-B aligned
+  p.bulk = ((reinterpret_cast<uintptr_t>(p.out) & 15) == 0 && (p.out_sr % 4) == 0 &&
+            (p.out_sj % 4) == 0 && ((size_t)p.crop * p.crop) % 4 == 0)
+               ? 1
+               : 0;
   auto kern = c2r_tma_kernel<M>;
   smem_optin(kern, T::SMEM);
   const size_t bins = (size_t)M * (M / 2 + 1);
@@ -409,9 +430,10 @@ static GemmGeom gemm_geom(size_t M, size_t N, const DevInfo& di) {
 
 // D[t] = A[t] . conj(B[t])^T per bin; im_sign = -1 returns conj(D) (the
 // accGrad orientation, conj(A) . B).  A: F[t][M][2*kpad], B: F[t][N][2*kpad].
+
 static void launch_gemm(const float* A, const float* B, float* out, size_t bins, size_t M,
-                        size_t N, size_t kpad, float im_sign, size_t ldm, const DevInfo& di,
-                        cudaStream_t st) {
+                        size_t N, size_t kpad, float im_sign, OutLayout lay, size_t ldm,
+                        const DevInfo& di, cudaStream_t st) {
   const GemmGeom g = gemm_geom(M, N, di);
   CUtensorMap ta = make_operand_map(A, kpad, M, bins, kTileM);
   CUtensorMap tb = make_operand_map(B, kpad, N, bins, (uint32_t)g.nc);
@@ -426,7 +448,16 @@ static void launch_gemm(const float* A, const float* B, float* out, size_t bins,
   p.nc = g.nc;
   p.stages = g.stages;
   p.im_sign = im_sign;
-  p.ldm = (int)ldm;
+  if (lay == kBinMajor) {
+    p.s_t = (long long)N * ldm;
+    p.s_mg = 16;
+    p.s_n = (long long)ldm;
+  } else {
+    const long long mg = (long long)((M + 15) / 16);
+    p.s_t = 16;
+    p.s_mg = (long long)bins * 16;
+    p.s_n = mg * (long long)bins * 16;
+  }
   smem_optin(cgemm_bins_tcgen05, (int)g.smem);
   const long long tiles = (long long)bins * g.m_tiles * g.n_tiles;
   const int grid = (int)std::min<long long>(tiles, di.sms);
@@ -586,10 +617,11 @@ void run_forward(fftconv_b200_ws* ws, const float* x, size_t S, size_t f, size_t
   const int nl = launch_r2c_both(m, a, b, st, ws->di);
   record(ws, 1, st);  // both forward transforms
   record(ws, 2, st);
-  launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, S, fo, kp, 1.0f, round_up(S, 2), ws->di, st);
+  launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, S, fo, kp, 1.0f, c2r_layout(m), round_up(S, 2), ws->di, st);
   record(ws, 3, st);
   C2RParams c{ws->bufD, y, (long long)(no * no), (long long)(fo * no * no), (int)fo, (int)S,
               (int)no, 0, 0, 1.0f / (float)(m * m), (int)round_up(S, 2)};
+  c.gm = c2r_layout(m) == kGroupMajor;
   launch_c2r(m, c, st, ws->di);
   record(ws, 4, st);
   ws->last_launches = nl + 2;
@@ -621,10 +653,11 @@ void run_grad_input(fftconv_b200_ws* ws, const float* gy, size_t S, size_t fo, s
   const int nl = launch_r2c_both(m, a, b, st, ws->di);
   record(ws, 1, st);  // both forward transforms
   record(ws, 2, st);
-  launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, S, f, kp, 1.0f, round_up(S, 2), ws->di, st);
+  launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, S, f, kp, 1.0f, c2r_layout(m), round_up(S, 2), ws->di, st);
   record(ws, 3, st);
   C2RParams c{ws->bufD, gx, (long long)(n * n), (long long)(f * n * n), (int)f, (int)S, (int)n,
               0, 0, 1.0f / (float)(m * m), (int)round_up(S, 2)};
+  c.gm = c2r_layout(m) == kGroupMajor;
   launch_c2r(m, c, st, ws->di);
   record(ws, 4, st);
   ws->last_launches = nl + 2;
@@ -658,10 +691,11 @@ void run_grad_weight(fftconv_b200_ws* ws, const float* gy, size_t Sg, size_t fo,
   const int nl = launch_r2c_both(m, a, b, st, ws->di);
   record(ws, 1, st);  // both forward transforms
   record(ws, 2, st);
-  launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, fo, f, kp, -1.0f, round_up(fo, 2), ws->di, st);
+  launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, fo, f, kp, -1.0f, c2r_layout(m), round_up(fo, 2), ws->di, st);
   record(ws, 3, st);
   C2RParams c{ws->bufD, gw, (long long)(k * k), (long long)(f * k * k), (int)f, (int)fo, (int)k,
               0, 0, 1.0f / (float)(m * m), (int)round_up(fo, 2)};
+  c.gm = c2r_layout(m) == kGroupMajor;
   launch_c2r(m, c, st, ws->di);
   record(ws, 4, st);
   ws->last_launches = nl + 2;
@@ -962,7 +996,7 @@ int fftconv_b200_debug_cgemm(const float* a, const float* b, float* out, size_t 
     if (mode == 1)  // A . B = A . conj(conj(B))
       conj_inplace_kernel<<<256, 256, 0, st>>>(reinterpret_cast<float2*>(B),
                                                (long long)(bins * N * kp));
-    launch_gemm(A, B, out, bins, M, N, kp, mode == 2 ? -1.0f : 1.0f, M, di, st);
+    launch_gemm(A, B, out, bins, M, N, kp, mode == 2 ? -1.0f : 1.0f, kBinMajor, M, di, st);
     FCB_CUDA(cudaStreamSynchronize(st));
     cudaFree(A);
     cudaFree(B);
