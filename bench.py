@@ -333,10 +333,10 @@ def main():
     # dominant kernel = largest total time across the step
     tot = {}
     for s_ in stages:
-        key = {"r2c": "r2c_ws_kernel", "c2r": "c2r_ws_kernel"}.get(s_["kernel"][:3], s_["kernel"])
+        key = {"r2c": "r2c_tma_kernel", "c2r": "c2r_tma_kernel"}.get(s_["kernel"][:3], s_["kernel"])
         tot[key] = tot.get(key, 0.0) + s_["ms"]
     dom = max(tot, key=tot.get)
-    dom_st = [s_ for s_ in stages if {"r2c": "r2c_ws_kernel", "c2r": "c2r_ws_kernel"}.get(
+    dom_st = [s_ for s_ in stages if {"r2c": "r2c_tma_kernel", "c2r": "c2r_tma_kernel"}.get(
         s_["kernel"][:3], s_["kernel"]) == dom]
     dom_ms = statistics.mean(s_["ms"] for s_ in dom_st)
     if dom == "cgemm_bins_tcgen05":
