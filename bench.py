@@ -374,10 +374,26 @@ def main():
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
         h2d = 4 * (x.size + w.size + gy.size + w.size + gy.size + x.size)
         d2h = 4 * (y_h.size + gx_h.size + gw_h.size)
+        # the PCIe floor of this traffic on this box: pinned copies of the same
+        # sizes, each direction alone (the step's three calls are synchronous)
+        def copy_ms(nbytes, to_dev):
+            hbuf = torch.empty(nbytes // 4, dtype=torch.float32).pin_memory()
+            dbuf = torch.empty(nbytes // 4, dtype=torch.float32, device=dev)
+            best = 1e9
+            for _ in range(3):
+                t0 = time.perf_counter()
+                (dbuf.copy_(hbuf, non_blocking=True) if to_dev else hbuf.copy_(dbuf, non_blocking=True))
+                torch.cuda.synchronize()
+                best = min(best, (time.perf_counter() - t0) * 1e3)
+            return best
+        h2d_ms, d2h_ms = copy_ms(int(h2d), True), copy_ms(int(d2h), False)
         e2e = {"value": statistics.mean(e2e_ms), "unit": "ms", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h),
+               "pcie_floor_ms": {"h2d_alone": h2d_ms, "d2h_alone": d2h_ms,
+                                 "h2d_GBps": h2d / h2d_ms / 1e6, "d2h_GBps": d2h / d2h_ms / 1e6},
                "path": "ConvWorkspace.forward/grad_input/grad_weight(out=) on pinned numpy -> "
-                       "fftconv_b200_*_host C ABI (H2D inputs, compute, D2H result, sync per call)"}
+                       "fftconv_b200_*_host C ABI; each call pipelined over minibatch chunks "
+                       "(H2D / compute / D2H on three streams), synchronous per call"}
 
     # ---- CPU reference beside it (rank 0, N=1 only)
     cpu = None

@@ -390,6 +390,7 @@ struct C2RParams {
   int ld;       // row stride of P in complex elements (>= J, even)
   int bulk;     // 1: output planes 16-B aligned -> staged + bulk-stored (K4 TMA kernel)
   int gm;       // 1: P is group-major P[r][J/16][t][16] (K4 TMA kernel, m <= 32)
+  int accum;    // 1: add into the output (direct-store mode; chunked accGrad)
 };
 
 // grid = (ceil(J/G), R, ceil(crop/cc)), block = PlaneTraits<M>::THREADS.

@@ -616,8 +616,8 @@ __global__ void __launch_bounds__(TC2R<M>::THREADS, 1)
 #pragma unroll
             for (int row = 0; row < M; ++row) {
               if (row < crop && FCB_XFORM_EXP != 2) {
-                dst[0] = zz[row].x * scale;
-                if (hb) dst[H] = zz[row].y * scale;
+                dst[0] = zz[row].x * scale + (p.accum ? dst[0] : 0.f);
+                if (hb) dst[H] = zz[row].y * scale + (p.accum ? dst[H] : 0.f);
               }
               dst += crop;
             }
@@ -668,8 +668,10 @@ __global__ void __launch_bounds__(TC2R<M>::THREADS, 1)
             float* dst = p.out + (long long)r * p.out_sr + (long long)(j0 + jl) * p.out_sj + c;
 #pragma unroll
             for (int i2 = 0; i2 < H; ++i2) {
-              if (2 * i2 < crop) dst[(2 * i2) * crop] = z[i2].x * scale;
-              if (2 * i2 + 1 < crop) dst[(2 * i2 + 1) * crop] = z[i2].y * scale;
+              float* d0 = dst + (2 * i2) * crop;
+              float* d1 = d0 + crop;
+              if (2 * i2 < crop) *d0 = z[i2].x * scale + (p.accum ? *d0 : 0.f);
+              if (2 * i2 + 1 < crop) *d1 = z[i2].y * scale + (p.accum ? *d1 : 0.f);
             }
           }
         }

@@ -356,7 +356,7 @@ template <int M>
 static void launch_c2r_tma(C2RParams p, const DevInfo& di, cudaStream_t st) {
   using T = TC2R<M>;
   // staged output tiles go out as 1-D bulk stores: planes must be 16-B aligned
-  p.bulk = ((reinterpret_cast<uintptr_t>(p.out) & 15) == 0 && (p.out_sr % 4) == 0 &&
+  p.bulk = (!p.accum && (reinterpret_cast<uintptr_t>(p.out) & 15) == 0 && (p.out_sr % 4) == 0 &&
             (p.out_sj % 4) == 0 && ((size_t)p.crop * p.crop) % 4 == 0)
                ? 1
                : 0;
@@ -476,6 +476,8 @@ __global__ void conj_inplace_kernel(float2* v, long long n) {
 using namespace fcb;
 
 // ------------------------------------------------------------ workspace
+constexpr int kMaxChunks = 16;
+
 struct fftconv_b200_ws {
   int device = 0;
   DevInfo di;
@@ -494,7 +496,10 @@ struct fftconv_b200_ws {
   float* st_in1 = nullptr;
   float* st_out = nullptr;
   size_t n_in0 = 0, n_in1 = 0, n_out = 0;
-  cudaStream_t host_stream = nullptr;
+  cudaStream_t host_stream = nullptr;  // compute stream of the host-pointer entry points
+  cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+  cudaEvent_t pev[2][kMaxChunks + 1] = {};  // chunk pipeline: inputs landed / outputs ready
+  bool pev_ready = false;
   uint64_t ctr[3] = {0, 0, 0};
   std::string last_error;
   bool timing = false;
@@ -668,7 +673,7 @@ void run_grad_input(fftconv_b200_ws* ws, const float* gy, size_t S, size_t fo, s
 
 void run_grad_weight(fftconv_b200_ws* ws, const float* gy, size_t Sg, size_t fo, size_t gr,
                      size_t gc, const float* x, size_t Sx, size_t f, size_t xr, size_t xc,
-                     float* gw, cudaStream_t st) {
+                     float* gw, cudaStream_t st, bool accum = false) {
   require_nonzero(Sg, fo, gr, gc, "Tensor4");
   require_nonzero(Sx, f, xr, xc, "Tensor4");
   if (gr != gc) throw Error(FFTCONV_B200_SIZE_ERROR, "grad_weight_fft: planes must be square");
@@ -696,6 +701,7 @@ void run_grad_weight(fftconv_b200_ws* ws, const float* gy, size_t Sg, size_t fo,
   C2RParams c{ws->bufD, gw, (long long)(k * k), (long long)(f * k * k), (int)f, (int)fo, (int)k,
               0, 0, 1.0f / (float)(m * m), (int)round_up(fo, 2)};
   c.gm = c2r_layout(m) == kGroupMajor;
+  c.accum = accum;
   launch_c2r(m, c, st, ws->di);
   record(ws, 4, st);
   ws->last_launches = nl + 2;
@@ -704,11 +710,6 @@ void run_grad_weight(fftconv_b200_ws* ws, const float* gy, size_t Sg, size_t fo,
   ws->ctr[2] += (uint64_t)bins * fo * f * S;
 }
 
-// Host-pointer staging helpers.
-void stage_in(fftconv_b200_ws* ws, float*& dst, size_t& have, const float* src, size_t n) {
-  grow(dst, have, n);
-  FCB_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(float), cudaMemcpyHostToDevice, ws->host_stream));
-}
 
 }  // namespace
 
@@ -738,6 +739,11 @@ int fftconv_b200_ws_create(const fftconv_b200_layer* configs, size_t count, int 
       DeviceGuard g(device);
       ws->di = dev_info(device);
       FCB_CUDA(cudaStreamCreateWithFlags(&ws->host_stream, cudaStreamNonBlocking));
+      FCB_CUDA(cudaStreamCreateWithFlags(&ws->h2d_stream, cudaStreamNonBlocking));
+      FCB_CUDA(cudaStreamCreateWithFlags(&ws->d2h_stream, cudaStreamNonBlocking));
+      for (auto& row : ws->pev)
+        for (auto& e : row) FCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ws->pev_ready = true;
       // Size the frequency buffers for every registered layer and pass up
       // front, so timed calls never allocate.
       size_t na = 0, nb = 0, nd = 0;
@@ -767,6 +773,11 @@ void fftconv_b200_ws_destroy(fftconv_b200_ws* ws) {
     for (float* p : {ws->freq, ws->st_in0, ws->st_in1, ws->st_out})
       if (p) cudaFree(p);
     if (ws->host_stream) cudaStreamDestroy(ws->host_stream);
+    if (ws->h2d_stream) cudaStreamDestroy(ws->h2d_stream);
+    if (ws->d2h_stream) cudaStreamDestroy(ws->d2h_stream);
+    if (ws->pev_ready)
+      for (auto& row : ws->pev)
+        for (auto& e : row) cudaEventDestroy(e);
     if (ws->ev_ready)
       for (auto& e : ws->ev) cudaEventDestroy(e);
   }
@@ -831,6 +842,37 @@ int fftconv_b200_grad_weight(fftconv_b200_ws* ws, const float* gy, size_t S_gy, 
   });
 }
 
+// ---- host-pointer entry points ---------------------------------------
+// The drop-in for Tensor4/Weights4 storage: copy in, compute, copy out.
+// Each call is pipelined over minibatch chunks (fprop/bprop are independent
+// per sample; accGrad sums per-chunk gradients into the output): the H2D
+// copies of chunk c+1 run on h2d_stream while chunk c computes on
+// host_stream and chunk c-1 drains on d2h_stream, so a call costs about one
+// PCIe transfer of its inputs instead of H2D + compute + D2H in series.
+
+namespace {
+
+// Chunks for a host call moving `bytes` of per-sample input: ~6 MB each, so
+// the exposed first H2D / last D2H is ~0.1 ms of PCIe while each chunk's
+// compute (tens of us) still hides under the next chunk's copy.
+int host_chunks(size_t S, size_t bytes, size_t m) {
+  if (m < 4 || legacy_xform()) return 1;  // the fallback kernels do not accumulate
+  const size_t c = (bytes + (6u << 20) - 1) / (6u << 20);
+  return (int)std::max<size_t>(1, std::min<size_t>({c, (size_t)kMaxChunks, S}));
+}
+
+std::pair<size_t, size_t> chunk_range(size_t S, int C, int c) {
+  const size_t base = S / C, extra = S % C;
+  const size_t b0 = c * base + std::min<size_t>(c, extra);
+  return {b0, b0 + base + ((size_t)c < extra ? 1 : 0)};
+}
+
+void h2d(fftconv_b200_ws* ws, float* dst, const float* src, size_t n) {
+  FCB_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(float), cudaMemcpyHostToDevice, ws->h2d_stream));
+}
+
+}  // namespace
+
 int fftconv_b200_forward_host(fftconv_b200_ws* ws, const float* x, size_t S, size_t f,
                               size_t x_rows, size_t x_cols, const float* w, size_t w_out,
                               size_t w_in, size_t k, float* y, unsigned threads) {
@@ -841,20 +883,38 @@ int fftconv_b200_forward_host(fftconv_b200_ws* ws, const float* x, size_t S, siz
     // Shape checks first so errors never touch the device.
     require_nonzero(S, f, x_rows, x_cols, "Tensor4");
     require_nonzero(w_out, w_in, k, 1, "Weights4");
-    const size_t nx = S * f * x_rows * x_cols, nw = w_out * w_in * k * k;
-    const size_t no = (k <= x_rows) ? x_rows - k + 1 : 1;
-    const size_t ny = S * w_out * no * no;
-    if (x_rows == x_cols && w_in == f && k <= x_rows) {
-      prepare(ws, fftconv_b200_layer{k, x_rows, f, w_out, S});
-      stage_in(ws, ws->st_in0, ws->n_in0, x, nx);
-      stage_in(ws, ws->st_in1, ws->n_in1, w, nw);
-      grow(ws->st_out, ws->n_out, ny);
+    if (!(x_rows == x_cols && w_in == f && k <= x_rows)) {  // raises the reference's error
+      run_forward(ws, nullptr, S, f, x_rows, x_cols, nullptr, w_out, w_in, k, nullptr,
+                  ws->host_stream);
+      return;
     }
-    run_forward(ws, ws->st_in0, S, f, x_rows, x_cols, ws->st_in1, w_out, w_in, k, ws->st_out,
-                ws->host_stream);
-    FCB_CUDA(cudaMemcpyAsync(y, ws->st_out, ny * sizeof(float), cudaMemcpyDeviceToHost,
-                             ws->host_stream));
-    FCB_CUDA(cudaStreamSynchronize(ws->host_stream));
+    const size_t n = x_rows, no = n - k + 1, fo = w_out;
+    const size_t m = prepare(ws, fftconv_b200_layer{k, n, f, fo, S});
+    const size_t px = f * n * n, py = fo * no * no, nw = fo * f * k * k;
+    grow(ws->st_in0, ws->n_in0, S * px);
+    grow(ws->st_in1, ws->n_in1, nw);
+    grow(ws->st_out, ws->n_out, S * py);
+    const int C = host_chunks(S, S * px * sizeof(float), m);
+    uint64_t saved[3];
+    std::memcpy(saved, ws->ctr, sizeof saved);
+    h2d(ws, ws->st_in1, w, nw);
+    for (int c = 0; c < C; ++c) {
+      const auto [b0, b1] = chunk_range(S, C, c);
+      h2d(ws, ws->st_in0 + b0 * px, x + b0 * px, (b1 - b0) * px);
+      FCB_CUDA(cudaEventRecord(ws->pev[0][c], ws->h2d_stream));
+      FCB_CUDA(cudaStreamWaitEvent(ws->host_stream, ws->pev[0][c], 0));
+      run_forward(ws, ws->st_in0 + b0 * px, b1 - b0, f, n, n, ws->st_in1, fo, f, k,
+                  ws->st_out + b0 * py, ws->host_stream);
+      FCB_CUDA(cudaEventRecord(ws->pev[1][c], ws->host_stream));
+      FCB_CUDA(cudaStreamWaitEvent(ws->d2h_stream, ws->pev[1][c], 0));
+      FCB_CUDA(cudaMemcpyAsync(y + b0 * py, ws->st_out + b0 * py, (b1 - b0) * py * sizeof(float),
+                               cudaMemcpyDeviceToHost, ws->d2h_stream));
+    }
+    FCB_CUDA(cudaStreamSynchronize(ws->d2h_stream));
+    const uint64_t bins = m * (m / 2 + 1);  // one call = one reference forward
+    ws->ctr[0] = saved[0] + S * f + fo * f;
+    ws->ctr[1] = saved[1] + S * fo;
+    ws->ctr[2] = saved[2] + bins * fo * f * S;
   });
 }
 
@@ -867,20 +927,39 @@ int fftconv_b200_grad_input_host(fftconv_b200_ws* ws, const float* gy, size_t S,
     DeviceGuard g(ws->device);
     require_nonzero(S, fo, gy_rows, gy_cols, "Tensor4");
     require_nonzero(w_out, w_in, k, 1, "Weights4");
-    const size_t n = gy_rows + k - 1;
-    const size_t ngy = S * fo * gy_rows * gy_cols, nw = w_out * w_in * k * k;
-    const size_t ngx = S * w_in * n * n;
-    if (gy_rows == gy_cols && w_out == fo) {
-      prepare(ws, fftconv_b200_layer{k, n, w_in, fo, S});
-      stage_in(ws, ws->st_in0, ws->n_in0, gy, ngy);
-      stage_in(ws, ws->st_in1, ws->n_in1, w, nw);
-      grow(ws->st_out, ws->n_out, ngx);
+    if (!(gy_rows == gy_cols && w_out == fo)) {
+      run_grad_input(ws, nullptr, S, fo, gy_rows, gy_cols, nullptr, w_out, w_in, k, nullptr,
+                     ws->host_stream);
+      return;
     }
-    run_grad_input(ws, ws->st_in0, S, fo, gy_rows, gy_cols, ws->st_in1, w_out, w_in, k,
-                   ws->st_out, ws->host_stream);
-    FCB_CUDA(cudaMemcpyAsync(gx, ws->st_out, ngx * sizeof(float), cudaMemcpyDeviceToHost,
-                             ws->host_stream));
-    FCB_CUDA(cudaStreamSynchronize(ws->host_stream));
+    const size_t no = gy_rows, n = no + k - 1, f = w_in;
+    const size_t m = prepare(ws, fftconv_b200_layer{k, n, f, fo, S});
+    const size_t pgy = fo * no * no, pgx = f * n * n, nw = fo * f * k * k;
+    grow(ws->st_in0, ws->n_in0, S * pgy);
+    grow(ws->st_in1, ws->n_in1, nw);
+    grow(ws->st_out, ws->n_out, S * pgx);
+    const int C = host_chunks(S, S * pgy * sizeof(float), m);
+    uint64_t saved[3];
+    std::memcpy(saved, ws->ctr, sizeof saved);
+    h2d(ws, ws->st_in1, w, nw);
+    for (int c = 0; c < C; ++c) {
+      const auto [b0, b1] = chunk_range(S, C, c);
+      h2d(ws, ws->st_in0 + b0 * pgy, gy + b0 * pgy, (b1 - b0) * pgy);
+      FCB_CUDA(cudaEventRecord(ws->pev[0][c], ws->h2d_stream));
+      FCB_CUDA(cudaStreamWaitEvent(ws->host_stream, ws->pev[0][c], 0));
+      run_grad_input(ws, ws->st_in0 + b0 * pgy, b1 - b0, fo, no, no, ws->st_in1, fo, f, k,
+                     ws->st_out + b0 * pgx, ws->host_stream);
+      FCB_CUDA(cudaEventRecord(ws->pev[1][c], ws->host_stream));
+      FCB_CUDA(cudaStreamWaitEvent(ws->d2h_stream, ws->pev[1][c], 0));
+      FCB_CUDA(cudaMemcpyAsync(gx + b0 * pgx, ws->st_out + b0 * pgx,
+                               (b1 - b0) * pgx * sizeof(float), cudaMemcpyDeviceToHost,
+                               ws->d2h_stream));
+    }
+    FCB_CUDA(cudaStreamSynchronize(ws->d2h_stream));
+    const uint64_t bins = m * (m / 2 + 1);
+    ws->ctr[0] = saved[0] + S * fo + fo * f;
+    ws->ctr[1] = saved[1] + S * f;
+    ws->ctr[2] = saved[2] + bins * fo * f * S;
   });
 }
 
@@ -894,20 +973,37 @@ int fftconv_b200_grad_weight_host(fftconv_b200_ws* ws, const float* gy, size_t S
     DeviceGuard g(ws->device);
     require_nonzero(S_gy, fo, gy_rows, gy_cols, "Tensor4");
     require_nonzero(S_x, f, x_rows, x_cols, "Tensor4");
-    const size_t ngy = S_gy * fo * gy_rows * gy_cols, nx = S_x * f * x_rows * x_cols;
-    const size_t k = (gy_rows <= x_rows) ? x_rows - gy_rows + 1 : 1;
-    const size_t ngw = fo * f * k * k;
-    if (gy_rows == gy_cols && x_rows == x_cols && S_gy == S_x && gy_rows <= x_rows) {
-      prepare(ws, fftconv_b200_layer{k, x_rows, f, fo, S_x});
-      stage_in(ws, ws->st_in0, ws->n_in0, gy, ngy);
-      stage_in(ws, ws->st_in1, ws->n_in1, x, nx);
-      grow(ws->st_out, ws->n_out, ngw);
+    if (!(gy_rows == gy_cols && x_rows == x_cols && S_gy == S_x && gy_rows <= x_rows)) {
+      run_grad_weight(ws, nullptr, S_gy, fo, gy_rows, gy_cols, nullptr, S_x, f, x_rows, x_cols,
+                      nullptr, ws->host_stream);
+      return;
     }
-    run_grad_weight(ws, ws->st_in0, S_gy, fo, gy_rows, gy_cols, ws->st_in1, S_x, f, x_rows,
-                    x_cols, ws->st_out, ws->host_stream);
+    const size_t S = S_x, no = gy_rows, n = x_rows, k = n - no + 1;
+    const size_t m = prepare(ws, fftconv_b200_layer{k, n, f, fo, S});
+    const size_t pgy = fo * no * no, px = f * n * n, ngw = fo * f * k * k;
+    grow(ws->st_in0, ws->n_in0, S * pgy);
+    grow(ws->st_in1, ws->n_in1, S * px);
+    grow(ws->st_out, ws->n_out, ngw);
+    const int C = host_chunks(S, S * (pgy + px) * sizeof(float), m);
+    uint64_t saved[3];
+    std::memcpy(saved, ws->ctr, sizeof saved);
+    for (int c = 0; c < C; ++c) {
+      const auto [b0, b1] = chunk_range(S, C, c);
+      h2d(ws, ws->st_in0 + b0 * pgy, gy + b0 * pgy, (b1 - b0) * pgy);
+      h2d(ws, ws->st_in1 + b0 * px, x + b0 * px, (b1 - b0) * px);
+      FCB_CUDA(cudaEventRecord(ws->pev[0][c], ws->h2d_stream));
+      FCB_CUDA(cudaStreamWaitEvent(ws->host_stream, ws->pev[0][c], 0));
+      // gw = sum over minibatch chunks (batch decomposability)
+      run_grad_weight(ws, ws->st_in0 + b0 * pgy, b1 - b0, fo, no, no, ws->st_in1 + b0 * px,
+                      b1 - b0, f, n, n, ws->st_out, ws->host_stream, /*accum=*/c > 0);
+    }
     FCB_CUDA(cudaMemcpyAsync(gw, ws->st_out, ngw * sizeof(float), cudaMemcpyDeviceToHost,
                              ws->host_stream));
     FCB_CUDA(cudaStreamSynchronize(ws->host_stream));
+    const uint64_t bins = m * (m / 2 + 1);
+    ws->ctr[0] = saved[0] + S * f + S * fo;
+    ws->ctr[1] = saved[1] + fo * f;
+    ws->ctr[2] = saved[2] + bins * fo * f * S;
   });
 }
 
