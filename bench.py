@@ -181,6 +181,8 @@ def main():
                     help="nccl (one GPU per rank); gloo lets ranks share a GPU for testing")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.config.startswith("stack"):
+        return run_stack(args)
     cfg, label = parse_config(args.config)
     if args.impl == "reference":
         return run_reference_arm(args, cfg, label)
@@ -433,6 +435,70 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_stack(args):
+    """--config stack[:preset]: one full training iteration (forward through
+    all stages, loss, backward with every weight gradient) of a layer-stack
+    preset (layers.hpp:321-348, run_iteration :441-609) on one GPU; the
+    reference arm runs the reference's own run_iteration on the host cores."""
+    import oracle
+    from paper_1312_5851_b200 import layers
+
+    name = args.config.split(":", 1)[1] if ":" in args.config else "reference-net"
+    spec = layers.preset_network(name)
+    S, seed = spec.default_batch, 1234
+    metric = f"ms per training iteration ({name} preset, S={S})"
+    base = {"metric": metric, "unit": "ms", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (reference init_params / make_batch, seed 1234)",
+            "config": {"workload": f"{name}: " + "; ".join(
+                f"conv {s.conv.kernel} {s.conv.image} {s.conv.in_maps} {s.conv.out_maps}" if s.kind == 0
+                else ("fc %d" % s.fc_outputs if s.kind == 3 else s.kind.name) for s in spec.stages),
+                "S": S, "parallelism": "dp1"}}
+    if args.impl == "reference":
+        th = cpu_threads()
+        t = []
+        for _ in range(max(1, args.steps)):
+            _, r = oracle.ref_run_iteration(spec.records(), S, seed, engine=1, threads=th)
+            t.append(r["update_output_ms"] + r["update_grad_input_ms"] + r["acc_grad_ms"])
+        ms = statistics.mean(t)
+        line = dict(base, value=ms, ms_per_step=ms, impl="reference",
+                    cpu_baseline={"value": ms, "unit": "ms", "cores": th, "kind": "reference",
+                                  "sample": f"reference run_iteration<float> (FFT engine), {len(t)} iterations"},
+                    e2e={"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
+        print(json.dumps(line), flush=True)
+        return
+    import torch
+
+    dev = torch.device("cuda", 0)
+    params = layers.init_params(spec, seed)
+    batch = torch.from_numpy(layers.make_batch(spec, S, seed)).to(dev)
+    ws = __import__("paper_1312_5851_b200").ConvWorkspace(spec.conv_configs(S), device=0)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    for _ in range(args.warmup):
+        layers.run_iteration(spec, params, batch, ws=ws)
+    cats = {"update_output_ms": [], "update_grad_input_ms": [], "acc_grad_ms": []}
+    wall = []
+    sampler = ClockSampler(0)
+    sampler.start()
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = layers.run_iteration(spec, params, batch, ws=ws)
+        wall.append((time.perf_counter() - t0) * 1e3)
+        for k in cats:
+            cats[k].append(getattr(r.times, k))
+    clocks = sampler.stop()
+    per = {k: statistics.mean(v) for k, v in cats.items()}
+    ms = sum(per.values())
+    line = dict(base, value=ms, ms_per_step=ms, per_category_ms=per,
+                wall_ms_incl_param_upload=statistics.mean(wall), loss=r.loss, grad_checksum=r.grad_checksum,
+                clocks=clocks, gpu_launches=None,
+                note="value = device time of the three reference categories (CUDA events); conv stages on the "
+                     "B200 kernels, relu/pool/fit_to on the layer-stack kernels, fc on fp32 cuBLAS")
+    print(json.dumps(line), flush=True)
 
 
 def ncu_traffic(kernel, config):

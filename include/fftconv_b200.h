@@ -125,6 +125,27 @@ int fftconv_b200_stage_ms(fftconv_b200_ws* ws, float out[4]);
 /* Number of kernel launches the last operator call enqueued. */
 int fftconv_b200_last_launch_count(const fftconv_b200_ws* ws);
 
+/* ---- Layer-stack stages (training-step driver, layers.hpp) ---------------
+ * Device pointers, enqueued on `stream`.  Used by the stack driver
+ * (paper_1312_5851_b200/layers.py) around the convolution operators. */
+/* relu_forward / relu_backward  layers.hpp:88-109 (n elements). */
+int fftconv_b200_relu_forward(const float* x, float* y, size_t n, void* stream);
+int fftconv_b200_relu_backward(const float* gy, const float* x, float* gx, size_t n,
+                               void* stream);
+/* maxpool_forward  layers.hpp:34-66: 2x2 / stride 2 over `planes` planes of
+ * rows x cols (both even, else FFTCONV_B200_SIZE_ERROR); argmax[o] = flat
+ * index of the winner inside its input plane (ties: earliest, row-major). */
+int fftconv_b200_maxpool_forward(const float* x, size_t planes, size_t rows, size_t cols,
+                                 float* y, uint32_t* argmax, void* stream);
+/* maxpool_backward  layers.hpp:68-83: gx (planes x rows x cols) = gy routed
+ * to each window's winner, zero elsewhere. */
+int fftconv_b200_maxpool_backward(const float* gy, const uint32_t* argmax, size_t planes,
+                                  size_t rows, size_t cols, float* gx, void* stream);
+/* fit_to  layers.hpp:393-407: every plane padded with zeros or cropped at
+ * the top-left corner to size x size. */
+int fftconv_b200_fit_to(const float* x, size_t planes, size_t rows, size_t cols, float* y,
+                        size_t size, void* stream);
+
 /* ---- Unit-level test hooks (K1 / K4 / K3 in isolation) ------------------ */
 
 /* Forward 2-D real transforms of `planes` square src x src planes

@@ -17,6 +17,8 @@
 //   fftconv::fill_uniform, uniform_at        rng.hpp:32-47
 //   fftconv::run_op_bench                    bench.hpp:80-145
 //   fftconv::random_verify_configs, verify_sweep  bench.hpp:164-222
+//   fftconv::preset_network / parse_network_string / init_params /
+//     make_batch / run_iteration        layers.hpp:321-609
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -28,6 +30,7 @@
 #include "fftconv/conv_direct.hpp"
 #include "fftconv/conv_fft.hpp"
 #include "fftconv/fft.hpp"
+#include "fftconv/layers.hpp"
 #include "fftconv/rng.hpp"
 
 namespace {
@@ -277,6 +280,62 @@ void ref_random_verify_configs(size_t count, uint64_t seed, uint64_t* out) {
     out[5 * i + 3] = v[i].out_maps;
     out[5 * i + 4] = v[i].batch;
   }
+}
+
+// One training iteration of a network (layers.hpp:441-609) with the
+// reference's own parameters and batch (init_params / make_batch, seed).
+// The network arrives as stage records {kind, k, n, f, f' | fc outputs}
+// (kind: 0 conv, 1 relu, 2 pool, 3 fc) and is validated by the reference's
+// NetworkSpec::validate; parse_network's istringstream is not used because
+// this library carries its own static libstdc++ next to the host process's.
+// engine: 0 direct, 1 fft.  out_grads receives, in order, every conv weight
+// gradient, then the fc weight and bias gradients (grads_cap floats
+// available; the length needed goes to *grads_len).  scalars: loss,
+// grad_checksum, update_output_ms, update_grad_input_ms, acc_grad_ms,
+// grad_input_calls.
+int ref_run_iteration_f32(const uint64_t* stages, size_t nstages, size_t S, uint64_t seed,
+                          int engine, unsigned threads, float* out_grads, size_t grads_cap,
+                          size_t* grads_len, double* scalars) {
+  return guarded([&] {
+    fftconv::NetworkSpec net;
+    for (size_t i = 0; i < nstages; ++i) {
+      const uint64_t* r = stages + 5 * i;
+      fftconv::Stage st;
+      st.kind = static_cast<fftconv::StageKind>(r[0]);
+      if (st.kind == fftconv::StageKind::conv) st.conv = fftconv::LayerConfig{r[1], r[2], r[3], r[4], 1};
+      if (st.kind == fftconv::StageKind::fc) st.fc_outputs = r[4];
+      net.stages.push_back(st);
+    }
+    if (!net.stages.empty() && net.stages.front().kind == fftconv::StageKind::conv) {
+      net.input_maps = net.stages.front().conv.in_maps;
+      net.input_image = net.stages.front().conv.image;
+    }
+    net.validate();
+    auto params = fftconv::init_params<float>(net, seed);
+    auto batch = fftconv::make_batch<float>(net, S, seed);
+    auto r = fftconv::run_iteration<float>(
+        net, params, batch, engine ? fftconv::Engine::fft : fftconv::Engine::direct, nullptr, threads);
+    size_t n = 0;
+    for (const auto& g : r.conv_weight_grads) n += g.size();
+    n += r.fc_weight_grad.size() + r.fc_bias_grad.size();
+    *grads_len = n;
+    if (out_grads && grads_cap >= n) {
+      size_t o = 0;
+      for (const auto& g : r.conv_weight_grads) {
+        std::memcpy(out_grads + o, g.data().data(), g.size() * sizeof(float));
+        o += g.size();
+      }
+      std::memcpy(out_grads + o, r.fc_weight_grad.data(), r.fc_weight_grad.size() * sizeof(float));
+      o += r.fc_weight_grad.size();
+      std::memcpy(out_grads + o, r.fc_bias_grad.data(), r.fc_bias_grad.size() * sizeof(float));
+    }
+    scalars[0] = r.loss;
+    scalars[1] = r.grad_checksum;
+    scalars[2] = r.times.update_output_ms;
+    scalars[3] = r.times.update_grad_input_ms;
+    scalars[4] = r.times.acc_grad_ms;
+    scalars[5] = (double)r.grad_input_calls;
+  });
 }
 
 }  // extern "C"

@@ -26,6 +26,7 @@
 #include "cgemm_tcgen05.cuh"
 #include "fft_planes.cuh"
 #include "fft_tma.cuh"
+#include "layers.cuh"
 
 namespace fcb {
 
@@ -1099,4 +1100,75 @@ int fftconv_b200_debug_cgemm(const float* a, const float* b, float* out, size_t 
   });
 }
 
+// ---- layer-stack stages (layers.hpp) -----------------------------------
+
+namespace {
+int ew_grid(long long n) {
+  return (int)std::max<long long>(1, std::min<long long>((n + 255) / 256, 148LL * 16));
+}
+}  // namespace
+
+int fftconv_b200_relu_forward(const float* x, float* y, size_t n, void* stream) {
+  return guarded(nullptr, [&] {
+    cudaStream_t st = (cudaStream_t)stream;
+    const long long n4 = (long long)n / 4;
+    if (n4) relu_fwd_kernel<<<ew_grid(n4), 256, 0, st>>>(reinterpret_cast<const float4*>(x),
+                                                       reinterpret_cast<float4*>(y), n4);
+    if (n % 4) relu_fwd_tail<<<1, 4, 0, st>>>(x, y, 4 * n4, (long long)n);
+    FCB_CUDA(cudaGetLastError());
+  });
+}
+
+int fftconv_b200_relu_backward(const float* gy, const float* x, float* gx, size_t n,
+                               void* stream) {
+  return guarded(nullptr, [&] {
+    cudaStream_t st = (cudaStream_t)stream;
+    const long long n4 = (long long)n / 4;
+    if (n4)
+      relu_bwd_kernel<<<ew_grid(n4), 256, 0, st>>>(reinterpret_cast<const float4*>(gy),
+                                                  reinterpret_cast<const float4*>(x),
+                                                  reinterpret_cast<float4*>(gx), n4);
+    if (n % 4) relu_bwd_tail<<<1, 4, 0, st>>>(gy, x, gx, 4 * n4, (long long)n);
+    FCB_CUDA(cudaGetLastError());
+  });
+}
+
+int fftconv_b200_maxpool_forward(const float* x, size_t planes, size_t rows, size_t cols,
+                                 float* y, uint32_t* argmax, void* stream) {
+  return guarded(nullptr, [&] {
+    if (rows % 2 || cols % 2)
+      throw Error(FFTCONV_B200_SIZE_ERROR, "maxpool: rows and cols must be even");
+    const long long total = (long long)planes * (rows / 2) * (cols / 2);
+    if (total)
+      maxpool_fwd_kernel<<<ew_grid(total), 256, 0, (cudaStream_t)stream>>>(
+          x, y, argmax, (long long)planes, (int)rows, (int)cols);
+    FCB_CUDA(cudaGetLastError());
+  });
+}
+
+int fftconv_b200_maxpool_backward(const float* gy, const uint32_t* argmax, size_t planes,
+                                  size_t rows, size_t cols, float* gx, void* stream) {
+  return guarded(nullptr, [&] {
+    if (rows % 2 || cols % 2)
+      throw Error(FFTCONV_B200_SIZE_ERROR, "maxpool: rows and cols must be even");
+    const long long total = (long long)planes * (rows / 2) * (cols / 2);
+    if (total)
+      maxpool_bwd_kernel<<<ew_grid(total), 256, 0, (cudaStream_t)stream>>>(
+          gy, argmax, gx, (long long)planes, (int)rows, (int)cols);
+    FCB_CUDA(cudaGetLastError());
+  });
+}
+
+int fftconv_b200_fit_to(const float* x, size_t planes, size_t rows, size_t cols, float* y,
+                        size_t size, void* stream) {
+  return guarded(nullptr, [&] {
+    const long long total = (long long)planes * size * size;
+    if (total)
+      fit_to_kernel<<<ew_grid(total), 256, 0, (cudaStream_t)stream>>>(
+          x, y, (long long)planes, (int)rows, (int)cols, (int)size);
+    FCB_CUDA(cudaGetLastError());
+  });
+}
+
 }  // extern "C"
+

@@ -1,0 +1,102 @@
+"""Layer-stack stages and one full training iteration on the GPU against the
+reference (layers.hpp): relu / max-pool / fit_to kernels vs numpy
+restatements of layers.hpp:34-109 and :393-407, and run_iteration on the
+reference-net-small preset vs the reference's own run_iteration (FFT engine)
+on identical parameters and batch."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1312_5851_b200 import layers
+
+pytestmark = pytest.mark.gpu
+
+
+def _t(a, dev):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+
+def test_relu(dev):
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal((3, 5, 7, 9)).astype(np.float32)   # 945 elements: vector body + tail
+    gy = rng.standard_normal(x.shape).astype(np.float32)
+    xd = _t(x, dev)
+    assert np.array_equal(layers.relu_forward(xd).cpu().numpy(), np.where(x > 0, x, 0))
+    assert np.array_equal(layers.relu_backward(_t(gy, dev), xd).cpu().numpy(), np.where(x > 0, gy, 0))
+
+
+def _pool_ref(x):
+    S, M, R, Cc = x.shape
+    y = np.zeros((S, M, R // 2, Cc // 2), np.float32)
+    arg = np.zeros(y.shape, np.int64)
+    for b in range(S):
+        for m in range(M):
+            for i in range(R // 2):
+                for j in range(Cc // 2):
+                    best = 2 * i * Cc + 2 * j
+                    bv = x[b, m].reshape(-1)[best]
+                    for di in range(2):
+                        for dj in range(2):
+                            p = (2 * i + di) * Cc + 2 * j + dj
+                            if x[b, m].reshape(-1)[p] > bv:
+                                bv, best = x[b, m].reshape(-1)[p], p
+                    y[b, m, i, j], arg[b, m, i, j] = bv, best
+    return y, arg
+
+
+def test_maxpool(dev):
+    rng = np.random.default_rng(2)
+    x = rng.integers(-3, 3, (2, 3, 6, 8)).astype(np.float32)  # many ties: earliest element wins
+    y_ref, arg_ref = _pool_ref(x)
+    y, arg, shape = layers.maxpool_forward(_t(x, dev))
+    assert np.array_equal(y.cpu().numpy(), y_ref)
+    assert np.array_equal(arg.cpu().numpy(), arg_ref)
+    gy = rng.standard_normal(y_ref.shape).astype(np.float32)
+    gx = layers.maxpool_backward(_t(gy, dev), (y, arg, shape)).cpu().numpy()
+    gx_ref = np.zeros_like(x)
+    for b in range(2):
+        for m in range(3):
+            flat = gx_ref[b, m].reshape(-1)
+            for i in range(3):
+                for j in range(4):
+                    flat[arg_ref[b, m, i, j]] += gy[b, m, i, j]
+    assert np.array_equal(gx, gx_ref)
+
+
+@pytest.mark.parametrize("size", [5, 8, 11])
+def test_fit_to(dev, size):
+    x = np.arange(2 * 3 * 8 * 8, dtype=np.float32).reshape(2, 3, 8, 8)
+    got = layers.fit_to(_t(x, dev), size).cpu().numpy()
+    ref = np.zeros((2, 3, size, size), np.float32)
+    r = min(size, 8)
+    ref[:, :, :r, :r] = x[:, :, :r, :r]
+    assert np.array_equal(got, ref)
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / np.linalg.norm(b))
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="reference library not built")
+def test_run_iteration_matches_reference(dev):
+    spec = layers.preset_network("reference-net-small")
+    seed, S = 1234, spec.default_batch
+    params = layers.init_params(spec, seed)
+    batch = layers.make_batch(spec, S, seed)
+    res = layers.run_iteration(spec, params, batch)
+    ref_flat, ref = oracle.ref_run_iteration(spec.records(), S, seed, engine=1)
+    assert res.grad_input_calls == int(ref["grad_input_calls"]) == 4
+    assert abs(res.loss - ref["loss"]) <= 1e-5 * abs(ref["loss"])
+    off = 0
+    for g in res.conv_weight_grads:
+        n = g.numel()
+        assert _rel(g.cpu().numpy().reshape(-1), ref_flat[off:off + n]) <= 1e-4
+        off += n
+    n = res.fc_weight_grad.numel()
+    assert _rel(res.fc_weight_grad.cpu().numpy().reshape(-1), ref_flat[off:off + n]) <= 1e-5
+    off += n
+    assert _rel(res.fc_bias_grad.cpu().numpy(), ref_flat[off:]) <= 1e-6
+    assert abs(res.grad_checksum - ref["grad_checksum"]) <= 1e-4 * abs(ref["grad_checksum"])
+    assert res.times.total_ms() > 0
