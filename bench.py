@@ -414,6 +414,15 @@ def main():
         except Exception as exc:  # reported, never fatal
             cpu = {"value": None, "unit": "ms", "cores": None, "kind": "reference", "sample": f"failed: {exc}"}
 
+    # fusion-proof pass-level roofline: sum of the stage
+    # floors at the measured peaks over the measured pass time
+    from paper_1312_5851_b200 import cost_model
+
+    stage_us = {op: {"r2c": 1e3 * (stage_ms[op][0] + stage_ms[op][1]), "gemm": 1e3 * stage_ms[op][2],
+                     "c2r": 1e3 * stage_ms[op][3]} for op in OPS}
+    pass_roof = {op: {k: round(v, 4) for k, v in r.items()}
+                 for op, r in cost_model.roofline_report(lcfg, stage_us, hbm_gbs, tf32x3_tflops).items()}
+
     E = 2 * S * f * fo * no * no * k * k
     line = {
         "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -425,6 +434,7 @@ def main():
         "tflops_equiv": 3 * E / (ms * 1e-3) / 1e12,
         "per_op_ms": {op: sum(stage_ms[op]) for op in OPS},
         "roofline": roofline,
+        "pass_roofline": pass_roof,
         "stages": stages,
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks,

@@ -258,6 +258,7 @@ def ref_lib():
     L.ref_resolve_threads.restype = C.c_uint
     L.ref_random_verify_configs.argtypes = [_sz, _u64, _p]
     L.ref_run_iteration_f32.argtypes = [_p, _sz, _sz, _u64, C.c_int, C.c_uint, _p, _sz, C.POINTER(_sz), _p]
+    L.ref_cost_model.argtypes = [_sz, _sz, _sz, _sz, _sz, C.c_double, C.c_int, _p]
     return L
 
 
@@ -359,3 +360,13 @@ def ref_run_iteration(stages, S: int, seed: int, engine: int = 1, threads: int =
     keys = ("loss", "grad_checksum", "update_output_ms", "update_grad_input_ms", "acc_grad_ms",
             "grad_input_calls")
     return g, dict(zip(keys, (float(v) for v in sc)))
+
+
+def ref_cost_model(k, n, f, fo, S, C, op):
+    """cost_model.hpp ops_* (op 0 forward, 1 grad_input, 2 grad_weight) and
+    memory_bytes / packed_memory_bytes(4)."""
+    out = np.zeros(6, dtype=np.float64)
+    code = ref_lib().ref_cost_model(k, n, f, fo, S, C, op, _ptr(out))
+    if code:
+        raise OracleError(code, ref_lib().ref_last_error().decode())
+    return out

@@ -29,6 +29,7 @@
 #include "fftconv/bench.hpp"
 #include "fftconv/conv_direct.hpp"
 #include "fftconv/conv_fft.hpp"
+#include "fftconv/cost_model.hpp"
 #include "fftconv/fft.hpp"
 #include "fftconv/layers.hpp"
 #include "fftconv/rng.hpp"
@@ -335,6 +336,22 @@ int ref_run_iteration_f32(const uint64_t* stages, size_t nstages, size_t S, uint
     scalars[3] = r.times.update_grad_input_ms;
     scalars[4] = r.times.acc_grad_ms;
     scalars[5] = (double)r.grad_input_calls;
+  });
+}
+
+// cost_model.hpp:39-110: op 0/1/2 -> {direct, transform, pointwise, inverse}
+// counts; out[4] = memory_bytes, out[5] = packed_memory_bytes(4 bytes).
+int ref_cost_model(size_t k, size_t n, size_t f, size_t fo, size_t S, double C, int op, double* out) {
+  return guarded([&] {
+    fftconv::CostParams p{{k, n, f, fo, S}, C};
+    fftconv::OpCounts c = op == 0 ? fftconv::ops_forward(p)
+                                  : (op == 1 ? fftconv::ops_grad_input(p) : fftconv::ops_grad_weight(p));
+    out[0] = c.direct_ops;
+    out[1] = c.transform_ops;
+    out[2] = c.pointwise_ops;
+    out[3] = c.inverse_ops;
+    out[4] = (double)fftconv::memory_bytes(p.config);
+    out[5] = (double)fftconv::packed_memory_bytes(p.config, 4);
   });
 }
 
