@@ -58,6 +58,12 @@ __device__ long long g_xform_trace[6][64];
   } while (0)
 #endif
 
+// Output-tile stores the copy engine keeps in flight before it recycles the
+// oldest stage (the refill lags by as many groups): one with a deep ring,
+// none with three stages (measured: K1 at P 41 -> 39 us with one in flight;
+// the 3-stage m = 64 kernels lose ~13% with one)
+__host__ __device__ constexpr int stores_inflight(int stages) { return stages >= 6 ? 1 : 0; }
+
 #ifndef FCB_C2R_G
 #define FCB_C2R_G 16  // planes per K4 group at m <= 32
 #endif
@@ -213,9 +219,12 @@ __global__ void __launch_bounds__(TR2C<M>::THREADS, 1)
           for (int k = 0; k < T::NBOX; ++k)
             tma_store_3d(tm, st + k * T::BT * G * 8, 2 * q.j0, q.r, k * T::BT);
         bulk_commit_group();
-        bulk_wait_group_read<0>();  // the store has read the tile: refill the stage
-        XTRACE(5, i);
-        issue_load(i + S);
+        constexpr int D = stores_inflight(S);
+        if (i >= D) {  // the store of group i-D has read its tile: refill its stage
+          bulk_wait_group_read<D>();
+          XTRACE(5, i);
+          issue_load(i - D + S);
+        }
       }
       bulk_wait_group<0>();  // spectra written before the grid completes
     }
@@ -490,11 +499,15 @@ __global__ void __launch_bounds__(TC2R<M>::THREADS, 1)
               bulk_store(p.out + (long long)r * p.out_sr + (long long)(j0 + jl) * p.out_sj,
                          tile + jl * plane_bytes, plane_bytes);
           bulk_commit_group();
-          bulk_wait_group_read<0>();  // the stores have read the tile: refill the stage
+          constexpr int D = stores_inflight(S);
+          if (i >= D) {  // group i-D's stores have read their tile: refill its stage
+            bulk_wait_group_read<D>();
+            issue_load(i - D + S);
+          }
         } else {
           mbar_wait(&empty[s], (i / S) & 1);
+          issue_load(i + S);
         }
-        issue_load(i + S);
       }
       if (p.bulk) bulk_wait_group<0>();
     }
