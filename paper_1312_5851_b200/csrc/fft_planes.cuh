@@ -1,4 +1,6 @@
-// K1 (r2c) and K4 (c2r) plane transforms for the FFT convolution path.
+// FFT codelets and the frequency layout shared by the plane transforms, plus
+// the simple one-pass-per-CTA K1/K4 kernels used for m in {1, 2} (the
+// TMA-pipelined kernels for m >= 4 are in fft_tma.cuh).
 //
 // Replaces the reference's per-plane CPU transforms plus the strided
 // bin-major scatter/gather glue:
@@ -259,6 +261,13 @@ struct R2CParams {
   int conj;  // 1: store the conjugate spectrum
 };
 
+// One launch transforms both operands of an operator (A groups first, then
+// B groups) in the TMA kernels.
+struct R2CPair {
+  R2CParams op[2];
+  int n;  // 1 or 2 operands
+};
+
 // grid = (kpad/G, R, ceil((M/2+1)/UC)), block = PlaneTraits<M>::THREADS.
 // smem = G * UC * cpad * sizeof(float2).
 template <int M>
@@ -498,393 +507,6 @@ __global__ void __launch_bounds__(PlaneTraits<M>::THREADS, PlaneTraits<M>::MIN_C
 #pragma unroll
       for (int i = 0; i < M; ++i)
         if (i < p.crop) dst[(long long)i * p.crop] = x[i] * scale;
-    }
-  }
-}
-
-// ======================================================================
-// m in {4, 8, 16, 32}: warp-specialised persistent kernels.
-//
-// Each CTA loops over 16-plane groups.  Producer warps run pass 1 of group
-// i+1 (global loads straight into registers, FFT, write the intermediate)
-// while consumer warps run pass 2 of group i (read the intermediate, FFT,
-// stream the result out), through a double-buffered shared-memory
-// intermediate guarded by named barriers (FULL[b]: producers -> consumers,
-// EMPTY[b]: consumers -> producers).  Loads of the next group therefore
-// overlap the FFTs and stores of the current one instead of alternating
-// within a CTA.
-// ======================================================================
-template <int M>
-struct WsR2CTraits {
-  static constexpr int G = 16;
-  static constexpr int PC = M / 2 + 1;
-  static constexpr int NPAIR = M / 2;
-  static constexpr int P1_THREADS = ((G * NPAIR + 31) / 32) * 32;
-  static constexpr int P2_THREADS = ((G * PC + 31) / 32) * 32;
-  static constexpr int THREADS = P1_THREADS + P2_THREADS;
-  static constexpr int CP = M + 1;  // intermediate row stride (float2), odd
-  static constexpr int BUF = G * PC * CP;
-  static constexpr int SMEM = 2 * BUF * 8;
-};
-
-enum : int { kBarFull0 = 1, kBarEmpty0 = 3 };  // named barrier ids (+buffer)
-
-// One launch transforms both operands of an operator (A groups first, then
-// B groups): the tail of one overlaps the other and a launch gap disappears.
-struct R2CPair {
-  R2CParams op[2];
-  int n;  // 1 or 2 operands
-};
-
-// grid = persistent (<= groups), block = THREADS, smem = SMEM.
-// Groups: g = r * (kpad/16) + jg.
-template <int M>
-__global__ void __launch_bounds__(WsR2CTraits<M>::THREADS, 1) r2c_ws_kernel(const R2CPair P) {
-  using Tr = WsR2CTraits<M>;
-  constexpr int G = Tr::G, PC = Tr::PC, NPAIR = Tr::NPAIR, CP = Tr::CP;
-  constexpr int NT = Tr::THREADS;
-  extern __shared__ __align__(16) float2 ws_s1[];  // [2][G][PC][CP]
-  const int ngA = P.op[0].R * (P.op[0].kpad / G);
-  const int ngroups = ngA + (P.n > 1 ? P.op[1].R * (P.op[1].kpad / G) : 0);
-  pdl_wait();
-  pdl_trigger();
-
-  if (threadIdx.x < Tr::P1_THREADS) {
-    // ---------------- producers: pass 1 (column pairs)
-    const int item = threadIdx.x;
-    const bool act = item < G * NPAIR;
-    const int jl = item / NPAIR, cp = item - (item / NPAIR) * NPAIR;
-    const int c = 2 * cp;
-    int i = 0;
-    for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++i) {
-      const int b = i & 1;
-      const int which = g >= ngA;
-      const R2CParams& p = P.op[which];
-      const int gl = g - which * ngA, ngj = p.kpad / G;
-      const int r = gl / ngj, j0 = (gl - r * ngj) * G;
-      const int src = p.src;
-      float2 z[M];
-      const bool ld = act && (j0 + jl) < p.J && c < src;
-      const bool has_b = c + 1 < src;
-      const float* col = p.in + (long long)r * p.in_sr + (long long)(j0 + jl) * p.in_sj + c;
-#pragma unroll
-      for (int row = 0; row < M; ++row) {
-        z[row].x = (ld && row < src) ? __ldg(col + row * src) : 0.f;
-        z[row].y = (ld && has_b && row < src) ? __ldg(col + row * src + 1) : 0.f;
-      }
-      fft_reg<M, false>(z);
-      if (i >= 2) named_bar_sync(kBarEmpty0 + b, NT);
-      if (act) {
-        float2* dst = ws_s1 + b * Tr::BUF + (jl * PC) * CP + c;
-        static_for<0, PC>([&](auto U) {
-          constexpr int u = decltype(U)::value;
-          const float2 zu = z[u];
-          const float2 zc = cconj(z[(M - u) % M]);
-          dst[u * CP] = make_float2(0.5f * (zu.x + zc.x), 0.5f * (zu.y + zc.y));
-          const float2 d = csub(zu, zc);
-          dst[u * CP + 1] = make_float2(0.5f * d.y, -0.5f * d.x);  // (zu - zc) / (2i)
-        });
-      }
-      named_bar_arrive(kBarFull0 + b, NT);
-    }
-    // balance the consumers' final EMPTY arrivals
-    for (int k = (i >= 2 ? i - 2 : 0); k < i; ++k) named_bar_sync(kBarEmpty0 + (k & 1), NT);
-  } else {
-    // ---------------- consumers: pass 2 (rows) + bin-major stores
-    const int item = threadIdx.x - Tr::P1_THREADS;
-    const bool act = item < G * PC;
-    const int jl = item % G, u = item / G;
-    int i = 0;
-    for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++i) {
-      const int b = i & 1;
-      const int which = g >= ngA;
-      const R2CParams& p = P.op[which];
-      const int gl = g - which * ngA, ngj = p.kpad / G;
-      const int r = gl / ngj, j0 = (gl - r * ngj) * G;
-      const long long bstride = (long long)p.R * p.kpad;  // float2 per bin
-      const float csign = p.conj ? -1.f : 1.f;
-      named_bar_sync(kBarFull0 + b, NT);
-      float2 w[M];
-      if (act) {
-        const float2* row = ws_s1 + b * Tr::BUF + (jl * PC + u) * CP;
-#pragma unroll
-        for (int cc = 0; cc < M; ++cc) w[cc] = row[cc];
-      }
-      named_bar_arrive(kBarEmpty0 + b, NT);
-      if (act) {
-        fft_reg<M, false>(w);
-        float2* o = reinterpret_cast<float2*>(p.out) + (long long)r * p.kpad + j0 + jl +
-                    (long long)(u * M) * bstride;
-#pragma unroll
-        for (int v = 0; v < M; ++v) {
-          *o = make_float2(w[v].x, csign * w[v].y);
-          o += bstride;
-        }
-      }
-    }
-  }
-}
-
-template <int M>
-struct WsC2RTraits {
-  static constexpr int G = 16;
-  static constexpr int PC = M / 2 + 1;
-  static constexpr int P1_THREADS = ((G * PC + 31) / 32) * 32;
-  static constexpr int P2_THREADS = ((G * (M / 2) + 31) / 32) * 32;
-  static constexpr int THREADS = P1_THREADS + P2_THREADS;
-  static constexpr int CP = M + 1;  // odd
-  static constexpr int BUF = G * PC * CP;
-  static constexpr int SMEM = 2 * BUF * 8;
-};
-
-// grid = persistent, groups g = r * ceil(J/16) + jg.  crop <= M.
-template <int M>
-__global__ void __launch_bounds__(WsC2RTraits<M>::THREADS, 1) c2r_ws_kernel(const C2RParams p) {
-  using Tr = WsC2RTraits<M>;
-  constexpr int G = Tr::G, PC = Tr::PC, CP = Tr::CP;
-  constexpr int NT = Tr::THREADS;
-  extern __shared__ __align__(16) float2 ws_s1[];  // [2][G][PC][CP]
-  pdl_wait();
-  pdl_trigger();
-  const int ngj = (p.J + G - 1) / G;
-  const int ngroups = p.R * ngj;
-  const int crop = p.crop;
-  const long long bstride = (long long)p.R * p.ld;  // float2 per bin
-
-  if (threadIdx.x < Tr::P1_THREADS) {
-    // ---------------- producers: inverse row FFT over v (lanes = planes)
-    const int item = threadIdx.x;
-    const bool act = item < G * PC;
-    const int jl = item % G, u = item / G;
-    int i = 0;
-    for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++i) {
-      const int b = i & 1;
-      const int r = g / ngj, j0 = (g - r * ngj) * G;
-      const bool ld = act && (j0 + jl) < p.J;
-      float2 z[M];
-      const float2* srcp = reinterpret_cast<const float2*>(p.in) + (long long)r * p.ld + j0 + jl +
-                           (long long)(u * M) * bstride;
-#pragma unroll
-      for (int v = 0; v < M; ++v) {
-        z[v] = ld ? __ldg(srcp) : make_float2(0.f, 0.f);
-        srcp += bstride;
-      }
-      fft_reg<M, true>(z);
-      if (i >= 2) named_bar_sync(kBarEmpty0 + b, NT);
-      if (act) {
-        float2* dst = ws_s1 + b * Tr::BUF + (jl * PC + u) * CP;
-#pragma unroll
-        for (int cc = 0; cc < M; ++cc)
-          if (cc < crop) dst[cc] = z[cc];
-      }
-      named_bar_arrive(kBarFull0 + b, NT);
-    }
-    for (int k = (i >= 2 ? i - 2 : 0); k < i; ++k) named_bar_sync(kBarEmpty0 + (k & 1), NT);
-  } else {
-    // ---------------- consumers: Hermitian c2r over u, two columns per FFT
-    const int item = threadIdx.x - Tr::P1_THREADS;
-    const int npair = (crop + 1) >> 1;
-    const bool act = item < G * npair;
-    const int jl = act ? item / npair : 0, cp = act ? item - (item / npair) * npair : 0;
-    const int cl = 2 * cp;
-    const bool has_b = cl + 1 < crop;
-    const float scale = p.scale;
-    int i = 0;
-    for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++i) {
-      const int b = i & 1;
-      const int r = g / ngj, j0 = (g - r * ngj) * G;
-      named_bar_sync(kBarFull0 + b, NT);
-      float2 zz[M];
-      if (act) {
-        const float2* colp = ws_s1 + b * Tr::BUF + (jl * PC) * CP + cl;
-        static_for<0, PC>([&](auto U) {
-          constexpr int uu = decltype(U)::value;
-          float2 a = colp[uu * CP];
-          float2 bb = has_b ? colp[uu * CP + 1] : make_float2(0.f, 0.f);
-          if constexpr (uu == 0 || 2 * uu == M) {  // c2r ignores these imaginary parts
-            a.y = 0.f;
-            bb.y = 0.f;
-          }
-          zz[uu] = make_float2(a.x - bb.y, a.y + bb.x);  // a + i b
-          if constexpr (uu != 0 && 2 * uu != M) zz[M - uu] = make_float2(a.x + bb.y, bb.x - a.y);
-        });
-      }
-      named_bar_arrive(kBarEmpty0 + b, NT);
-      if (act && (j0 + jl) < p.J) {
-        fft_reg<M, true>(zz);
-        float* dst = p.out + (long long)r * p.out_sr + (long long)(j0 + jl) * p.out_sj + cl;
-#pragma unroll
-        for (int row = 0; row < M; ++row) {
-          if (row < crop) {
-            dst[0] = zz[row].x * scale;
-            if (has_b) dst[1] = zz[row].y * scale;
-            dst += crop;
-          }
-        }
-      }
-    }
-  }
-}
-
-// ======================================================================
-// m = 64: warp-specialised persistent kernels, 4 planes per group (a 64x33
-// intermediate per plane; double-buffered that is 137 KB).  Pass-1 columns
-// use the half-length real FFT; 64-point complex row FFTs are split into
-// two 32-point halves by one decimation-in-frequency stage so a thread
-// holds 32 complex values.
-// ======================================================================
-struct Ws64 {
-  static constexpr int M = 64, G = 4, PC = 33, CP = 65;
-  static constexpr int BUF = G * PC * CP;             // float2 per buffer
-  static constexpr int SMEM = 2 * BUF * 8;
-  static constexpr int COLS_THREADS = G * M;          // 256: one column per thread
-  static constexpr int ROWS_THREADS = ((G * PC * 2 + 31) / 32) * 32;  // 264 -> 288
-  static constexpr int THREADS = COLS_THREADS + ROWS_THREADS;
-};
-
-// grid = persistent, groups g = r * (kpad/4) + jg.
-__global__ void __maxnreg__(96) r2c_ws64_kernel(const R2CPair P) {
-  constexpr int M = 64, G = Ws64::G, PC = Ws64::PC, CP = Ws64::CP, NT = Ws64::THREADS;
-  extern __shared__ __align__(16) float2 ws_s1[];  // [2][G][PC][CP]
-  const int ngA = P.op[0].R * (P.op[0].kpad / G);
-  const int ngroups = ngA + (P.n > 1 ? P.op[1].R * (P.op[1].kpad / G) : 0);
-  pdl_wait();
-  pdl_trigger();
-  if (threadIdx.x < Ws64::COLS_THREADS) {
-    // ---------------- producers: one real column per thread
-    const int jl = threadIdx.x / M, c = threadIdx.x % M;
-    int i = 0;
-    for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++i) {
-      const int b = i & 1;
-      const int which = g >= ngA;
-      const R2CParams& p = P.op[which];
-      const int gl = g - which * ngA, ngj = p.kpad / G;
-      const int r = gl / ngj, j0 = (gl - r * ngj) * G;
-      const int src = p.src;
-      const bool ld = (j0 + jl) < p.J && c < src;
-      const float* col = p.in + (long long)r * p.in_sr + (long long)(j0 + jl) * p.in_sj + c;
-      float x[M];
-#pragma unroll
-      for (int row = 0; row < M; ++row) x[row] = (ld && row < src) ? __ldg(col + row * src) : 0.f;
-      if (i >= 2) named_bar_sync(kBarEmpty0 + b, NT);
-      float2* dst = ws_s1 + b * Ws64::BUF + (jl * PC) * CP + c;
-      rfft_emit<M>(x, [&](int u, float2 v) { dst[u * CP] = v; });
-      named_bar_arrive(kBarFull0 + b, NT);
-    }
-    for (int k = (i >= 2 ? i - 2 : 0); k < i; ++k) named_bar_sync(kBarEmpty0 + (k & 1), NT);
-  } else {
-    // ---------------- consumers: (plane, u, half) -> 32-point FFT -> v = 2i + h
-    const int item = threadIdx.x - Ws64::COLS_THREADS;
-    const bool act = item < G * PC * 2;
-    const int jl = item % G, h = (item / G) & 1, u = item / (2 * G);
-    int i = 0;
-    for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++i) {
-      const int b = i & 1;
-      const int which = g >= ngA;
-      const R2CParams& p = P.op[which];
-      const int gl = g - which * ngA, ngj = p.kpad / G;
-      const int r = gl / ngj, j0 = (gl - r * ngj) * G;
-      const long long bstride = (long long)p.R * p.kpad;  // float2 per bin
-      const float csign = p.conj ? -1.f : 1.f;
-      named_bar_sync(kBarFull0 + b, NT);
-      float2 z[32];
-      if (act) {
-        const float2* row = ws_s1 + b * Ws64::BUF + (jl * PC + u) * CP;
-        static_for<0, 32>([&](auto Cc) {
-          constexpr int cc = decltype(Cc)::value;
-          const float2 a0 = row[cc], a1 = row[cc + 32];
-          if (h == 0) {
-            z[cc] = cadd(a0, a1);
-          } else {
-            if constexpr (cc == 0) z[cc] = csub(a0, a1);
-            else z[cc] = cmul(csub(a0, a1), tw128c<false, cc * 2>());
-          }
-        });
-      }
-      named_bar_arrive(kBarEmpty0 + b, NT);
-      if (act) {
-        fft_reg<32, false>(z);
-        float2* o = reinterpret_cast<float2*>(p.out) + (long long)r * p.kpad + j0 + jl +
-                    (long long)(u * M + h) * bstride;
-        const long long st2 = 2 * bstride;
-#pragma unroll
-        for (int v = 0; v < 32; ++v) {
-          *o = make_float2(z[v].x, csign * z[v].y);
-          o += st2;
-        }
-      }
-    }
-  }
-}
-
-// grid = persistent, groups g = r * ceil(J/4) + jg.
-__global__ void __maxnreg__(96) c2r_ws64_kernel(const C2RParams p) {
-  constexpr int M = 64, G = Ws64::G, PC = Ws64::PC, CP = Ws64::CP, NT = Ws64::THREADS;
-  extern __shared__ __align__(16) float2 ws_s1[];  // [2][G][PC][CP]
-  pdl_wait();
-  pdl_trigger();
-  const int ngj = (p.J + G - 1) / G;
-  const int ngroups = p.R * ngj;
-  const int crop = p.crop;
-  const long long bstride = (long long)p.R * p.ld;  // float2 per bin
-  if (threadIdx.x >= Ws64::COLS_THREADS) {
-    // ---------------- producers: (plane, u, half) inverse 64-point row FFT
-    const int item = threadIdx.x - Ws64::COLS_THREADS;
-    const bool act = item < G * PC * 2;
-    const int jl = item % G, h = (item / G) & 1, u = item / (2 * G);
-    int i = 0;
-    for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++i) {
-      const int b = i & 1;
-      const int r = g / ngj, j0 = (g - r * ngj) * G;
-      const bool ld = act && (j0 + jl) < p.J;
-      const float2* srcp = reinterpret_cast<const float2*>(p.in) + (long long)r * p.ld + j0 + jl +
-                           (long long)(u * M) * bstride;
-      float2 z[32];
-      static_for<0, 32>([&](auto Vv) {
-        constexpr int v = decltype(Vv)::value;
-        const float2 a0 = ld ? __ldg(srcp + v * bstride) : make_float2(0.f, 0.f);
-        const float2 a1 = ld ? __ldg(srcp + (v + 32) * bstride) : make_float2(0.f, 0.f);
-        if (h == 0) {
-          z[v] = cadd(a0, a1);
-        } else {
-          if constexpr (v == 0) z[v] = csub(a0, a1);
-          else z[v] = cmul(csub(a0, a1), tw128c<true, v * 2>());
-        }
-      });
-      fft_reg<32, true>(z);
-      if (i >= 2) named_bar_sync(kBarEmpty0 + b, NT);
-      if (act) {
-        float2* dst = ws_s1 + b * Ws64::BUF + (jl * PC + u) * CP;
-#pragma unroll
-        for (int k = 0; k < 32; ++k)
-          if (2 * k + h < crop) dst[2 * k + h] = z[k];
-      }
-      named_bar_arrive(kBarFull0 + b, NT);
-    }
-    for (int k = (i >= 2 ? i - 2 : 0); k < i; ++k) named_bar_sync(kBarEmpty0 + (k & 1), NT);
-  } else {
-    // ---------------- consumers: one Hermitian column per thread
-    const int jl = threadIdx.x / M, c = threadIdx.x % M;
-    const bool act = c < crop;
-    const float scale = p.scale;
-    int i = 0;
-    for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++i) {
-      const int b = i & 1;
-      const int r = g / ngj, j0 = (g - r * ngj) * G;
-      named_bar_sync(kBarFull0 + b, NT);
-      float2 X[PC];
-      if (act) {
-        const float2* colp = ws_s1 + b * Ws64::BUF + (jl * PC) * CP + c;
-#pragma unroll
-        for (int uu = 0; uu < PC; ++uu) X[uu] = colp[uu * CP];
-      }
-      named_bar_arrive(kBarEmpty0 + b, NT);
-      if (act && (j0 + jl) < p.J) {
-        float* dst = p.out + (long long)r * p.out_sr + (long long)(j0 + jl) * p.out_sj + c;
-        irfft_emit<M>(X, [&](int row, float v) {
-          if (row < crop) dst[row * crop] = v * scale;
-        });
-      }
     }
   }
 }

@@ -64,6 +64,18 @@ __device__ long long g_xform_trace[6][64];
 // the 3-stage m = 64 kernels lose ~13% with one)
 __host__ __device__ constexpr int stores_inflight(int stages) { return stages >= 6 ? 1 : 0; }
 
+#ifndef FCB_R2C_G
+#define FCB_R2C_G 8  // planes per K1 group at m <= 32
+#endif
+
+// Independent pass-1/pass-2 pipelines: the largest of 4, 2, 1 that divides
+// the stage count (each stage then belongs to one pipeline) and keeps the
+// CTA within 1024 threads.
+__host__ __device__ constexpr int npipe_for(int stages, int fixed, int per_pipe) {
+  return (stages % 4 == 0 && fixed + 4 * per_pipe <= 1024) ? 4
+         : (stages % 2 == 0 && fixed + 2 * per_pipe <= 1024) ? 2 : 1;
+}
+
 #ifndef FCB_C2R_G
 #define FCB_C2R_G 16  // planes per K4 group at m <= 32
 #endif
@@ -92,7 +104,7 @@ struct TR2C {
   // planes (K indices) per group: 8 (64-B spectrum segments; a 16-plane
   // group made 72-KB stages, only 3 of which fit, too shallow to hide the
   // ~4.5k-cycle load latency under load), 4 at m = 64
-  static constexpr int G = BIG ? 4 : 8;
+  static constexpr int G = BIG ? 4 : FCB_R2C_G;
   static constexpr int PC = M / 2 + 1;
   static constexpr int CP = M + 1;        // intermediate row stride (float2)
   static constexpr int BINS = M * PC;
@@ -111,7 +123,7 @@ struct TR2C {
   // independent pass-1/pass-2 pipelines on alternating groups (an even
   // stage count keeps every stage in one parity class, so no mbarrier
   // phase is ever shared between the pipelines)
-  static constexpr int NPIPE = (!BIG && S % 2 == 0) ? 2 : 1;
+  static constexpr int NPIPE = BIG ? 1 : npipe_for(S, 32, P1W + P2W);
   static constexpr int THREADS = 32 + NPIPE * (P1W + P2W);
   static constexpr int SMEM = S * STAGE + 3 * S * 8 + 128;
   // output tile stores: NBOX boxes of BT bins x G planes

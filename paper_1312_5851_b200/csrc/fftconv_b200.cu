@@ -161,7 +161,7 @@ static void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 // Per-kernel host-side caches, keyed by the kernel's address (several
 // kernels share a signature, so a function-local static would be shared).
 static std::mutex g_kcache_mu;
-static std::unordered_map<const void*, int> g_smem_done, g_occ;
+static std::unordered_map<const void*, int> g_smem_done;
 
 // Opt a kernel into > 48 KB dynamic shared memory (once per size).
 template <typename K>
@@ -175,19 +175,19 @@ static void smem_optin(K kern, int bytes) {
   }
 }
 
-template <typename K>
-static int occupancy(K kern, int threads, int smem) {
-  std::lock_guard<std::mutex> lk(g_kcache_mu);
-  auto it = g_occ.find(reinterpret_cast<const void*>(kern));
-  if (it != g_occ.end()) return it->second;
-  int per_sm = 1;
-  FCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
-  return g_occ[reinterpret_cast<const void*>(kern)] = std::max(per_sm, 1);
+
+// ---- K1 / K4 dispatch ----------------------------------------------------
+// m in {4..64}: the TMA-pipelined kernels (fft_tma.cuh).  m in {1, 2} (tiny
+// non-pow2-padded planes of the verification sweeps): the simple
+// one-pass-per-CTA plane kernels (fft_planes.cuh).
+
+static void size_unsupported(size_t m) {
+  throw Error(FFTCONV_B200_SIZE_ERROR,
+              "fft size " + std::to_string(m) + " not supported by the B200 kernels (max 64)");
 }
 
-// ---- K1 ---------------------------------------------------------------
 template <int M>
-static void launch_r2c_legacy(const R2CParams& p, cudaStream_t st) {
+static void launch_r2c_small(const R2CParams& p, cudaStream_t st) {
   using Tr = PlaneTraits<M>;
   auto kern = r2c_planes_kernel<M>;
   const size_t smem = (size_t)Tr::G * Tr::UC * p.cpad * sizeof(float2);
@@ -196,41 +196,16 @@ static void launch_r2c_legacy(const R2CParams& p, cudaStream_t st) {
   launch_pdl(kern, grid, dim3(Tr::THREADS), smem, st, p);
 }
 
-// Warp-specialised kernels: m in {4..32}, or m = 64 with planes wider than
-// 32 (kernels at m = 64 keep 16-plane groups so every store is a full line).
-static bool legacy_xform();
-static bool r2c_ws_capable(size_t m, const R2CParams& p) {
-  if (!legacy_xform()) return m >= 4 && m <= 64;
-  return (m >= 4 && m <= 32) || (m == 64 && p.src > 32);
-}
-
 template <int M>
-static void launch_r2c_ws(const R2CPair& P, const DevInfo& di, cudaStream_t st) {
-  using Tr = WsR2CTraits<M>;
-  auto kern = r2c_ws_kernel<M>;
-  smem_optin(kern, Tr::SMEM);
-  int groups = 0;
-  for (int i = 0; i < P.n; ++i) groups += P.op[i].R * (P.op[i].kpad / Tr::G);
-  const int grid = std::max(1, std::min(groups, di.sms * occupancy(kern, Tr::THREADS, Tr::SMEM)));
-  launch_pdl(kern, dim3(grid), dim3(Tr::THREADS), Tr::SMEM, st, P);
-}
-
-static void launch_r2c_ws64(const R2CPair& P, const DevInfo& di, cudaStream_t st) {
-  smem_optin(r2c_ws64_kernel, Ws64::SMEM);
-  int groups = 0;
-  for (int i = 0; i < P.n; ++i) groups += P.op[i].R * (P.op[i].kpad / Ws64::G);
-  const int grid = std::max(1, std::min(groups, di.sms));
-  launch_pdl(r2c_ws64_kernel, dim3(grid), dim3(Ws64::THREADS), Ws64::SMEM, st, P);
-}
-
-// TMA-fed transforms (fft_tma.cuh) for m in {4..64}; FFTCONV_B200_LEGACY_XFORM=1
-// selects the first-cut register-fed kernels (A/B measurements only).
-static bool legacy_xform() {
-  static const bool v = [] {
-    const char* e = getenv("FFTCONV_B200_LEGACY_XFORM");
-    return e && e[0] == '1';
-  }();
-  return v;
+static void launch_c2r_small(C2RParams p, cudaStream_t st) {
+  using Tr = PlaneTraits<M>;
+  p.cc = p.crop;
+  p.ccpad = (p.cc % 2) ? p.cc : p.cc + 1;
+  auto kern = c2r_planes_kernel<M>;
+  const size_t smem = (size_t)Tr::G * Tr::PC * p.ccpad * sizeof(float2);
+  smem_optin(kern, (int)smem);
+  dim3 grid((p.J + Tr::G - 1) / Tr::G, p.R, 1);
+  launch_pdl(kern, grid, dim3(Tr::THREADS), smem, st, p);
 }
 
 // 3-D fp32 map over a bin-major spectrum X[t][R][2*ld] (complex, ld even)
@@ -268,90 +243,43 @@ static void launch_r2c_tma(const R2CPair& P, const DevInfo& di, cudaStream_t st)
   launch_pdl(kern, dim3(grid), dim3(T::THREADS), T::SMEM, st, P, tm[0], tm[1]);
 }
 
-static void launch_r2c_group(size_t m, const R2CPair& P, cudaStream_t st, const DevInfo& di) {
-  if (!legacy_xform()) {
-    switch (m) {
-      case 4: return launch_r2c_tma<4>(P, di, st);
-      case 8: return launch_r2c_tma<8>(P, di, st);
-      case 16: return launch_r2c_tma<16>(P, di, st);
-      case 32: return launch_r2c_tma<32>(P, di, st);
-      case 64: return launch_r2c_tma<64>(P, di, st);
-    }
-  }
+// Both forward transforms of an operator (one launch at m >= 4; operand A's
+// groups first, then B's).  Returns the number of launches.
+static int launch_r2c_both(size_t m, const R2CParams& a, const R2CParams& b, cudaStream_t st,
+                           const DevInfo& di) {
+  const R2CPair P{{a, b}, 2};
   switch (m) {
-    case 4: return launch_r2c_ws<4>(P, di, st);
-    case 8: return launch_r2c_ws<8>(P, di, st);
-    case 16: return launch_r2c_ws<16>(P, di, st);
-    case 32: return launch_r2c_ws<32>(P, di, st);
-    case 64: return launch_r2c_ws64(P, di, st);
+    case 1: launch_r2c_small<1>(a, st); launch_r2c_small<1>(b, st); return 2;
+    case 2: launch_r2c_small<2>(a, st); launch_r2c_small<2>(b, st); return 2;
+    case 4: launch_r2c_tma<4>(P, di, st); return 1;
+    case 8: launch_r2c_tma<8>(P, di, st); return 1;
+    case 16: launch_r2c_tma<16>(P, di, st); return 1;
+    case 32: launch_r2c_tma<32>(P, di, st); return 1;
+    case 64: launch_r2c_tma<64>(P, di, st); return 1;
+    default: size_unsupported(m);
   }
+  return 0;
 }
 
 static void launch_r2c_one(size_t m, const R2CParams& p, cudaStream_t st, const DevInfo& di) {
-  if (r2c_ws_capable(m, p)) {
-    R2CPair P{{p, p}, 1};
-    return launch_r2c_group(m, P, st, di);
-  }
+  const R2CPair P{{p, p}, 1};
   switch (m) {
-    case 1: return launch_r2c_legacy<1>(p, st);
-    case 2: return launch_r2c_legacy<2>(p, st);
-    case 4: return launch_r2c_legacy<4>(p, st);
-    case 8: return launch_r2c_legacy<8>(p, st);
-    case 16: return launch_r2c_legacy<16>(p, st);
-    case 32: return launch_r2c_legacy<32>(p, st);
-    case 64: return launch_r2c_legacy<64>(p, st);
-    default:
-      throw Error(FFTCONV_B200_SIZE_ERROR,
-                  "fft size " + std::to_string(m) + " not supported by the B200 kernels (max 64)");
+    case 1: return launch_r2c_small<1>(p, st);
+    case 2: return launch_r2c_small<2>(p, st);
+    case 4: return launch_r2c_tma<4>(P, di, st);
+    case 8: return launch_r2c_tma<8>(P, di, st);
+    case 16: return launch_r2c_tma<16>(P, di, st);
+    case 32: return launch_r2c_tma<32>(P, di, st);
+    case 64: return launch_r2c_tma<64>(P, di, st);
+    default: size_unsupported(m);
   }
-}
-
-// Both forward transforms of an operator: one launch when one kernel can
-// take both operands.  Returns the number of launches.
-static int launch_r2c_both(size_t m, const R2CParams& a, const R2CParams& b, cudaStream_t st,
-                           const DevInfo& di) {
-  if (r2c_ws_capable(m, a) && r2c_ws_capable(m, b)) {
-    R2CPair P{{a, b}, 2};
-    launch_r2c_group(m, P, st, di);
-    return 1;
-  }
-  launch_r2c_one(m, a, st, di);
-  launch_r2c_one(m, b, st, di);
-  return 2;
-}
-
-// ---- K4 ---------------------------------------------------------------
-template <int M>
-static void launch_c2r_legacy(C2RParams p, cudaStream_t st) {
-  using Tr = PlaneTraits<M>;
-  constexpr int CCMAX = (M == 64) ? 22 : 32;
-  const int nchunks = (p.crop + CCMAX - 1) / CCMAX;
-  p.cc = (p.crop + nchunks - 1) / nchunks;
-  p.ccpad = (p.cc % 2) ? p.cc : p.cc + 1;
-  auto kern = c2r_planes_kernel<M>;
-  const size_t smem = (size_t)Tr::G * Tr::PC * p.ccpad * sizeof(float2);
-  smem_optin(kern, (int)smem);
-  dim3 grid((p.J + Tr::G - 1) / Tr::G, p.R, nchunks);
-  launch_pdl(kern, grid, dim3(Tr::THREADS), smem, st, p);
-}
-
-template <int M>
-static void launch_c2r_ws(const C2RParams& p, const DevInfo& di, cudaStream_t st) {
-  using Tr = WsC2RTraits<M>;
-  auto kern = c2r_ws_kernel<M>;
-  smem_optin(kern, Tr::SMEM);
-  const int groups = p.R * ((p.J + Tr::G - 1) / Tr::G);
-  const int grid = std::max(1, std::min(groups, di.sms * occupancy(kern, Tr::THREADS, Tr::SMEM)));
-  launch_pdl(kern, dim3(grid), dim3(Tr::THREADS), Tr::SMEM, st, p);
 }
 
 static_assert(FCB_C2R_G == 16, "group-major products hold 16-plane K4 groups");
 
 // Layout the GEMM writes for K4 at fft size m (group-major where the TMA K4
 // kernel groups 16 planes).
-static OutLayout c2r_layout(size_t m) {
-  return (m >= 4 && m <= 32 && !legacy_xform()) ? kGroupMajor : kBinMajor;
-}
+static OutLayout c2r_layout(size_t m) { return (m >= 4 && m <= 32) ? kGroupMajor : kBinMajor; }
 
 template <int M>
 static void launch_c2r_tma(C2RParams p, const DevInfo& di, cudaStream_t st) {
@@ -371,41 +299,15 @@ static void launch_c2r_tma(C2RParams p, const DevInfo& di, cudaStream_t st) {
 }
 
 static void launch_c2r(size_t m, const C2RParams& p, cudaStream_t st, const DevInfo& di) {
-  if (!legacy_xform()) {
-    switch (m) {
-      case 4: return launch_c2r_tma<4>(p, di, st);
-      case 8: return launch_c2r_tma<8>(p, di, st);
-      case 16: return launch_c2r_tma<16>(p, di, st);
-      case 32: return launch_c2r_tma<32>(p, di, st);
-      case 64: return launch_c2r_tma<64>(p, di, st);
-    }
-  }
   switch (m) {
-    case 4: return launch_c2r_ws<4>(p, di, st);
-    case 8: return launch_c2r_ws<8>(p, di, st);
-    case 16: return launch_c2r_ws<16>(p, di, st);
-    case 32: return launch_c2r_ws<32>(p, di, st);
-    case 64: {
-      if (p.crop <= 32) break;  // small crops (gw): 16-plane groups read full lines
-      smem_optin(c2r_ws64_kernel, Ws64::SMEM);
-      const int groups = p.R * ((p.J + Ws64::G - 1) / Ws64::G);
-      const int grid = std::max(1, std::min(groups, di.sms));
-      launch_pdl(c2r_ws64_kernel, dim3(grid), dim3(Ws64::THREADS), Ws64::SMEM, st, p);
-      return;
-    }
-    default: break;
-  }
-  switch (m) {
-    case 1: return launch_c2r_legacy<1>(p, st);
-    case 2: return launch_c2r_legacy<2>(p, st);
-    case 4: return launch_c2r_legacy<4>(p, st);
-    case 8: return launch_c2r_legacy<8>(p, st);
-    case 16: return launch_c2r_legacy<16>(p, st);
-    case 32: return launch_c2r_legacy<32>(p, st);
-    case 64: return launch_c2r_legacy<64>(p, st);
-    default:
-      throw Error(FFTCONV_B200_SIZE_ERROR,
-                  "fft size " + std::to_string(m) + " not supported by the B200 kernels (max 64)");
+    case 1: return launch_c2r_small<1>(p, st);
+    case 2: return launch_c2r_small<2>(p, st);
+    case 4: return launch_c2r_tma<4>(p, di, st);
+    case 8: return launch_c2r_tma<8>(p, di, st);
+    case 16: return launch_c2r_tma<16>(p, di, st);
+    case 32: return launch_c2r_tma<32>(p, di, st);
+    case 64: return launch_c2r_tma<64>(p, di, st);
+    default: size_unsupported(m);
   }
 }
 
@@ -857,7 +759,7 @@ namespace {
 // the exposed first H2D / last D2H is ~0.1 ms of PCIe while each chunk's
 // compute (tens of us) still hides under the next chunk's copy.
 int host_chunks(size_t S, size_t bytes, size_t m) {
-  if (m < 4 || legacy_xform()) return 1;  // the fallback kernels do not accumulate
+  if (m < 4) return 1;  // the small-plane kernels do not accumulate
   const size_t c = (bytes + (6u << 20) - 1) / (6u << 20);
   return (int)std::max<size_t>(1, std::min<size_t>({c, (size_t)kMaxChunks, S}));
 }
