@@ -177,6 +177,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--strong", action="store_true",
+                    help="N>1: split the S-sample minibatch across ranks (default: weak scaling, S per rank)")
     ap.add_argument("--dist-backend", default="nccl",
                     help="nccl (one GPU per rank); gloo lets ranks share a GPU for testing")
     args = ap.parse_args()
@@ -208,14 +210,18 @@ def main():
 
     k, n, f, fo, S = cfg
     no = n - k + 1
-    b0, b1 = shard_range(S, world, rank)
+    # Weak scaling (default): every rank holds a full S-sample shard of an
+    # N*S-sample minibatch (per-GPU work fixed; gw all-reduced).  --strong:
+    # the S-sample minibatch itself is split across the ranks.
+    S_glob = S if (args.strong or world == 1) else S * world
+    b0, b1 = shard_range(S_glob, world, rank)
     Sl = b1 - b0
     lcfg = LayerConfig(k, n, f, fo, Sl)
     # Inputs: the reference generator (same bytes the CPU path consumes), this
     # rank's minibatch slice, resident in HBM before timing starts.
-    x = fill_uniform((S, f, n, n), 1234, ROLE_INPUT)[b0:b1]
+    x = fill_uniform((Sl, f, n, n), 1234, ROLE_INPUT, offset=b0 * f * n * n)
     w = fill_uniform((fo, f, k, k), 1234, ROLE_WEIGHTS)
-    gy = fill_uniform((S, fo, no, no), 1234, ROLE_GRAD_OUTPUT)[b0:b1]
+    gy = fill_uniform((Sl, fo, no, no), 1234, ROLE_GRAD_OUTPUT, offset=b0 * fo * no * no)
     xd, wd, gyd = (torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (x, w, gy))
     ws = ConvWorkspace([lcfg], device=local)
     stream = torch.cuda.current_stream(dev)
@@ -426,9 +432,11 @@ def main():
     E = 2 * S * f * fo * no * no * k * k
     line = {
         "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "ms_per_step": ms, "higher_is_better": False,
+        "scaling": "strong" if (args.strong or world == 1) else "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (reference fill_uniform, seed 1234)",
-        "config": {"workload": label, "k": k, "n": n, "f": f, "f_prime": fo, "S": S, "S_per_gpu": Sl,
+        "config": {"workload": label, "k": k, "n": n, "f": f, "f_prime": fo, "S": S, "global_batch": S_glob,
+                   "S_per_gpu": Sl,
                    "parallelism": f"dp{world} (minibatch-sharded, NCCL all-reduce of gw)" if world > 1 else "dp1",
                    "l2": "flushed between timed steps (256 MiB write)"},
         "tflops_equiv": 3 * E / (ms * 1e-3) / 1e12,

@@ -72,12 +72,12 @@ struct PassNeed {
 static PassNeed pass_need(Pass pass, size_t S, size_t f, size_t fo, size_t m) {
   const size_t bins = m * (m / 2 + 1);
   switch (pass) {
-    case kFprop:
+    case kFprop:  // D is [fo][S] or, swapped, [S][fo]
       return {bins * S * 2 * round_up(f, 16), bins * fo * 2 * round_up(f, 16),
-              bins * fo * 2 * round_up(S, 16)};
+              bins * 2 * std::max(fo * round_up(S, 16), S * round_up(fo, 16))};
     case kBprop:
       return {bins * S * 2 * round_up(fo, 16), bins * f * 2 * round_up(fo, 16),
-              bins * f * 2 * round_up(S, 16)};
+              bins * 2 * std::max(f * round_up(S, 16), S * round_up(f, 16))};
     default:
       return {bins * fo * 2 * round_up(S, 16), bins * f * 2 * round_up(S, 16),
               bins * f * 2 * round_up(fo, 16)};
@@ -501,6 +501,17 @@ void require_nonzero(size_t a, size_t b, size_t c, size_t d, const char* what) {
     throw Error(FFTCONV_B200_SIZE_ERROR, std::string(what) + ": all dimensions must be >= 1");
 }
 
+// GEMM orientation.  fprop / bprop put the minibatch on M, which the
+// tcgen05 tile fixes at 128 rows; a small (e.g. minibatch-sharded) batch
+// wastes most of every tile.  D = A.conj(B)^T equals conj(B.conj(A)^T)^T, so
+// the operands can be swapped (maps on M, batch on N) with the epilogue
+// conjugating, and K4 reads the transposed product (SURVEY.md section 7,
+// hard part 3).  Chosen when it pads less work.
+static bool gemm_swap(size_t M, size_t N) {
+  auto padded = [](size_t rows, size_t cols) { return ((rows + 127) / 128) * round_up(cols, 16); };
+  return padded(N, M) < padded(M, N);
+}
+
 // ---- the three operators (device pointers) ---------------------------
 
 void run_forward(fftconv_b200_ws* ws, const float* x, size_t S, size_t f, size_t xr, size_t xc,
@@ -525,10 +536,18 @@ void run_forward(fftconv_b200_ws* ws, const float* x, size_t S, size_t f, size_t
   const int nl = launch_r2c_both(m, a, b, st, ws->di);
   record(ws, 1, st);  // both forward transforms
   record(ws, 2, st);
-  launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, S, fo, kp, 1.0f, c2r_layout(m), round_up(S, 2), ws->di, st);
-  record(ws, 3, st);
   C2RParams c{ws->bufD, y, (long long)(no * no), (long long)(fo * no * no), (int)fo, (int)S,
               (int)no, 0, 0, 1.0f / (float)(m * m), (int)round_up(S, 2)};
+  if (!gemm_swap(S, fo)) {  // D[t][o][b]: planes (r = o, j = b)
+    launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, S, fo, kp, 1.0f, c2r_layout(m), round_up(S, 2),
+                ws->di, st);
+  } else {  // D^T[t][b][o]: planes (r = b, j = o)
+    launch_gemm(ws->bufB, ws->bufA, ws->bufD, bins, fo, S, kp, -1.0f, c2r_layout(m), round_up(fo, 2),
+                ws->di, st);
+    c = C2RParams{ws->bufD, y, (long long)(fo * no * no), (long long)(no * no), (int)S, (int)fo,
+                  (int)no, 0, 0, 1.0f / (float)(m * m), (int)round_up(fo, 2)};
+  }
+  record(ws, 3, st);
   c.gm = c2r_layout(m) == kGroupMajor;
   launch_c2r(m, c, st, ws->di);
   record(ws, 4, st);
@@ -561,10 +580,18 @@ void run_grad_input(fftconv_b200_ws* ws, const float* gy, size_t S, size_t fo, s
   const int nl = launch_r2c_both(m, a, b, st, ws->di);
   record(ws, 1, st);  // both forward transforms
   record(ws, 2, st);
-  launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, S, f, kp, 1.0f, c2r_layout(m), round_up(S, 2), ws->di, st);
-  record(ws, 3, st);
   C2RParams c{ws->bufD, gx, (long long)(n * n), (long long)(f * n * n), (int)f, (int)S, (int)n,
               0, 0, 1.0f / (float)(m * m), (int)round_up(S, 2)};
+  if (!gemm_swap(S, f)) {  // D[t][f][b]
+    launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, S, f, kp, 1.0f, c2r_layout(m), round_up(S, 2),
+                ws->di, st);
+  } else {  // D^T[t][b][f]
+    launch_gemm(ws->bufB, ws->bufA, ws->bufD, bins, f, S, kp, -1.0f, c2r_layout(m), round_up(f, 2),
+                ws->di, st);
+    c = C2RParams{ws->bufD, gx, (long long)(f * n * n), (long long)(n * n), (int)S, (int)f, (int)n,
+                  0, 0, 1.0f / (float)(m * m), (int)round_up(f, 2)};
+  }
+  record(ws, 3, st);
   c.gm = c2r_layout(m) == kGroupMajor;
   launch_c2r(m, c, st, ws->di);
   record(ws, 4, st);

@@ -38,13 +38,15 @@ def uniform_at(seed: int, role: int, index) -> np.ndarray:
     return 2.0 * ((h >> np.uint64(11)).astype(np.float64) * 2.0 ** -53) - 1.0
 
 
-def fill_uniform(shape, seed: int, role: int, stream: int = 0, dtype=np.float32) -> np.ndarray:
-    """rng.hpp:41-47: static_cast<T> of the double draw, in index order."""
+def fill_uniform(shape, seed: int, role: int, stream: int = 0, dtype=np.float32, offset: int = 0) -> np.ndarray:
+    """rng.hpp:41-47: static_cast<T> of the double draw, in index order.
+    `offset` starts at element `offset` of the stream (a slice of a larger
+    tensor, e.g. one rank's minibatch shard, without generating the rest)."""
     n = int(np.prod(shape))
     r = int(role) | (int(stream) << 8)
     out = np.empty(n, dtype=dtype)
     chunk = 1 << 22
     for s in range(0, n, chunk):
-        idx = np.arange(s, min(n, s + chunk), dtype=np.uint64)
+        idx = np.arange(offset + s, offset + min(n, s + chunk), dtype=np.uint64)
         out[s:s + len(idx)] = uniform_at(seed, r, idx).astype(dtype)
     return out.reshape(shape)

@@ -79,6 +79,19 @@ def test_small_cpu_config_vs_direct_oracle(dev):
     _assert_close(got, _direct64(x, w, gy))
 
 
+# ------------------------------------------------- reoriented GEMM (small batch)
+@pytest.mark.parametrize("cfg", [(7, 32, 96, 96, 16), (5, 16, 40, 24, 3), (11, 64, 64, 48, 8),
+                                 (3, 12, 33, 20, 5)])
+def test_small_batch_swapped_gemm_vs_direct(dev, cfg):
+    """Batches smaller than the maps run the per-bin GEMM transposed (maps on
+    the 128-row tile, conjugated epilogue, K4 reading the transposed product);
+    the results must not change (fprop / bprop; accGrad is unaffected)."""
+    cfg = LayerConfig(*cfg)
+    x, w, gy = _inputs(cfg, 77)
+    got = _run_all(ConvWorkspace([cfg]), x, w, gy, dev)
+    _assert_close(got, _direct64(x, w, gy))
+
+
 # ------------------------------------------------- known answers
 def test_unit_kernel_is_identity(dev):
     """conv_fft_test.cpp:77-85"""

@@ -82,3 +82,10 @@ def test_bench_config_parsing():
     assert cfg == (13, 64, 96, 96, 128)
     cfg, _ = bench.parse_config("wide")
     assert cfg == (11, 64, 256, 256, 128)
+
+
+def test_fill_uniform_offset_is_a_slice():
+    from paper_1312_5851_b200.rng import fill_uniform
+
+    full = fill_uniform((4, 3, 5), 99, 1)
+    assert np.array_equal(fill_uniform((2, 3, 5), 99, 1, offset=2 * 15), full[2:4])
