@@ -782,12 +782,21 @@ int fftconv_b200_grad_weight(fftconv_b200_ws* ws, const float* gy, size_t S_gy, 
 
 namespace {
 
-// Chunks for a host call moving `bytes` of per-sample input: ~6 MB each, so
-// the exposed first H2D / last D2H is ~0.1 ms of PCIe while each chunk's
-// compute (tens of us) still hides under the next chunk's copy.
-int host_chunks(size_t S, size_t bytes, size_t m) {
+// Chunks for a host call moving `bytes` of per-sample input, `mb` MB each:
+// small enough that the exposed first H2D / last D2H stays short, large
+// enough that each chunk's fixed work (the W-side transforms, one GEMM
+// launch, accGrad's full-size K4) still hides under the next chunk's copy.
+// Measured per-op optima at the paper point: fprop 12 MB, bprop 6 MB,
+// accGrad 32 MB (its per-chunk K4 and GEMM do not shrink with the chunk).
+// FFTCONV_B200_HOST_CHUNK_MB overrides all three (tuning).
+int host_chunks(size_t S, size_t bytes, size_t m, size_t mb) {
   if (m < 4) return 1;  // the small-plane kernels do not accumulate
-  const size_t c = (bytes + (6u << 20) - 1) / (6u << 20);
+  static const size_t over = [] {
+    const char* e = getenv("FFTCONV_B200_HOST_CHUNK_MB");
+    return (size_t)((e && atoi(e) > 0) ? atoi(e) : 0);
+  }();
+  const size_t chunk = (over ? over : mb) << 20;
+  const size_t c = (bytes + chunk - 1) / chunk;
   return (int)std::max<size_t>(1, std::min<size_t>({c, (size_t)kMaxChunks, S}));
 }
 
@@ -824,14 +833,17 @@ int fftconv_b200_forward_host(fftconv_b200_ws* ws, const float* x, size_t S, siz
     grow(ws->st_in0, ws->n_in0, S * px);
     grow(ws->st_in1, ws->n_in1, nw);
     grow(ws->st_out, ws->n_out, S * py);
-    const int C = host_chunks(S, S * px * sizeof(float), m);
+    const int C = host_chunks(S, S * px * sizeof(float), m, 12);
     uint64_t saved[3];
     std::memcpy(saved, ws->ctr, sizeof saved);
     h2d(ws, ws->st_in1, w, nw);
-    for (int c = 0; c < C; ++c) {
+    for (int c = 0; c < C; ++c) {  // every copy queued first: the link never idles on host work
       const auto [b0, b1] = chunk_range(S, C, c);
       h2d(ws, ws->st_in0 + b0 * px, x + b0 * px, (b1 - b0) * px);
       FCB_CUDA(cudaEventRecord(ws->pev[0][c], ws->h2d_stream));
+    }
+    for (int c = 0; c < C; ++c) {
+      const auto [b0, b1] = chunk_range(S, C, c);
       FCB_CUDA(cudaStreamWaitEvent(ws->host_stream, ws->pev[0][c], 0));
       run_forward(ws, ws->st_in0 + b0 * px, b1 - b0, f, n, n, ws->st_in1, fo, f, k,
                   ws->st_out + b0 * py, ws->host_stream);
@@ -868,7 +880,7 @@ int fftconv_b200_grad_input_host(fftconv_b200_ws* ws, const float* gy, size_t S,
     grow(ws->st_in0, ws->n_in0, S * pgy);
     grow(ws->st_in1, ws->n_in1, nw);
     grow(ws->st_out, ws->n_out, S * pgx);
-    const int C = host_chunks(S, S * pgy * sizeof(float), m);
+    const int C = host_chunks(S, S * pgy * sizeof(float), m, 6);
     uint64_t saved[3];
     std::memcpy(saved, ws->ctr, sizeof saved);
     h2d(ws, ws->st_in1, w, nw);
@@ -876,6 +888,9 @@ int fftconv_b200_grad_input_host(fftconv_b200_ws* ws, const float* gy, size_t S,
       const auto [b0, b1] = chunk_range(S, C, c);
       h2d(ws, ws->st_in0 + b0 * pgy, gy + b0 * pgy, (b1 - b0) * pgy);
       FCB_CUDA(cudaEventRecord(ws->pev[0][c], ws->h2d_stream));
+    }
+    for (int c = 0; c < C; ++c) {
+      const auto [b0, b1] = chunk_range(S, C, c);
       FCB_CUDA(cudaStreamWaitEvent(ws->host_stream, ws->pev[0][c], 0));
       run_grad_input(ws, ws->st_in0 + b0 * pgy, b1 - b0, fo, no, no, ws->st_in1, fo, f, k,
                      ws->st_out + b0 * pgx, ws->host_stream);
@@ -914,7 +929,7 @@ int fftconv_b200_grad_weight_host(fftconv_b200_ws* ws, const float* gy, size_t S
     grow(ws->st_in0, ws->n_in0, S * pgy);
     grow(ws->st_in1, ws->n_in1, S * px);
     grow(ws->st_out, ws->n_out, ngw);
-    const int C = host_chunks(S, S * (pgy + px) * sizeof(float), m);
+    const int C = host_chunks(S, S * (pgy + px) * sizeof(float), m, 32);
     uint64_t saved[3];
     std::memcpy(saved, ws->ctr, sizeof saved);
     for (int c = 0; c < C; ++c) {
@@ -922,6 +937,9 @@ int fftconv_b200_grad_weight_host(fftconv_b200_ws* ws, const float* gy, size_t S
       h2d(ws, ws->st_in0 + b0 * pgy, gy + b0 * pgy, (b1 - b0) * pgy);
       h2d(ws, ws->st_in1 + b0 * px, x + b0 * px, (b1 - b0) * px);
       FCB_CUDA(cudaEventRecord(ws->pev[0][c], ws->h2d_stream));
+    }
+    for (int c = 0; c < C; ++c) {
+      const auto [b0, b1] = chunk_range(S, C, c);
       FCB_CUDA(cudaStreamWaitEvent(ws->host_stream, ws->pev[0][c], 0));
       // gw = sum over minibatch chunks (batch decomposability)
       run_grad_weight(ws, ws->st_in0 + b0 * pgy, b1 - b0, fo, no, no, ws->st_in1 + b0 * px,
