@@ -270,8 +270,10 @@ __global__ void __launch_bounds__(TR2C<M>::THREADS, 1)
         const float* raw = reinterpret_cast<const float*>(st + r2c_raw_off(jl, PS)) +
                            ((reinterpret_cast<uintptr_t>(pin) & 15) >> 2) + c;
         float2* dst = reinterpret_cast<float2*>(st + jl * PS * 8) + c;
-        auto pass1 = [&](auto full_tag) {
+        // NZ: rows >= NZ are zero (src <= NZ): pruned column FFT
+        auto pass1 = [&](auto full_tag, auto nz_tag) {
           constexpr bool FULL = decltype(full_tag)::value;
+          constexpr int NZ = decltype(nz_tag)::value;
           float2 z[M];
 #pragma unroll
           for (int row = 0; row < M; ++row) {
@@ -279,7 +281,7 @@ __global__ void __launch_bounds__(TR2C<M>::THREADS, 1)
               z[row].x = act ? raw[row * M] : 0.f;
               z[row].y = act ? raw[row * M + M / 2] : 0.f;
             } else {
-              const bool ok = act && row < src;
+              const bool ok = act && row < NZ && row < src;
               z[row].x = ok ? raw[0] : 0.f;
               z[row].y = (ok && hb) ? raw[H] : 0.f;
               raw += src;
@@ -287,7 +289,7 @@ __global__ void __launch_bounds__(TR2C<M>::THREADS, 1)
           }
           named_bar_sync(bar, T::P1W);  // every raw plane is read: overwrite in place
           if (act) {
-            if (FCB_XFORM_EXP != 1) fft_reg<M, false>(z);
+            if (FCB_XFORM_EXP != 1) fft_reg_nz<M, NZ, false>(z);
             static_for<0, PC>([&](auto U) {
               constexpr int u = decltype(U)::value;
               const float2 zu = z[u];
@@ -300,8 +302,11 @@ __global__ void __launch_bounds__(TR2C<M>::THREADS, 1)
             });
           }
         };
-        if (src == M) pass1(std::true_type{});
-        else pass1(std::false_type{});
+        using FT = std::true_type;
+        using FF = std::false_type;
+        if (src == M) pass1(FT{}, std::integral_constant<int, M>{});
+        else if (M >= 16 && src <= M / 4) pass1(FF{}, std::integral_constant<int, (M >= 16 ? M / 4 : M)>{});
+        else pass1(FF{}, std::integral_constant<int, M>{});
       } else {
         // m = 64: one real column per thread (half-length complex FFT)
         const bool act = t < jv * src;
@@ -355,20 +360,24 @@ __global__ void __launch_bounds__(TR2C<M>::THREADS, 1)
         const int jl = t % G, u = t / G;
         const bool valid = act && jl < jv;
         const float2* row = reinterpret_cast<const float2*>(st + jl * PS * 8) + u * CP;
-        auto pass2 = [&](auto full_tag) {
+        auto pass2 = [&](auto full_tag, auto nz_tag) {
           constexpr bool FULL = decltype(full_tag)::value;
+          constexpr int NZ = decltype(nz_tag)::value;  // columns >= NZ are zero
           float2 w[M];
 #pragma unroll
           for (int cc = 0; cc < M; ++cc)
-            w[cc] = (valid && (FULL || cc < src)) ? row[cc] : make_float2(0.f, 0.f);
+            w[cc] = (valid && cc < NZ && (FULL || cc < src)) ? row[cc] : make_float2(0.f, 0.f);
           named_bar_sync(bar, T::P2W);  // the intermediate is read: reuse the stage as the tile
           if (act) {  // invalid (K padding) planes store exact zeros
-            if (FCB_XFORM_EXP != 1) fft_reg<M, false>(w);
+            if (FCB_XFORM_EXP != 1) fft_reg_nz<M, NZ, false>(w);
             tile_row<M>(tile + (u * M) * G + jl, G, w, csign);
           }
         };
-        if (src == M) pass2(std::true_type{});
-        else pass2(std::false_type{});
+        using FT = std::true_type;
+        using FF = std::false_type;
+        if (src == M) pass2(FT{}, std::integral_constant<int, M>{});
+        else if (M >= 16 && src <= M / 4) pass2(FF{}, std::integral_constant<int, (M >= 16 ? M / 4 : M)>{});
+        else pass2(FF{}, std::integral_constant<int, M>{});
       } else {
         // (plane, u, half): one decimation-in-frequency stage splits the
         // 64-point row FFT into two 32-point halves, outputs v = 2k + h
