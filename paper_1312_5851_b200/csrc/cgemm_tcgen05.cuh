@@ -57,7 +57,7 @@ namespace fcb {
 
 struct GemmParams {
   float* out;     // product spectrum, complex element (t, n, m) at
-                  // t*s_t + (m/16)*s_mg + n*s_n + m%16 (see OutLayout)
+                  // t*s_t + (m/gm)*s_mg + n*s_n + m%gm (see OutLayout)
   int bins;
   int m_valid;    // A rows (M)
   int n_valid;    // complex output columns (N)
@@ -67,6 +67,7 @@ struct GemmParams {
   int stages;
   float im_sign;  // +1 (fprop, bprop) or -1 (accGrad)
   long long s_t, s_mg, s_n;  // output strides in complex elements
+  int gm_log2;                // log2 of the m-group size gm
 };
 
 constexpr int kGemmThreads = 640;
@@ -309,7 +310,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int m = mt * kTileM + row;
       const bool mok = m < p.m_valid;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + a * (2 * nc);
-      float2* out = reinterpret_cast<float2*>(p.out) + (long long)t * p.s_t + (m >> 4) * p.s_mg + (m & 15);
+      float2* out = reinterpret_cast<float2*>(p.out) + (long long)t * p.s_t + (m >> p.gm_log2) * p.s_mg +
+                    (m & ((1 << p.gm_log2) - 1));
       for (int nb = half * 16; nb < nc; nb += 32) {
         float re[16], im[16];
         tmem_ld_32x32b_x16(tbase + nb, re);

@@ -87,9 +87,10 @@ static PassNeed pass_need(Pass pass, size_t S, size_t f, size_t fo, size_t m) {
 // Product-spectrum layouts written by the GEMM epilogue:
 //   kBinMajor   P[t][n][ld]         (ld >= M, even) -- m = 64 K4 and the
 //                                    debug hook
-//   kGroupMajor P[n][m/16][t][16]   every 16-plane K4 group is one
-//                                    contiguous bins x 128-B block (one bulk
-//                                    load instead of bins scattered rows)
+//   kGroupMajor P[n][m/G][t][G]     every G-plane K4 group (G = the K4
+//                                    group size) is one contiguous block
+//                                    (one bulk load instead of bins
+//                                    scattered rows)
 enum OutLayout { kBinMajor = 0, kGroupMajor = 1 };
 
 // ------------------------------------------------------------ driver API
@@ -275,7 +276,9 @@ static void launch_r2c_one(size_t m, const R2CParams& p, cudaStream_t st, const 
   }
 }
 
-static_assert(FCB_C2R_G == 16, "group-major products hold 16-plane K4 groups");
+// group-major products are laid out in K4-group-sized blocks
+constexpr int kGroupPlanes = FCB_C2R_G;
+static_assert((kGroupPlanes & (kGroupPlanes - 1)) == 0 && kGroupPlanes >= 2, "K4 group size");
 
 // Layout the GEMM writes for K4 at fft size m (group-major where the TMA K4
 // kernel groups 16 planes).
@@ -351,15 +354,17 @@ static void launch_gemm(const float* A, const float* B, float* out, size_t bins,
   p.nc = g.nc;
   p.stages = g.stages;
   p.im_sign = im_sign;
+  p.gm_log2 = 4;
   if (lay == kBinMajor) {
     p.s_t = (long long)N * ldm;
     p.s_mg = 16;
     p.s_n = (long long)ldm;
   } else {
-    const long long mg = (long long)((M + 15) / 16);
-    p.s_t = 16;
-    p.s_mg = (long long)bins * 16;
-    p.s_n = mg * (long long)bins * 16;
+    const long long G = kGroupPlanes;
+    p.gm_log2 = ilog2c(kGroupPlanes);
+    p.s_t = G;
+    p.s_mg = (long long)bins * G;
+    p.s_n = (long long)((M + G - 1) / G) * (long long)bins * G;
   }
   smem_optin(cgemm_bins_tcgen05, (int)g.smem);
   const long long tiles = (long long)bins * g.m_tiles * g.n_tiles;
