@@ -79,6 +79,12 @@ constexpr int kMaxNc = 96;                  // TMEM: 2 x 2*96 accumulator + 2 x 
 // (development builds only).
 #ifdef FCB_GEMM_TRACE
 __device__ long long g_gemm_trace[6][64];
+__device__ unsigned long long g_cta_time[3][160];  // globaltimer: launch, work start, end
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 #define GTRACE(ev, idx)                                                      \
   do {                                                                       \
     if (blockIdx.x == 0 && (idx) < 64) g_gemm_trace[ev][idx] = clock64();    \
@@ -100,6 +106,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     cgemm_bins_tcgen05(const __grid_constant__ CUtensorMap tmA,
                        const __grid_constant__ CUtensorMap tmB, const GemmParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
+#ifdef FCB_GEMM_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 160) g_cta_time[0][blockIdx.x] = gtimer();
+#endif
   // 1024-B alignment for the swizzle atoms, derived from the __shared__
   // pointer so the converters' accesses compile to LDS/STS.
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -151,6 +160,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
   pdl_wait();  // prologue above overlaps the previous kernel's tail
   pdl_trigger();
+#ifdef FCB_GEMM_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 160) g_cta_time[1][blockIdx.x] = gtimer();
+#endif
 
   const int tiles_per_bin = p.m_tiles * p.n_tiles;
   const int total_tiles = p.bins * tiles_per_bin;
@@ -337,6 +349,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tmem_dealloc(tmem_base, kTmemCols);
   }
 #ifdef FCB_GEMM_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 160) g_cta_time[2][blockIdx.x] = gtimer();
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const long long t0 = g_gemm_trace[0][0];
     for (int i = 0; i < 30; ++i)

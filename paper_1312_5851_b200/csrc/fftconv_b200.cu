@@ -370,6 +370,26 @@ static void launch_gemm(const float* A, const float* B, float* out, size_t bins,
   const long long tiles = (long long)bins * g.m_tiles * g.n_tiles;
   const int grid = (int)std::min<long long>(tiles, di.sms);
   launch_pdl(cgemm_bins_tcgen05, dim3(grid), dim3(kGemmThreads), g.smem, st, ta, tb, p);
+#ifdef FCB_GEMM_TRACE
+  {  // per-CTA timeline (ns): launch -> work start -> end, relative to the earliest launch
+    unsigned long long h[3][160];
+    cudaStreamSynchronize(st);
+    cudaMemcpyFromSymbol(h, g_cta_time, sizeof h);
+    unsigned long long t0 = ~0ull;
+    for (int i = 0; i < grid; ++i) t0 = std::min(t0, h[0][i]);
+    std::vector<double> st_, en;
+    for (int i = 0; i < grid; ++i) {
+      st_.push_back((h[1][i] - t0) * 1e-3);
+      en.push_back((h[2][i] - t0) * 1e-3);
+    }
+    std::vector<double> es = en;
+    std::sort(es.begin(), es.end());
+    printf("gemm %d CTAs: start max %.1f us; end min %.1f p50 %.1f p90 %.1f max %.1f us; tiles/CTA %.2f\n", grid,
+           *std::max_element(st_.begin(), st_.end()), es.front(), es[es.size() / 2], es[es.size() * 9 / 10],
+           es.back(), (double)tiles / grid);
+    for (int i = 0; i < grid; i += 16) printf("  cta %3d start %.1f end %.1f\n", i, st_[i], en[i]);
+  }
+#endif
 }
 
 // Negates every imaginary part of n complex values (debug hook helper).
