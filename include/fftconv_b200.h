@@ -66,6 +66,19 @@ void fftconv_b200_ws_destroy(fftconv_b200_ws* ws);
  * workspace (when non-NULL). */
 const char* fftconv_b200_last_error(const fftconv_b200_ws* ws);
 
+/* Precision scheme of the per-bin complex GEMM (K3), process-wide.  Both
+ * keep fp32-level accuracy (rel. L2 ~1e-6 against the fp64 oracle):
+ *   FFTCONV_B200_GEMM_F16X3  (default) operands scaled by a power of two
+ *       from their max magnitude (found by K1) and split into fp16
+ *       hi + mid; D = hi.hi + hi.mid + mid.hi on kind::f16 tensor cores;
+ *   FFTCONV_B200_GEMM_TF32X3 x = tf32 hi + lo, D = hi.hi + hi.lo + lo.hi
+ *       on kind::tf32 (half the fp16 rate; also used at FFT sizes m < 4).
+ * The environment variable FFTCONV_B200_GEMM=tf32 selects the latter at
+ * load time.  Returns the previous kind, or -1 for an unknown kind. */
+#define FFTCONV_B200_GEMM_F16X3 0
+#define FFTCONV_B200_GEMM_TF32X3 1
+int fftconv_b200_set_gemm_kind(int kind);
+
 /* ConvWorkspace::max_fft_size/capacity_x/capacity_w/capacity_y/
  * frequency_bytes  conv_fft.hpp:60-69.
  * out[0..4] = max_fft_size, cap_x, cap_w, cap_y, frequency_bytes (the

@@ -40,6 +40,7 @@ SIGNATURES = [
     ("fftconv_b200_maxpool_forward", _i, [_p, _sz, _sz, _sz, _p, _p, _p]),
     ("fftconv_b200_maxpool_backward", _i, [_p, _p, _sz, _sz, _sz, _p, _p]),
     ("fftconv_b200_fit_to", _i, [_p, _sz, _sz, _sz, _p, _sz, _p]),
+    ("fftconv_b200_set_gemm_kind", _i, [_i]),
     ("fftconv_b200_debug_r2c", _i, [_p, _sz, _sz, _sz, _p, _p]),
     ("fftconv_b200_debug_c2r", _i, [_p, _sz, _sz, _sz, _p, _p]),
     ("fftconv_b200_debug_cgemm", _i, [_p, _p, _p, _sz, _sz, _sz, _sz, _i, _p]),

@@ -68,6 +68,10 @@ struct GemmParams {
   float im_sign;  // +1 (fprop, bprop) or -1 (accGrad)
   long long s_t, s_mg, s_n;  // output strides in complex elements
   int gm_log2;                // log2 of the m-group size gm
+  // fp16x3 mode: the operands' max |component| words written by K1
+  // (R2CParams::amax; low 32 bits = float bits)
+  const unsigned long long* amax_a;
+  const unsigned long long* amax_b;
 };
 
 constexpr int kGemmThreads = 640;
@@ -95,13 +99,39 @@ __device__ __forceinline__ unsigned long long gtimer() {
   } while (0)
 #endif
 
-__host__ __device__ inline int gemm_raw_stage_bytes(int nc) {
-  return kChunkBytesA + nc * 128;  // raw A | raw B
+// One raw stage holds one K chunk (tf32 mode) or two (fp16 mode: a 128-B
+// fp16 row covers 32 complex).
+__host__ __device__ inline int gemm_raw_stage_bytes(int nc, bool f16 = false) {
+  return (f16 ? 2 : 1) * (kChunkBytesA + nc * 128);  // raw A | raw B (x2: A0 A1 B0 B1)
+}
+
+// fp16 operand scaling: max|x| < 2^e  ->  x * 2^(14 - e) < 2^14, inside the
+// fp16 range with headroom; 0 / non-finite maxima keep scale 1.
+__device__ __forceinline__ int amax_exp(unsigned long long w) {
+  const float a = __uint_as_float((uint32_t)w);
+  if (!(a > 0.f) || !isfinite(a)) return 14;
+  int e;
+  frexpf(a, &e);
+  return max(-100, min(e, 120));
+}
+
+// x -> (hi, mid) fp16 with x ~= hi + mid to ~2^-22 relative (hi = rn(x),
+// mid = rn(x - hi)); pairs packed low = even K.
+__device__ __forceinline__ void split_f16x2(float x0, float x1, uint32_t& hi, uint32_t& mid) {
+  const __half2 h = __floats2half2_rn(x0, x1);
+  const float2 hf = __half22float2(h);
+  const __half2 m = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  mid = *reinterpret_cast<const uint32_t*>(&m);
 }
 __host__ __device__ inline int gemm_bbuf_bytes(int nc) {
   return 4 * nc * 128;  // B re (= raw) | B im | B lo re | B lo im
 }
 
+// F16 = false: 3xTF32 (hi = raw fp32, lo = x - tf32(x)); true: 3xFP16 on
+// per-operand power-of-two scaled values, kind::f16 MMAs (twice the K per
+// instruction), hi.hi + hi.mid + mid.hi.
+template <bool F16>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     cgemm_bins_tcgen05(const __grid_constant__ CUtensorMap tmA,
                        const __grid_constant__ CUtensorMap tmB, const GemmParams p) {
@@ -115,7 +145,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int nc = p.nc;
   const int RS = p.stages;  // raw stages
   const int rowsB = nc * 128;  // bytes of nc rows
-  const int rawBytes = gemm_raw_stage_bytes(nc);
+  const int rawBytes = gemm_raw_stage_bytes(nc, F16);
+  const int offB = (F16 ? 2 : 1) * kChunkBytesA;  // raw B within a stage
   uint8_t* bbuf0 = smem + RS * rawBytes;  // 2 converted-B buffers
   const int bbufBytes = gemm_bbuf_bytes(nc);
   uint64_t* bars = reinterpret_cast<uint64_t*>(bbuf0 + 2 * bbufBytes);
@@ -166,14 +197,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   const int tiles_per_bin = p.m_tiles * p.n_tiles;
   const int total_tiles = p.bins * tiles_per_bin;
-  const int kc_n = p.k_chunks;
+  // pipeline steps per tile: K chunks (tf32) or chunk pairs (fp16)
+  const int kc_n = F16 ? (p.k_chunks + 1) >> 1 : p.k_chunks;
+  int ea = 14, eb = 14;  // fp16 operand scale exponents
+  if constexpr (F16) {
+    ea = amax_exp(p.amax_a[0]);
+    eb = amax_exp(p.amax_b[0]);
+  }
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      const uint32_t tx = kChunkBytesA + rowsB;
       int gi = 0;
       (void)gi;
       for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
@@ -185,16 +221,27 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           GTRACE(0, gi);
           ++gi;
           uint8_t* st = smem + s * rawBytes;
-          mbar_arrive_expect_tx(&rfull[s], tx);
-          tma_load_3d(st, &tmA, &rfull[s], kc * 32, mt * kTileM, t);
-          tma_load_3d(st + kChunkBytesA, &tmB, &rfull[s], kc * 32, nt * nc, t);
+          if constexpr (!F16) {
+            mbar_arrive_expect_tx(&rfull[s], kChunkBytesA + rowsB);
+            tma_load_3d(st, &tmA, &rfull[s], kc * 32, mt * kTileM, t);
+            tma_load_3d(st + offB, &tmB, &rfull[s], kc * 32, nt * nc, t);
+          } else {  // chunks 2kc, 2kc+1 (the second absent at odd k_chunks: converters zero it)
+            const bool two = 2 * kc + 1 < p.k_chunks;
+            mbar_arrive_expect_tx(&rfull[s], (two ? 2 : 1) * (kChunkBytesA + rowsB));
+            tma_load_3d(st, &tmA, &rfull[s], kc * 64, mt * kTileM, t);
+            tma_load_3d(st + offB, &tmB, &rfull[s], kc * 64, nt * nc, t);
+            if (two) {
+              tma_load_3d(st + kChunkBytesA, &tmA, &rfull[s], kc * 64 + 32, mt * kTileM, t);
+              tma_load_3d(st + offB + rowsB, &tmB, &rfull[s], kc * 64 + 32, nt * nc, t);
+            }
+          }
           if (++s == RS) { s = 0; ph ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
-    const uint32_t idesc = umma_idesc_tf32(kTileM, 2 * nc);
+    const uint32_t idesc = F16 ? umma_idesc_f16(kTileM, 2 * nc) : umma_idesc_tf32(kTileM, 2 * nc);
     uint32_t g = 0;  // global chunk counter (TMEM A buffer / B buffer = g & 1)
     int local = 0;
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++local) {
@@ -217,9 +264,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           for (int kk = 0; kk < 4; ++kk) {
             const uint64_t dbh = umma_desc_sw128(b_hi + kk * 32);
             const uint64_t dbl = umma_desc_sw128(b_lo + kk * 32);
-            umma_tf32_ts(d_tmem, a_hi + kk * 8, dbh, idesc, (kc | kk) ? 1u : 0u);
-            umma_tf32_ts(d_tmem, a_hi + kk * 8, dbl, idesc, 1u);
-            umma_tf32_ts(d_tmem, a_lo + kk * 8, dbh, idesc, 1u);
+            if constexpr (F16) {  // K = 16 fp16 = 8 TMEM columns / 32 B per step
+              umma_f16_ts(d_tmem, a_hi + kk * 8, dbh, idesc, (kc | kk) ? 1u : 0u);
+              umma_f16_ts(d_tmem, a_hi + kk * 8, dbl, idesc, 1u);
+              umma_f16_ts(d_tmem, a_lo + kk * 8, dbh, idesc, 1u);
+            } else {
+              umma_tf32_ts(d_tmem, a_hi + kk * 8, dbh, idesc, (kc | kk) ? 1u : 0u);
+              umma_tf32_ts(d_tmem, a_hi + kk * 8, dbl, idesc, 1u);
+              umma_tf32_ts(d_tmem, a_lo + kk * 8, dbh, idesc, 1u);
+            }
           }
           umma_commit(&atfree[b]);
           umma_commit(&bfree[b]);
@@ -241,26 +294,52 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         mbar_wait(&rfull[s], ph);
         if (threadIdx.x == 128) GTRACE(1, g);
         const uint8_t* arow = smem + s * rawBytes + (m >> 3) * 1024 + (m & 7) * 128;
-        float x[32], lo[32];
+        if constexpr (F16) {
+          // TMEM column 16c + j holds the scaled pair (K 32c + 2j, 32c + 2j + 1)
+          const float sc = ldexpf(1.f, 14 - ea);
+          const bool two = 2 * kc + 1 < p.k_chunks;
+          uint32_t hi[32], mid[32];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {  // 16-B chunk c of the row sits at c ^ (m & 7)
-          const float4 v = *reinterpret_cast<const float4*>(arow + ((c ^ (m & 7)) << 4));
-          x[4 * c + 0] = v.x;
-          x[4 * c + 1] = v.y;
-          x[4 * c + 2] = v.z;
-          x[4 * c + 3] = v.w;
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+              if (c == 0 || two)
+                v = *reinterpret_cast<const float4*>(arow + c * kChunkBytesA + ((j ^ (m & 7)) << 4));
+              split_f16x2(v.x * sc, v.y * sc, hi[16 * c + 2 * j], mid[16 * c + 2 * j]);
+              split_f16x2(v.z * sc, v.w * sc, hi[16 * c + 2 * j + 1], mid[16 * c + 2 * j + 1]);
+            }
+          mbar_arrive(&rempty[s]);
+          mbar_wait(&atfree[g & 1], ((g >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t ta = tmem_base + lane_off + a_col0 + (g & 1) * 64;
+          tmem_st_32x32b_x32(ta, hi);
+          tmem_st_32x32b_x32(ta + 32, mid);
+          tmem_st_wait();
+          tc_fence_before();
+          mbar_arrive(&aready[g & 1]);
+        } else {
+          float x[32], lo[32];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {  // 16-B chunk c of the row sits at c ^ (m & 7)
+            const float4 v = *reinterpret_cast<const float4*>(arow + ((c ^ (m & 7)) << 4));
+            x[4 * c + 0] = v.x;
+            x[4 * c + 1] = v.y;
+            x[4 * c + 2] = v.z;
+            x[4 * c + 3] = v.w;
+          }
+          mbar_arrive(&rempty[s]);  // raw A read: the TMA may refill the stage
+#pragma unroll
+          for (int i = 0; i < 32; ++i) lo[i] = tf32_lo(x[i]);
+          mbar_wait(&atfree[g & 1], ((g >> 1) & 1) ^ 1);  // MMAs of chunk g-2 done with it
+          tc_fence_after();
+          const uint32_t ta = tmem_base + lane_off + a_col0 + (g & 1) * 64;
+          tmem_st_32x32b_x32(ta, x);
+          tmem_st_32x32b_x32(ta + 32, lo);
+          tmem_st_wait();
+          tc_fence_before();
+          mbar_arrive(&aready[g & 1]);
         }
-        mbar_arrive(&rempty[s]);  // raw A read: the TMA may refill the stage
-#pragma unroll
-        for (int i = 0; i < 32; ++i) lo[i] = tf32_lo(x[i]);
-        mbar_wait(&atfree[g & 1], ((g >> 1) & 1) ^ 1);  // MMAs of chunk g-2 done with it
-        tc_fence_after();
-        const uint32_t ta = tmem_base + lane_off + a_col0 + (g & 1) * 64;
-        tmem_st_32x32b_x32(ta, x);
-        tmem_st_32x32b_x32(ta + 32, lo);
-        tmem_st_wait();
-        tc_fence_before();
-        mbar_arrive(&aready[g & 1]);
         if (threadIdx.x == 128) GTRACE(2, g);
         if (++s == RS) { s = 0; ph ^= 1; }
       }
@@ -275,28 +354,60 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
       for (int kc = 0; kc < kc_n; ++kc, ++g) {
         mbar_wait(&rfull[s], ph);
-        const float4* braw = reinterpret_cast<const float4*>(smem + s * rawBytes + kChunkBytesA);
-        float4 v[6];  // nb / 128 <= 6 (nc <= 96)
+        const float4* braw = reinterpret_cast<const float4*>(smem + s * rawBytes + offB);
+        if constexpr (F16) {
+          // raw float4 i of chunk c: row n = i / 8, logical 16-B slot
+          // j = (i % 8) ^ (n % 8) = K 32c + 4j .. +3 -> fp16 bytes 64c + 8j of
+          // the row: SW128 slot q = 4c + j / 2 (stored at q ^ (n % 8)), half j % 2
+          const float sc = ldexpf(1.f, 14 - eb);
+          const bool two = 2 * kc + 1 < p.k_chunks;
+          mbar_wait(&bfree[g & 1], ((g >> 1) & 1) ^ 1);
+          uint8_t* bb = bbuf0 + (g & 1) * bbufBytes;
+#pragma unroll 2
+          for (int k = 0; k < 12; ++k) {  // 2 chunks x nb / 128 (<= 6)
+            const int c = k / 6, i = ct + (k % 6) * 128;
+            if (i < nb) {
+              float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
+              if (c == 0 || two) w = braw[c * nb + i];
+              const int n = i >> 3, j = (i & 7) ^ (n & 7);
+              const int off = (n >> 3) * 1024 + (n & 7) * 128 + (((4 * c + (j >> 1)) ^ (n & 7)) << 4) + (j & 1) * 8;
+              uint2 h, l, hi_im, lo_im;  // (p0, q0, p1, q1) -> re rows; (-q0, p0, -q1, p1) -> im rows
+              split_f16x2(w.x * sc, w.y * sc, h.x, l.x);
+              split_f16x2(w.z * sc, w.w * sc, h.y, l.y);
+              hi_im.x = __byte_perm(h.x ^ 0x80000000u, 0, 0x1032);  // (q, p) -> (-q, p) swapped halves
+              hi_im.y = __byte_perm(h.y ^ 0x80000000u, 0, 0x1032);
+              lo_im.x = __byte_perm(l.x ^ 0x80000000u, 0, 0x1032);
+              lo_im.y = __byte_perm(l.y ^ 0x80000000u, 0, 0x1032);
+              *reinterpret_cast<uint2*>(bb + off) = h;
+              *reinterpret_cast<uint2*>(bb + rowsB + off) = hi_im;
+              *reinterpret_cast<uint2*>(bb + 2 * rowsB + off) = l;
+              *reinterpret_cast<uint2*>(bb + 3 * rowsB + off) = lo_im;
+            }
+          }
+          mbar_arrive(&rempty[s]);
+        } else {
+          float4 v[6];  // nb / 128 <= 6 (nc <= 96)
 #pragma unroll
-        for (int k = 0; k < 6; ++k)
-          if (ct + k * 128 < nb) v[k] = braw[ct + k * 128];
-        mbar_arrive(&rempty[s]);
-        mbar_wait(&bfree[g & 1], ((g >> 1) & 1) ^ 1);  // MMAs of chunk g-2 done with it
-        uint8_t* bb = bbuf0 + (g & 1) * bbufBytes;
-        float4* bre = reinterpret_cast<float4*>(bb);
-        float4* bim = reinterpret_cast<float4*>(bb + rowsB);
-        float4* blr = reinterpret_cast<float4*>(bb + 2 * rowsB);
-        float4* bli = reinterpret_cast<float4*>(bb + 3 * rowsB);
+          for (int k = 0; k < 6; ++k)
+            if (ct + k * 128 < nb) v[k] = braw[ct + k * 128];
+          mbar_arrive(&rempty[s]);
+          mbar_wait(&bfree[g & 1], ((g >> 1) & 1) ^ 1);  // MMAs of chunk g-2 done with it
+          uint8_t* bb = bbuf0 + (g & 1) * bbufBytes;
+          float4* bre = reinterpret_cast<float4*>(bb);
+          float4* bim = reinterpret_cast<float4*>(bb + rowsB);
+          float4* blr = reinterpret_cast<float4*>(bb + 2 * rowsB);
+          float4* bli = reinterpret_cast<float4*>(bb + 3 * rowsB);
 #pragma unroll
-        for (int k = 0; k < 6; ++k) {
-          const int i = ct + k * 128;
-          if (i < nb) {
-            const float4 w = v[k];  // (p0, q0, p1, q1): re rows are the raw rows
-            bre[i] = w;
-            bim[i] = make_float4(-w.y, w.x, -w.w, w.z);
-            const float4 l = make_float4(tf32_lo(w.x), tf32_lo(w.y), tf32_lo(w.z), tf32_lo(w.w));
-            blr[i] = l;
-            bli[i] = make_float4(-l.y, l.x, -l.w, l.z);
+          for (int k = 0; k < 6; ++k) {
+            const int i = ct + k * 128;
+            if (i < nb) {
+              const float4 w = v[k];  // (p0, q0, p1, q1): re rows are the raw rows
+              bre[i] = w;
+              bim[i] = make_float4(-w.y, w.x, -w.w, w.z);
+              const float4 l = make_float4(tf32_lo(w.x), tf32_lo(w.y), tf32_lo(w.z), tf32_lo(w.w));
+              blr[i] = l;
+              bli[i] = make_float4(-l.y, l.x, -l.w, l.z);
+            }
           }
         }
         fence_proxy_async_smem();
@@ -311,6 +422,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int half = (warp - 12) >> 2;   // which 16-column blocks
     const int row = q * 32 + lane;
     const float im_sign = p.im_sign;
+    const float oscale = F16 ? ldexpf(1.f, ea - 14) * ldexpf(1.f, eb - 14) : 1.f;
     int local = 0;
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++local) {
       const int t = tile / tiles_per_bin;
@@ -334,7 +446,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int i = 0; i < 16; ++i) {
           const int n = n0 + i;
           if (mok && n < p.n_valid)
-            out[(long long)n * p.s_n] = make_float2(re[i], im_sign * im[i]);
+            out[(long long)n * p.s_n] = F16 ? make_float2(re[i] * oscale, im_sign * oscale * im[i])
+                                            : make_float2(re[i], im_sign * im[i]);
         }
       }
       tc_fence_before();

@@ -318,17 +318,17 @@ struct GemmGeom {
   int nc, n_tiles, m_tiles, stages;
   size_t smem;
 };
-static GemmGeom gemm_geom(size_t M, size_t N, const DevInfo& di) {
+static GemmGeom gemm_geom(size_t M, size_t N, const DevInfo& di, bool f16) {
   GemmGeom g;
   const size_t n16 = round_up(N, 16);
   g.n_tiles = (int)((n16 + kMaxNc - 1) / kMaxNc);
   g.nc = (int)round_up((n16 + g.n_tiles - 1) / g.n_tiles, 16);
   g.m_tiles = (int)((M + kTileM - 1) / kTileM);
   // raw TMA stages (A + B chunks) fill what the two converted-B buffers leave
-  const int sb = gemm_raw_stage_bytes(g.nc);
+  const int sb = gemm_raw_stage_bytes(g.nc, f16);
   const int fixed = 2 * gemm_bbuf_bytes(g.nc);
   const int budget = di.max_smem_optin - 1024 - 256 - fixed;
-  g.stages = std::min(8, budget / sb);
+  g.stages = std::min(f16 ? 4 : 8, budget / sb);
   if (g.stages < 2) throw Error(FFTCONV_B200_CUDA_ERROR, "gemm tile does not fit shared memory");
   g.smem = (size_t)g.stages * sb + fixed + 1024 + 256;
   return g;
@@ -337,10 +337,20 @@ static GemmGeom gemm_geom(size_t M, size_t N, const DevInfo& di) {
 // D[t] = A[t] . conj(B[t])^T per bin; im_sign = -1 returns conj(D) (the
 // accGrad orientation, conj(A) . B).  A: F[t][M][2*kpad], B: F[t][N][2*kpad].
 
+// GEMM operand precision: fp16x3 (default) or 3xTF32 (FFTCONV_B200_GEMM=tf32,
+// fftconv_b200_set_gemm_kind); fp16x3 needs the operands' max-magnitude words
+// (amax_a / amax_b from K1), so callers without them get 3xTF32.
+static int g_gemm_kind = [] {
+  const char* e = getenv("FFTCONV_B200_GEMM");
+  return (e && std::string(e) == "tf32") ? FFTCONV_B200_GEMM_TF32X3 : FFTCONV_B200_GEMM_F16X3;
+}();
+
 static void launch_gemm(const float* A, const float* B, float* out, size_t bins, size_t M,
                         size_t N, size_t kpad, float im_sign, OutLayout lay, size_t ldm,
-                        const DevInfo& di, cudaStream_t st) {
-  const GemmGeom g = gemm_geom(M, N, di);
+                        const DevInfo& di, cudaStream_t st, const unsigned long long* amax_a = nullptr,
+                        const unsigned long long* amax_b = nullptr) {
+  const bool f16 = amax_a && amax_b && g_gemm_kind == FFTCONV_B200_GEMM_F16X3;
+  const GemmGeom g = gemm_geom(M, N, di, f16);
   CUtensorMap ta = make_operand_map(A, kpad, M, bins, kTileM);
   CUtensorMap tb = make_operand_map(B, kpad, N, bins, (uint32_t)g.nc);
   GemmParams p;
@@ -354,6 +364,8 @@ static void launch_gemm(const float* A, const float* B, float* out, size_t bins,
   p.nc = g.nc;
   p.stages = g.stages;
   p.im_sign = im_sign;
+  p.amax_a = amax_a;
+  p.amax_b = amax_b;
   p.gm_log2 = 4;
   if (lay == kBinMajor) {
     p.s_t = (long long)N * ldm;
@@ -366,10 +378,11 @@ static void launch_gemm(const float* A, const float* B, float* out, size_t bins,
     p.s_mg = (long long)bins * G;
     p.s_n = (long long)((M + G - 1) / G) * (long long)bins * G;
   }
-  smem_optin(cgemm_bins_tcgen05, (int)g.smem);
+  auto kern = f16 ? cgemm_bins_tcgen05<true> : cgemm_bins_tcgen05<false>;
+  smem_optin(kern, (int)g.smem);
   const long long tiles = (long long)bins * g.m_tiles * g.n_tiles;
   const int grid = (int)std::min<long long>(tiles, di.sms);
-  launch_pdl(cgemm_bins_tcgen05, dim3(grid), dim3(kGemmThreads), g.smem, st, ta, tb, p);
+  launch_pdl(kern, dim3(grid), dim3(kGemmThreads), g.smem, st, ta, tb, p);
 #ifdef FCB_GEMM_TRACE
   {  // per-CTA timeline (ns): launch -> work start -> end, relative to the earliest launch
     unsigned long long h[3][160];
@@ -390,6 +403,16 @@ static void launch_gemm(const float* A, const float* B, float* out, size_t bins,
     for (int i = 0; i < grid; i += 16) printf("  cta %3d start %.1f end %.1f\n", i, st_[i], en[i]);
   }
 #endif
+}
+
+// max |component| of n floats into *out (epoch 0 word; debug hook helper).
+__global__ void absmax_kernel(const float* v, long long n, unsigned long long* out) {
+  uint32_t m = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    m = max(m, __float_as_uint(v[i]) & 0x7fffffffu);
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)m);
 }
 
 // Negates every imaginary part of n complex values (debug hook helper).
@@ -429,6 +452,8 @@ struct fftconv_b200_ws {
   cudaEvent_t pev[2][kMaxChunks + 1] = {};  // chunk pipeline: inputs landed / outputs ready
   bool pev_ready = false;
   uint64_t ctr[3] = {0, 0, 0};
+  unsigned long long* amax = nullptr;  // K1 -> K3 operand max-magnitude words [A, B]
+  unsigned epoch = 0;
   std::string last_error;
   bool timing = false;
   cudaEvent_t ev[5] = {};
@@ -539,6 +564,18 @@ static bool gemm_swap(size_t M, size_t N) {
 
 // ---- the three operators (device pointers) ---------------------------
 
+// Both forward transforms; at m >= 4 (the TMA K1) they also record the
+// operands' max-magnitude words for the fp16x3 GEMM under a fresh epoch.
+// a.amax / b.amax stay null otherwise (the GEMM then runs 3xTF32).
+int r2c_operands(fftconv_b200_ws* ws, size_t m, R2CParams& a, R2CParams& b, cudaStream_t st) {
+  if (m >= 4 && g_gemm_kind == FFTCONV_B200_GEMM_F16X3) {
+    a.amax = ws->amax;
+    b.amax = ws->amax + 1;
+    a.epoch = b.epoch = ++ws->epoch;
+  }
+  return launch_r2c_both(m, a, b, st, ws->di);
+}
+
 void run_forward(fftconv_b200_ws* ws, const float* x, size_t S, size_t f, size_t xr, size_t xc,
                  const float* w, size_t wo, size_t wi, size_t k, float* y, cudaStream_t st) {
   require_nonzero(S, f, xr, xc, "Tensor4");
@@ -558,17 +595,17 @@ void run_forward(fftconv_b200_ws* ws, const float* x, size_t S, size_t f, size_t
               (int)n, (int)(n | 1)};
   R2CParams b{w, ws->bufB, (long long)(f * k * k), (long long)(k * k), (int)fo, (int)f, (int)kp,
               (int)k, (int)(k | 1)};
-  const int nl = launch_r2c_both(m, a, b, st, ws->di);
+  const int nl = r2c_operands(ws, m, a, b, st);
   record(ws, 1, st);  // both forward transforms
   record(ws, 2, st);
   C2RParams c{ws->bufD, y, (long long)(no * no), (long long)(fo * no * no), (int)fo, (int)S,
               (int)no, 0, 0, 1.0f / (float)(m * m), (int)round_up(S, 2)};
   if (!gemm_swap(S, fo)) {  // D[t][o][b]: planes (r = o, j = b)
     launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, S, fo, kp, 1.0f, c2r_layout(m), round_up(S, 2),
-                ws->di, st);
+                ws->di, st, a.amax, b.amax);
   } else {  // D^T[t][b][o]: planes (r = b, j = o)
     launch_gemm(ws->bufB, ws->bufA, ws->bufD, bins, fo, S, kp, -1.0f, c2r_layout(m), round_up(fo, 2),
-                ws->di, st);
+                ws->di, st, b.amax, a.amax);
     c = C2RParams{ws->bufD, y, (long long)(fo * no * no), (long long)(no * no), (int)S, (int)fo,
                   (int)no, 0, 0, 1.0f / (float)(m * m), (int)round_up(fo, 2)};
   }
@@ -602,17 +639,17 @@ void run_grad_input(fftconv_b200_ws* ws, const float* gy, size_t S, size_t fo, s
               (int)kp, (int)no, (int)(no | 1)};
   R2CParams b{w, ws->bufB, (long long)(k * k), (long long)(f * k * k), (int)f, (int)fo, (int)kp,
               (int)k, (int)(k | 1), /*conj=*/1};  // GX = GY . W = GY . conj(conj W)
-  const int nl = launch_r2c_both(m, a, b, st, ws->di);
+  const int nl = r2c_operands(ws, m, a, b, st);
   record(ws, 1, st);  // both forward transforms
   record(ws, 2, st);
   C2RParams c{ws->bufD, gx, (long long)(n * n), (long long)(f * n * n), (int)f, (int)S, (int)n,
               0, 0, 1.0f / (float)(m * m), (int)round_up(S, 2)};
   if (!gemm_swap(S, f)) {  // D[t][f][b]
     launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, S, f, kp, 1.0f, c2r_layout(m), round_up(S, 2),
-                ws->di, st);
+                ws->di, st, a.amax, b.amax);
   } else {  // D^T[t][b][f]
     launch_gemm(ws->bufB, ws->bufA, ws->bufD, bins, f, S, kp, -1.0f, c2r_layout(m), round_up(f, 2),
-                ws->di, st);
+                ws->di, st, b.amax, a.amax);
     c = C2RParams{ws->bufD, gx, (long long)(f * n * n), (long long)(n * n), (int)S, (int)f, (int)n,
                   0, 0, 1.0f / (float)(m * m), (int)round_up(f, 2)};
   }
@@ -648,10 +685,11 @@ void run_grad_weight(fftconv_b200_ws* ws, const float* gy, size_t Sg, size_t fo,
               (int)kp, (int)no, (int)(no | 1)};
   R2CParams b{x, ws->bufB, (long long)(n * n), (long long)(f * n * n), (int)f, (int)S, (int)kp,
               (int)n, (int)(n | 1)};
-  const int nl = launch_r2c_both(m, a, b, st, ws->di);
+  const int nl = r2c_operands(ws, m, a, b, st);
   record(ws, 1, st);  // both forward transforms
   record(ws, 2, st);
-  launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, fo, f, kp, -1.0f, c2r_layout(m), round_up(fo, 2), ws->di, st);
+  launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, fo, f, kp, -1.0f, c2r_layout(m), round_up(fo, 2), ws->di, st,
+              a.amax, b.amax);
   record(ws, 3, st);
   C2RParams c{ws->bufD, gw, (long long)(k * k), (long long)(f * k * k), (int)f, (int)fo, (int)k,
               0, 0, 1.0f / (float)(m * m), (int)round_up(fo, 2)};
@@ -694,6 +732,8 @@ int fftconv_b200_ws_create(const fftconv_b200_layer* configs, size_t count, int 
       DeviceGuard g(device);
       ws->di = dev_info(device);
       FCB_CUDA(cudaStreamCreateWithFlags(&ws->host_stream, cudaStreamNonBlocking));
+      FCB_CUDA(cudaMalloc(&ws->amax, 2 * sizeof(unsigned long long)));
+      FCB_CUDA(cudaMemset(ws->amax, 0, 2 * sizeof(unsigned long long)));
       FCB_CUDA(cudaStreamCreateWithFlags(&ws->h2d_stream, cudaStreamNonBlocking));
       FCB_CUDA(cudaStreamCreateWithFlags(&ws->d2h_stream, cudaStreamNonBlocking));
       for (auto& row : ws->pev)
@@ -727,6 +767,7 @@ void fftconv_b200_ws_destroy(fftconv_b200_ws* ws) {
     DeviceGuard g(ws->device);
     for (float* p : {ws->freq, ws->st_in0, ws->st_in1, ws->st_out})
       if (p) cudaFree(p);
+    if (ws->amax) cudaFree(ws->amax);
     if (ws->host_stream) cudaStreamDestroy(ws->host_stream);
     if (ws->h2d_stream) cudaStreamDestroy(ws->h2d_stream);
     if (ws->d2h_stream) cudaStreamDestroy(ws->d2h_stream);
@@ -737,6 +778,13 @@ void fftconv_b200_ws_destroy(fftconv_b200_ws* ws) {
       for (auto& e : ws->ev) cudaEventDestroy(e);
   }
   delete ws;
+}
+
+int fftconv_b200_set_gemm_kind(int kind) {
+  if (kind != FFTCONV_B200_GEMM_F16X3 && kind != FFTCONV_B200_GEMM_TF32X3) return -1;
+  const int prev = g_gemm_kind;
+  g_gemm_kind = kind;
+  return prev;
 }
 
 const char* fftconv_b200_last_error(const fftconv_b200_ws* ws) {
@@ -1065,10 +1113,16 @@ int fftconv_b200_debug_cgemm(const float* a, const float* b, float* out, size_t 
     if (mode == 1)  // A . B = A . conj(conj(B))
       conj_inplace_kernel<<<256, 256, 0, st>>>(reinterpret_cast<float2*>(B),
                                                (long long)(bins * N * kp));
-    launch_gemm(A, B, out, bins, M, N, kp, mode == 2 ? -1.0f : 1.0f, kBinMajor, M, di, st);
+    unsigned long long* amax = nullptr;
+    FCB_CUDA(cudaMalloc(&amax, 2 * sizeof(unsigned long long)));
+    FCB_CUDA(cudaMemsetAsync(amax, 0, 2 * sizeof(unsigned long long), st));
+    absmax_kernel<<<256, 256, 0, st>>>(A, (long long)(bins * M * kp * 2), amax);
+    absmax_kernel<<<256, 256, 0, st>>>(B, (long long)(bins * N * kp * 2), amax + 1);
+    launch_gemm(A, B, out, bins, M, N, kp, mode == 2 ? -1.0f : 1.0f, kBinMajor, M, di, st, amax, amax + 1);
     FCB_CUDA(cudaStreamSynchronize(st));
     cudaFree(A);
     cudaFree(B);
+    cudaFree(amax);
   });
 }
 

@@ -76,9 +76,9 @@ def test_r2c_c2r_round_trip(dev, m, src):
 
 @pytest.mark.parametrize("bins,M,N,K", [(3, 8, 16, 16), (5, 128, 96, 96), (2, 96, 96, 128),
                                         (4, 5, 3, 7), (2, 200, 40, 20), (3, 128, 256, 64),
-                                        (2, 130, 130, 33)])
+                                        (2, 130, 130, 33), (2, 64, 48, 48), (3, 40, 100, 80)])
 @pytest.mark.parametrize("mode", [0, 1, 2])
-def test_cgemm_bins(dev, bins, M, N, K, mode):
+def test_cgemm_bins(dev, gemm_kind, bins, M, N, K, mode):
     import torch
 
     from paper_1312_5851_b200 import kernels
@@ -95,5 +95,49 @@ def test_cgemm_bins(dev, bins, M, N, K, mode):
     else:
         ref = torch.einsum("tmk,tnk->tnm", A.conj(), B)
     err = float((got - ref).abs().norm() / ref.abs().norm())
-    # 3xTF32 holds fp32-level accuracy; plain TF32 would sit near 3e-4.
+    # 3xTF32 and fp16x3 hold fp32-level accuracy; plain TF32 would sit near 3e-4.
     assert err < 5e-6, err
+
+
+@pytest.mark.parametrize("scale_a,scale_b", [(2.0 ** -60, 2.0 ** 50), (1e-30, 1e-8), (1e20, 1e15), (0.0, 1.0)])
+def test_cgemm_operand_scaling(dev, gemm_kind, scale_a, scale_b):
+    """fp16x3 rescales each operand by a power of two from its max magnitude:
+    results far outside the fp16 range (and all-zero operands) stay exact to
+    fp32 level."""
+    import torch
+
+    from paper_1312_5851_b200 import kernels
+
+    g = torch.Generator().manual_seed(5)
+    a = torch.complex(torch.randn(3, 70, 40, generator=g), torch.randn(3, 70, 40, generator=g)) * scale_a
+    b = torch.complex(torch.randn(3, 50, 40, generator=g), torch.randn(3, 50, 40, generator=g)) * scale_b
+    got = kernels.cgemm(a.to(dev), b.to(dev), 0).cpu().to(torch.complex128)
+    ref = torch.einsum("tmk,tnk->tnm", a.to(torch.complex128), b.to(torch.complex128).conj())
+    assert torch.isfinite(got.real).all() and torch.isfinite(got.imag).all()
+    if scale_a == 0.0:
+        assert float(got.abs().max()) == 0.0
+        return
+    err = float((got - ref).abs().norm() / ref.abs().norm())
+    assert err < 5e-6, err
+
+
+def test_cgemm_wide_dynamic_range_rows(dev, gemm_kind):
+    """Rows spanning 2^20 in magnitude within one operand: each output row
+    keeps its own relative accuracy (fp16x3 scales by the operand maximum;
+    components below ~2^-24 of it reach fp16's subnormal floor and keep only
+    an absolute error of ~2^-38 of the maximum)."""
+    import torch
+
+    from paper_1312_5851_b200 import kernels
+
+    g = torch.Generator().manual_seed(6)
+    rows = (2.0 ** torch.linspace(-10, 10, 64)).reshape(1, 64, 1)
+    a = torch.complex(torch.randn(2, 64, 32, generator=g), torch.randn(2, 64, 32, generator=g)) * rows
+    b = torch.complex(torch.randn(2, 32, 32, generator=g), torch.randn(2, 32, 32, generator=g))
+    got = kernels.cgemm(a.to(dev), b.to(dev), 0).cpu().to(torch.complex128)
+    ref = torch.einsum("tmk,tnk->tnm", a.to(torch.complex128), b.to(torch.complex128).conj())
+    # per output row m: error relative to that row's norm
+    num = (got - ref).abs().pow(2).sum(dim=(0, 1)).sqrt()
+    den = ref.abs().pow(2).sum(dim=(0, 1)).sqrt()
+    rel = (num / den).max().item()
+    assert rel < 2e-5, rel
