@@ -78,6 +78,7 @@ constexpr int kGemmThreads = 640;
 constexpr int kTileM = 128;
 constexpr int kChunkBytesA = kTileM * 128;  // 128 rows x 128 B (32 fp32)
 constexpr int kMaxNc = 96;                  // TMEM: 2 x 2*96 accumulator + 2 x 64 A columns
+constexpr int kBConvF16 = 192;              // fp16 B converters: warps 2, 3, 8-11
 
 // FCB_GEMM_TRACE: per-chunk clock64 timeline of CTA 0, printed at exit
 // (development builds only).
@@ -115,14 +116,25 @@ __device__ __forceinline__ int amax_exp(unsigned long long w) {
   return max(-100, min(e, 120));
 }
 
-// x -> (hi, mid) fp16 with x ~= hi + mid to ~2^-22 relative (hi = rn(x),
-// mid = rn(x - hi)); pairs packed low = even K.
+// x -> hi + mid: hi = x rounded to an 11-bit significand in fp32 (exact in
+// fp16 for the scaled range), mid = x - hi (exact, |mid| <= 2^-11 |x|), so
+// hi + rn16(mid) = x to ~2^-22 relative.
+struct Split {
+  float hi, mid;
+};
+__device__ __forceinline__ Split split11(float x) {
+  const float h = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
+  return {h, x - h};
+}
+// fp16x2 with `lo` in the low half (= the even K element)
+__device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
+  const __half2 h = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
 __device__ __forceinline__ void split_f16x2(float x0, float x1, uint32_t& hi, uint32_t& mid) {
-  const __half2 h = __floats2half2_rn(x0, x1);
-  const float2 hf = __half22float2(h);
-  const __half2 m = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
-  hi = *reinterpret_cast<const uint32_t*>(&h);
-  mid = *reinterpret_cast<const uint32_t*>(&m);
+  const Split a = split11(x0), b = split11(x1);
+  hi = pack_f16x2(a.hi, b.hi);
+  mid = pack_f16x2(a.mid, b.mid);
 }
 __host__ __device__ inline int gemm_bbuf_bytes(int nc) {
   return 4 * nc * 128;  // B re (= raw) | B im | B lo re | B lo im
@@ -168,11 +180,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < RS; ++s) {
       mbar_init(&rfull[s], 1);
-      mbar_init(&rempty[s], 256);  // every A and B converter thread
+      mbar_init(&rempty[s], F16 ? 128 + kBConvF16 : 256);  // every A and B converter thread
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&aready[a], 128);
-      mbar_init(&bready[a], 128);
+      mbar_init(&bready[a], F16 ? kBConvF16 : 128);
       mbar_init(&atfree[a], 1);
       mbar_init(&bfree[a], 1);
       mbar_init(&tfull[a], 1);
@@ -295,26 +307,28 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (threadIdx.x == 128) GTRACE(1, g);
         const uint8_t* arow = smem + s * rawBytes + (m >> 3) * 1024 + (m & 7) * 128;
         if constexpr (F16) {
-          // TMEM column 16c + j holds the scaled pair (K 32c + 2j, 32c + 2j + 1)
+          // TMEM column 16c + j holds the scaled pair (K 32c + 2j, 32c + 2j + 1);
+          // hi in columns 0-31 of the staging buffer, mid in 32-63
           const float sc = ldexpf(1.f, 14 - ea);
           const bool two = 2 * kc + 1 < p.k_chunks;
-          uint32_t hi[32], mid[32];
+          mbar_wait(&atfree[g & 1], ((g >> 1) & 1) ^ 1);  // MMAs of step g-2 done with it
+          tc_fence_after();
+          const uint32_t ta = tmem_base + lane_off + a_col0 + (g & 1) * 64;
 #pragma unroll
-          for (int c = 0; c < 2; ++c)
+          for (int c = 0; c < 2; ++c) {
+            uint32_t hi[16], mid[16];
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
               if (c == 0 || two)
                 v = *reinterpret_cast<const float4*>(arow + c * kChunkBytesA + ((j ^ (m & 7)) << 4));
-              split_f16x2(v.x * sc, v.y * sc, hi[16 * c + 2 * j], mid[16 * c + 2 * j]);
-              split_f16x2(v.z * sc, v.w * sc, hi[16 * c + 2 * j + 1], mid[16 * c + 2 * j + 1]);
+              split_f16x2(v.x * sc, v.y * sc, hi[2 * j], mid[2 * j]);
+              split_f16x2(v.z * sc, v.w * sc, hi[2 * j + 1], mid[2 * j + 1]);
             }
-          mbar_arrive(&rempty[s]);
-          mbar_wait(&atfree[g & 1], ((g >> 1) & 1) ^ 1);
-          tc_fence_after();
-          const uint32_t ta = tmem_base + lane_off + a_col0 + (g & 1) * 64;
-          tmem_st_32x32b_x32(ta, hi);
-          tmem_st_32x32b_x32(ta + 32, mid);
+            if (c == 1) mbar_arrive(&rempty[s]);
+            tmem_st_32x32b_x16(ta + 16 * c, hi);
+            tmem_st_32x32b_x16(ta + 32 + 16 * c, mid);
+          }
           tmem_st_wait();
           tc_fence_before();
           mbar_arrive(&aready[g & 1]);
@@ -344,7 +358,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (++s == RS) { s = 0; ph ^= 1; }
       }
     }
-  } else if (warp >= 8 && warp < 12) {
+  } else if ((warp >= 8 && warp < 12) || (F16 && (warp == 2 || warp == 3))) {
     // ------------------------------------------------ B converters: raw -> re, im, lo, lo-im
     const int ct = threadIdx.x - 256;  // 0..127
     const int nb = nc * 8;             // float4 per raw B tile
@@ -356,35 +370,49 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         mbar_wait(&rfull[s], ph);
         const float4* braw = reinterpret_cast<const float4*>(smem + s * rawBytes + offB);
         if constexpr (F16) {
-          // raw float4 i of chunk c: row n = i / 8, logical 16-B slot
-          // j = (i % 8) ^ (n % 8) = K 32c + 4j .. +3 -> fp16 bytes 64c + 8j of
-          // the row: SW128 slot q = 4c + j / 2 (stored at q ^ (n % 8)), half j % 2
+          // Six warps; warp task = (chunk c, 8-row block b, row half hv).
+          // Raw float4 (row n, logical slot j) = K 32c + 4j .. +3 -> fp16
+          // bytes 64c + 8j of row n: SW128 slot q = 4c + j/2 stored at
+          // q ^ (n % 8), half j % 2.  8-B stores go out per half-warp; a half
+          // takes rows r and r + 4, which fill opposite bank halves.
+          const int bw = warp >= 8 ? warp - 6 : warp - 2;  // 0..5
+          const int hv = bw & 1, b0 = bw >> 1;             // blocks b0, b0+3, b0+6, b0+9
+          const int r7 = 2 * hv + (((lane >> 3) & 1) << 2) + (lane >> 4);  // n % 8
+          const int j = (lane & 7) ^ r7;
+          const int rawoff = r7 * 8 + (lane & 7);  // float4 index within a block
+          const int off0 = r7 * 128 + (((j >> 1) ^ r7) << 4) + (j & 1) * 8;
+          const int off1 = r7 * 128 + (((4 + (j >> 1)) ^ r7) << 4) + (j & 1) * 8;
+          const int nblk = nc >> 3;
           const float sc = ldexpf(1.f, 14 - eb);
           const bool two = 2 * kc + 1 < p.k_chunks;
-          mbar_wait(&bfree[g & 1], ((g >> 1) & 1) ^ 1);
-          uint8_t* bb = bbuf0 + (g & 1) * bbufBytes;
-#pragma unroll 2
-          for (int k = 0; k < 12; ++k) {  // 2 chunks x nb / 128 (<= 6)
-            const int c = k / 6, i = ct + (k % 6) * 128;
-            if (i < nb) {
-              float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
-              if (c == 0 || two) w = braw[c * nb + i];
-              const int n = i >> 3, j = (i & 7) ^ (n & 7);
-              const int off = (n >> 3) * 1024 + (n & 7) * 128 + (((4 * c + (j >> 1)) ^ (n & 7)) << 4) + (j & 1) * 8;
-              uint2 h, l, hi_im, lo_im;  // (p0, q0, p1, q1) -> re rows; (-q0, p0, -q1, p1) -> im rows
-              split_f16x2(w.x * sc, w.y * sc, h.x, l.x);
-              split_f16x2(w.z * sc, w.w * sc, h.y, l.y);
-              hi_im.x = __byte_perm(h.x ^ 0x80000000u, 0, 0x1032);  // (q, p) -> (-q, p) swapped halves
-              hi_im.y = __byte_perm(h.y ^ 0x80000000u, 0, 0x1032);
-              lo_im.x = __byte_perm(l.x ^ 0x80000000u, 0, 0x1032);
-              lo_im.y = __byte_perm(l.y ^ 0x80000000u, 0, 0x1032);
-              *reinterpret_cast<uint2*>(bb + off) = h;
-              *reinterpret_cast<uint2*>(bb + rowsB + off) = hi_im;
-              *reinterpret_cast<uint2*>(bb + 2 * rowsB + off) = l;
-              *reinterpret_cast<uint2*>(bb + 3 * rowsB + off) = lo_im;
-            }
+          float4 v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int c = u >> 2, b = b0 + 3 * (u & 3);
+            v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (b < nblk && (c == 0 || two)) v[u] = braw[c * nb + b * 64 + rawoff];
           }
           mbar_arrive(&rempty[s]);
+          mbar_wait(&bfree[g & 1], ((g >> 1) & 1) ^ 1);
+          uint8_t* bb = bbuf0 + (g & 1) * bbufBytes;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int c = u >> 2, b = b0 + 3 * (u & 3);
+            if (b < nblk) {
+              const float4 w = v[u];  // (p0, q0, p1, q1)
+              const Split p0 = split11(w.x * sc), q0 = split11(w.y * sc);
+              const Split p1 = split11(w.z * sc), q1 = split11(w.w * sc);
+              uint8_t* o = bb + b * 1024 + (c ? off1 : off0);
+              // re rows (p, q); im rows (-q, p)
+              *reinterpret_cast<uint2*>(o) = make_uint2(pack_f16x2(p0.hi, q0.hi), pack_f16x2(p1.hi, q1.hi));
+              *reinterpret_cast<uint2*>(o + rowsB) =
+                  make_uint2(pack_f16x2(-q0.hi, p0.hi), pack_f16x2(-q1.hi, p1.hi));
+              *reinterpret_cast<uint2*>(o + 2 * rowsB) =
+                  make_uint2(pack_f16x2(p0.mid, q0.mid), pack_f16x2(p1.mid, q1.mid));
+              *reinterpret_cast<uint2*>(o + 3 * rowsB) =
+                  make_uint2(pack_f16x2(-q0.mid, p0.mid), pack_f16x2(-q1.mid, p1.mid));
+            }
+          }
         } else {
           float4 v[6];  // nb / 128 <= 6 (nc <= 96)
 #pragma unroll
