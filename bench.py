@@ -153,6 +153,7 @@ def run_reference_arm(args, cfg, label):
         "config": {"workload": label, "k": k, "n": n, "f": f, "f_prime": fo, "S": S,
                    "parallelism": "reference CPU (std::thread parallel_for)"},
         "impl": "reference",
+        "gemm_kind": kind,
         "tflops_equiv": 3 * E / (ms * 1e-3) / 1e12,
         "cpu_baseline": {"value": ms, "unit": "ms", "cores": threads, "kind": "reference",
                          "sample": f"reference run_op_bench<float> (FFT method) fprop+bprop+accGrad on the "
@@ -195,6 +196,8 @@ def main():
     from paper_1312_5851_b200 import ConvWorkspace, LayerConfig
     from paper_1312_5851_b200.rng import ROLE_GRAD_OUTPUT, ROLE_INPUT, ROLE_WEIGHTS, fill_uniform
     from paper_1312_5851_b200.sharded import shard_range
+    from paper_1312_5851_b200 import cost_model
+    from paper_1312_5851_b200._native import gemm_kind
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -302,7 +305,8 @@ def main():
     stage_ms = {op: [statistics.mean(v[i] for v in stage[op]) for i in range(4)] for op in OPS}
 
     hbm_gbs, bf16_tflops, peak_src = load_peaks()
-    tf32x3_tflops = bf16_tflops / 2.0 / 3.0
+    kind = gemm_kind()
+    gemm_tflops = cost_model.gemm_tensor_tflops(bf16_tflops, kind)
     lc = lcfg
     bins = lc.bins()
     # algorithmic bytes per launch of each transform kernel, flops of the GEMM
@@ -329,11 +333,18 @@ def main():
                                "peak": hbm_gbs, "unit": "GB/s", "frac": ach / hbm_gbs,
                                "alg_bytes": alg[op][0] + alg[op][1]})
                 continue
-            if i == 2:
-                ach = alg[op][i] / (t_ms * 1e-3) / 1e12
-                stages.append({"op": op, "kernel": kname[i], "ms": t_ms, "bound": "tensor", "achieved": ach,
-                               "peak": tf32x3_tflops, "unit": "TFLOP/s", "frac": ach / tf32x3_tflops,
-                               "alg_flops": alg[op][i]})
+            if i == 2:  # bound by whichever floor is larger: tensor passes or operand/product bytes
+                gb = cost_model.gemm_bytes(lc)
+                if alg[op][i] / (gemm_tflops * 1e12) >= gb / (hbm_gbs * 1e9):
+                    ach = alg[op][i] / (t_ms * 1e-3) / 1e12
+                    stages.append({"op": op, "kernel": kname[i], "ms": t_ms, "bound": "tensor", "achieved": ach,
+                                   "peak": gemm_tflops, "unit": "TFLOP/s", "frac": ach / gemm_tflops,
+                                   "alg_flops": alg[op][i], "gemm_kind": kind})
+                else:
+                    ach = gb / (t_ms * 1e-3) / 1e9
+                    stages.append({"op": op, "kernel": kname[i], "ms": t_ms, "bound": "hbm", "achieved": ach,
+                                   "peak": hbm_gbs, "unit": "GB/s", "frac": ach / hbm_gbs, "alg_bytes": gb,
+                                   "alg_flops": alg[op][i], "gemm_kind": kind})
             else:
                 ach = alg[op][i] / (t_ms * 1e-3) / 1e9
                 stages.append({"op": op, "kernel": kname[i], "ms": t_ms, "bound": "hbm", "achieved": ach,
@@ -347,12 +358,13 @@ def main():
     dom_st = [s_ for s_ in stages if {"r2c": "r2c_tma_kernel", "c2r": "c2r_tma_kernel"}.get(
         s_["kernel"][:3], s_["kernel"]) == dom]
     dom_ms = statistics.mean(s_["ms"] for s_ in dom_st)
-    if dom == "cgemm_bins_tcgen05":
+    if dom == "cgemm_bins_tcgen05" and dom_st[0]["bound"] == "tensor":
         alg_per_launch = statistics.mean(s_["alg_flops"] for s_ in dom_st)
         achieved = alg_per_launch / (dom_ms * 1e-3) / 1e12
-        roofline = {"bound": "tensor", "achieved": achieved, "peak": tf32x3_tflops, "unit": "TFLOP/s",
-                    "frac": achieved / tf32x3_tflops,
-                    "peak_basis": f"{peak_src} bf16 {bf16_tflops} TF/s / 2 (TF32 rate) / 3 (3xTF32 passes)"}
+        basis = "/ 3 (fp16x3 passes)" if kind == "f16x3" else "/ 2 (TF32 rate) / 3 (3xTF32 passes)"
+        roofline = {"bound": "tensor", "achieved": achieved, "peak": gemm_tflops, "unit": "TFLOP/s",
+                    "frac": achieved / gemm_tflops,
+                    "peak_basis": f"{peak_src} bf16 {bf16_tflops} TF/s {basis}"}
     else:
         alg_per_launch = statistics.mean(s_["alg_bytes"] for s_ in dom_st)
         achieved = alg_per_launch / (dom_ms * 1e-3) / 1e9
@@ -422,13 +434,12 @@ def main():
 
     # fusion-proof pass-level roofline: sum of the stage
     # floors at the measured peaks over the measured pass time
-    from paper_1312_5851_b200 import cost_model
 
     stage_us = {op: {"r2c": 1e3 * (stage_ms[op][0] + (0.0 if stage_ms[op][1] < 0.005 else stage_ms[op][1])),
                      "gemm": 1e3 * stage_ms[op][2],
                      "c2r": 1e3 * stage_ms[op][3]} for op in OPS}
     pass_roof = {op: {k: round(v, 4) for k, v in r.items()}
-                 for op, r in cost_model.roofline_report(lcfg, stage_us, hbm_gbs, tf32x3_tflops).items()}
+                 for op, r in cost_model.roofline_report(lcfg, stage_us, hbm_gbs, gemm_tflops).items()}
 
     E = 2 * S * f * fo * no * no * k * k
     line = {

@@ -74,3 +74,19 @@ def lib() -> C.CDLL:
 def last_error(ws=None) -> str:
     msg = lib().fftconv_b200_last_error(ws)
     return msg.decode() if msg else ""
+
+
+GEMM_KINDS = {"f16x3": 0, "tf32x3": 1}
+
+
+def gemm_kind() -> str:
+    """The K3 precision scheme in effect (include/fftconv_b200.h)."""
+    prev = lib().fftconv_b200_set_gemm_kind(0)
+    lib().fftconv_b200_set_gemm_kind(prev)
+    return {v: k for k, v in GEMM_KINDS.items()}[prev]
+
+
+def set_gemm_kind(kind: str) -> str:
+    """Selects fp16x3 or 3xTF32 for K3; returns the previous kind."""
+    prev = lib().fftconv_b200_set_gemm_kind(GEMM_KINDS[kind])
+    return {v: k for k, v in GEMM_KINDS.items()}[prev]

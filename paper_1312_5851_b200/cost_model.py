@@ -135,14 +135,31 @@ def kernel_bytes(c: LayerConfig, op: str) -> Dict[str, int]:
     raise ValueError(op)
 
 
+def gemm_bytes(c: LayerConfig) -> int:
+    """Algorithmic HBM bytes of the per-bin GEMM (any op): both operand
+    spectra read once, the product spectrum written once.  The three ops
+    pair the dims (S, f), (f', f), (S, f') in some order."""
+    S, f, fo, bins = c.batch, c.in_maps, c.out_maps, c.bins()
+    return 8 * bins * (S * f + fo * f + S * fo)
+
+
+def gemm_tensor_tflops(bf16_tflops: float, kind: str = "f16x3") -> float:
+    """Useful complex-GEMM rate of the tensor cores: 3 MMA passes per
+    product, at the fp16 (= bf16) rate for fp16x3 or half of it for 3xTF32."""
+    return bf16_tflops / 3.0 if kind == "f16x3" else bf16_tflops / 2.0 / 3.0
+
+
 def pass_floor_us(c: LayerConfig, op: str, hbm_gbs: float, tensor_tflops: float) -> Dict[str, float]:
-    """Floors of one pass at the given peaks: transform bytes / HBM and
-    contraction flops / tensor peak (pass-level
-    roofline), in microseconds."""
+    """Floors of one pass at the given peaks: transform bytes / HBM, and for
+    the GEMM the larger of contraction flops / tensor peak and its operand +
+    product bytes / HBM (pass-level roofline), in
+    microseconds."""
     kb = kernel_bytes(c, op)
     out = {k: v / (hbm_gbs * 1e9) * 1e6 for k, v in kb.items()}
-    out["gemm"] = c.contraction_flops() / (tensor_tflops * 1e12) * 1e6
-    out["pass"] = sum(out.values())
+    out["gemm_tensor"] = c.contraction_flops() / (tensor_tflops * 1e12) * 1e6
+    out["gemm_hbm"] = gemm_bytes(c) / (hbm_gbs * 1e9) * 1e6
+    out["gemm"] = max(out["gemm_tensor"], out["gemm_hbm"])
+    out["pass"] = out["r2c"] + out["gemm"] + out["c2r"]
     return out
 
 

@@ -36,8 +36,22 @@ def test_crossover_pad_pow2():
 
 def test_roofline_floors_paper_point():
     c = LayerConfig(7, 32, 96, 96, 128)
-    fl = cm.pass_floor_us(c, "forward", 6551.0, 274.25)
+    fl = cm.pass_floor_us(c, "forward", 6551.0, cm.gemm_tensor_tflops(1645.5, "f16x3"))
     assert math.isclose(sum(cm.kernel_bytes(c, "forward").values()), c.transform_bytes("forward"))
-    assert 20 < fl["r2c"] < 25 and 17 < fl["gemm"] < 20 and 12 < fl["c2r"] < 15
-    rep = cm.roofline_report(c, {"forward": {"r2c": 41.0, "gemm": 31.0, "c2r": 27.0}}, 6551.0, 274.25)
-    assert 0.5 < rep["forward"]["r2c_frac"] < 0.6 and 0.5 < rep["forward"]["pass_frac"] < 0.6
+    # GEMM: 5.13 GFLOP at 548 TF/s = 9.4 us < 147 MB at 6551 GB/s = 22.4 us (HBM-bound)
+    assert cm.gemm_bytes(c) == 8 * 544 * (128 * 96 * 2 + 96 * 96)
+    assert 9 < fl["gemm_tensor"] < 10 and 22 < fl["gemm_hbm"] < 23 and fl["gemm"] == fl["gemm_hbm"]
+    assert 20 < fl["r2c"] < 25 and 12 < fl["c2r"] < 15
+    assert math.isclose(fl["pass"], fl["r2c"] + fl["gemm"] + fl["c2r"])
+    rep = cm.roofline_report(c, {"forward": {"r2c": 41.0, "gemm": 31.0, "c2r": 27.0}}, 6551.0, 548.5)
+    assert 0.5 < rep["forward"]["r2c_frac"] < 0.6 and 0.55 < rep["forward"]["pass_frac"] < 0.65
+
+
+def test_gemm_tensor_rates():
+    assert math.isclose(cm.gemm_tensor_tflops(1645.5, "f16x3"), 548.5)
+    assert math.isclose(cm.gemm_tensor_tflops(1645.5, "tf32x3"), 274.25)
+    # the wide layer's GEMM is tensor-heavier but still byte-bound at fp16x3
+    w = LayerConfig(11, 64, 256, 256, 128)
+    fl = cm.pass_floor_us(w, "forward", 6551.0, 548.5)
+    assert fl["gemm_hbm"] > fl["gemm_tensor"]
+    assert cm.pass_floor_us(w, "forward", 6551.0, 274.25)["gemm_tensor"] > fl["gemm_hbm"]
