@@ -25,6 +25,7 @@
 #include "../../include/fftconv_b200.h"
 #include "cgemm_tcgen05.cuh"
 #include "fft_planes.cuh"
+#include "fft_large.cuh"
 #include "fft_tma.cuh"
 #include "layers.cuh"
 
@@ -184,7 +185,7 @@ static void smem_optin(K kern, int bytes) {
 
 static void size_unsupported(size_t m) {
   throw Error(FFTCONV_B200_SIZE_ERROR,
-              "fft size " + std::to_string(m) + " not supported by the B200 kernels (max 64)");
+              "fft size " + std::to_string(m) + " not supported by the B200 kernels (max 128)");
 }
 
 template <int M>
@@ -282,7 +283,7 @@ static_assert((kGroupPlanes & (kGroupPlanes - 1)) == 0 && kGroupPlanes >= 2, "K4
 
 // Layout the GEMM writes for K4 at fft size m (group-major where the TMA K4
 // kernel groups 16 planes).
-static OutLayout c2r_layout(size_t m) { return (m >= 4 && m <= 32) ? kGroupMajor : kBinMajor; }
+static OutLayout c2r_layout(size_t m) { return ((m >= 4 && m <= 32) || m == kL) ? kGroupMajor : kBinMajor; }
 
 template <int M>
 static void launch_c2r_tma(C2RParams p, const DevInfo& di, cudaStream_t st) {
@@ -312,6 +313,52 @@ static void launch_c2r(size_t m, const C2RParams& p, cudaStream_t st, const DevI
     case 64: return launch_c2r_tma<64>(p, di, st);
     default: size_unsupported(m);
   }
+}
+
+// ---- m = 128: two passes per direction through an L2-sized scratch
+// (fft_large.cuh).  Operand rows are walked in chunks whose scratch fits.
+constexpr size_t kLScratchBudget = (size_t)48 << 20;  // bytes
+
+static size_t large_scratch_budget() {  // FFTCONV_B200_LSCRATCH_MB overrides (tests: force chunking)
+  const char* e = getenv("FFTCONV_B200_LSCRATCH_MB");
+  return (e && atoi(e) > 0) ? ((size_t)atoi(e) << 20) : kLScratchBudget;
+}
+
+static size_t large_scratch_elems(size_t maxJ) {  // float2
+  return std::max(large_scratch_budget() / sizeof(float2), maxJ * kLRows * kL);
+}
+
+static int large_rows_per_chunk(size_t J, size_t width, size_t scratch_elems) {
+  const size_t per_row = J * kLRows * width;
+  const size_t cap = std::min(scratch_elems, large_scratch_budget() / sizeof(float2));
+  return (int)std::max<size_t>(1, cap / std::max<size_t>(per_row, 1));
+}
+
+// Returns the number of launches.
+static int launch_r2c_large(const R2CParams& p, float2* scr, size_t scr_n, cudaStream_t st) {
+  const int rpc = large_rows_per_chunk(p.J, p.src, scr_n);
+  int nl = 0;
+  for (int r0 = 0; r0 < p.R; r0 += rpc) {
+    const int rows = std::min(rpc, p.R - r0);
+    launch_pdl(r2c128_cols_kernel, dim3(rows * p.J, 4), dim3(128), 0, st, p, r0, scr);
+    launch_pdl(r2c128_rows_kernel, dim3(rows, p.kpad / 16, kLRows), dim3(64), 0, st, p, r0,
+               (const float2*)scr);
+    nl += 2;
+  }
+  return nl;
+}
+
+static int launch_c2r_large(const C2RParams& p, float2* scr, size_t scr_n, cudaStream_t st) {
+  const int rpc = large_rows_per_chunk(p.J, p.crop, scr_n);
+  int nl = 0;
+  for (int r0 = 0; r0 < p.R; r0 += rpc) {
+    const int rows = std::min(rpc, p.R - r0);
+    launch_pdl(c2r128_rows_kernel, dim3(rows, (p.J + 15) / 16, kLRows), dim3(64), 0, st, p, r0, scr);
+    launch_pdl(c2r128_cols_kernel, dim3(rows * p.J, (p.crop + 31) / 32), dim3(128), 0, st, p, r0,
+               (const float2*)scr);
+    nl += 2;
+  }
+  return nl;
 }
 
 struct GemmGeom {
@@ -453,6 +500,8 @@ struct fftconv_b200_ws {
   bool pev_ready = false;
   uint64_t ctr[3] = {0, 0, 0};
   unsigned long long* amax = nullptr;  // K1 -> K3 operand max-magnitude words [A, B]
+  float2* lscr = nullptr;              // m = 128 transform scratch (fft_large.cuh)
+  size_t lscr_n = 0;
   unsigned epoch = 0;
   std::string last_error;
   bool timing = false;
@@ -509,9 +558,9 @@ size_t prepare(fftconv_b200_ws* ws, const fftconv_b200_layer& c) {
   if (bins * c.batch * c.in_maps > ws->cap_x || bins * c.out_maps * c.in_maps > ws->cap_w ||
       bins * c.batch * c.out_maps > ws->cap_y)
     throw Error(FFTCONV_B200_CAPACITY_ERROR, "workspace too small for this layer");
-  if (m > 64)
+  if (m > kL)
     throw Error(FFTCONV_B200_SIZE_ERROR,
-                "fft size " + std::to_string(m) + " not supported by the B200 kernels (max 64)");
+                "fft size " + std::to_string(m) + " not supported by the B200 kernels (max 128)");
   return m;
 }
 
@@ -532,9 +581,21 @@ void set_arena(fftconv_b200_ws* ws, size_t na, size_t nb, size_t nd) {
   ws->nD = nd;
 }
 
+void ensure_large_scratch(fftconv_b200_ws* ws, const fftconv_b200_layer& c, size_t m) {
+  if (m != kL) return;
+  const size_t need = large_scratch_elems(std::max({c.batch, c.in_maps, c.out_maps}));
+  if (need <= ws->lscr_n) return;
+  if (ws->lscr) cudaFree(ws->lscr);
+  ws->lscr = nullptr;
+  ws->lscr_n = 0;
+  FCB_CUDA(cudaMalloc(&ws->lscr, need * sizeof(float2)));
+  ws->lscr_n = need;
+}
+
 void ensure_freq(fftconv_b200_ws* ws, Pass pass, const fftconv_b200_layer& c, size_t m) {
   const PassNeed need = pass_need(pass, c.batch, c.in_maps, c.out_maps, m);
   if (need.a > ws->nA || need.b > ws->nB || need.d > ws->nD) set_arena(ws, need.a, need.b, need.d);
+  ensure_large_scratch(ws, c, m);
 }
 
 void record(fftconv_b200_ws* ws, int i, cudaStream_t st) {
@@ -573,7 +634,15 @@ int r2c_operands(fftconv_b200_ws* ws, size_t m, R2CParams& a, R2CParams& b, cuda
     b.amax = ws->amax + 1;
     a.epoch = b.epoch = ++ws->epoch;
   }
+  if (m == kL) return launch_r2c_large(a, ws->lscr, ws->lscr_n, st) + launch_r2c_large(b, ws->lscr, ws->lscr_n, st);
   return launch_r2c_both(m, a, b, st, ws->di);
+}
+
+// K4 for any supported m; returns the number of launches.
+int c2r_run(fftconv_b200_ws* ws, size_t m, const C2RParams& c, cudaStream_t st) {
+  if (m == kL) return launch_c2r_large(c, ws->lscr, ws->lscr_n, st);
+  launch_c2r(m, c, st, ws->di);
+  return 1;
 }
 
 void run_forward(fftconv_b200_ws* ws, const float* x, size_t S, size_t f, size_t xr, size_t xc,
@@ -611,9 +680,9 @@ void run_forward(fftconv_b200_ws* ws, const float* x, size_t S, size_t f, size_t
   }
   record(ws, 3, st);
   c.gm = c2r_layout(m) == kGroupMajor;
-  launch_c2r(m, c, st, ws->di);
+  const int nc = c2r_run(ws, m, c, st);
   record(ws, 4, st);
-  ws->last_launches = nl + 2;
+  ws->last_launches = nl + 1 + nc;
   ws->ctr[0] += S * f + fo * f;
   ws->ctr[1] += S * fo;
   ws->ctr[2] += (uint64_t)bins * fo * f * S;
@@ -655,9 +724,9 @@ void run_grad_input(fftconv_b200_ws* ws, const float* gy, size_t S, size_t fo, s
   }
   record(ws, 3, st);
   c.gm = c2r_layout(m) == kGroupMajor;
-  launch_c2r(m, c, st, ws->di);
+  const int nc = c2r_run(ws, m, c, st);
   record(ws, 4, st);
-  ws->last_launches = nl + 2;
+  ws->last_launches = nl + 1 + nc;
   ws->ctr[0] += S * fo + fo * f;
   ws->ctr[1] += S * f;
   ws->ctr[2] += (uint64_t)bins * fo * f * S;
@@ -695,9 +764,9 @@ void run_grad_weight(fftconv_b200_ws* ws, const float* gy, size_t Sg, size_t fo,
               0, 0, 1.0f / (float)(m * m), (int)round_up(fo, 2)};
   c.gm = c2r_layout(m) == kGroupMajor;
   c.accum = accum;
-  launch_c2r(m, c, st, ws->di);
+  const int nc = c2r_run(ws, m, c, st);
   record(ws, 4, st);
-  ws->last_launches = nl + 2;
+  ws->last_launches = nl + 1 + nc;
   ws->ctr[0] += S * f + S * fo;
   ws->ctr[1] += fo * f;
   ws->ctr[2] += (uint64_t)bins * fo * f * S;
@@ -753,6 +822,7 @@ int fftconv_b200_ws_create(const fftconv_b200_layer* configs, size_t count, int 
         }
       }
       set_arena(ws, na, nb, nd);
+      for (size_t i = 0; i < count; ++i) ensure_large_scratch(ws, configs[i], next_pow2(configs[i].image));
     } catch (...) {
       fftconv_b200_ws_destroy(ws);
       throw;
@@ -768,6 +838,7 @@ void fftconv_b200_ws_destroy(fftconv_b200_ws* ws) {
     for (float* p : {ws->freq, ws->st_in0, ws->st_in1, ws->st_out})
       if (p) cudaFree(p);
     if (ws->amax) cudaFree(ws->amax);
+    if (ws->lscr) cudaFree(ws->lscr);
     if (ws->host_stream) cudaStreamDestroy(ws->host_stream);
     if (ws->h2d_stream) cudaStreamDestroy(ws->h2d_stream);
     if (ws->d2h_stream) cudaStreamDestroy(ws->d2h_stream);
@@ -1061,7 +1132,13 @@ int fftconv_b200_debug_r2c(const float* in, size_t planes, size_t src, size_t m,
     FCB_CUDA(cudaMalloc(&F, bins * planes * kp * 2 * sizeof(float)));
     R2CParams p{in, F, (long long)(src * src), 0, (int)planes, 1, (int)kp, (int)src,
                 (int)(src | 1)};
-    launch_r2c_one(m, p, (cudaStream_t)stream, dev_info(0));
+    float2* scr = nullptr;
+    if (m == kL) {
+      FCB_CUDA(cudaMalloc(&scr, large_scratch_elems(planes) * sizeof(float2)));
+      launch_r2c_large(p, scr, large_scratch_elems(planes), (cudaStream_t)stream);
+    } else {
+      launch_r2c_one(m, p, (cudaStream_t)stream, dev_info(0));
+    }
     // F[(t*planes + p)*32 + 0..1] -> out[(p*bins + t)*2]
     for (size_t pl = 0; pl < planes; ++pl)
       FCB_CUDA(cudaMemcpy2DAsync(out + pl * bins * 2, 2 * sizeof(float), F + pl * kp * 2,
@@ -1069,6 +1146,7 @@ int fftconv_b200_debug_r2c(const float* in, size_t planes, size_t src, size_t m,
                                  cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
     FCB_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
     cudaFree(F);
+    if (scr) cudaFree(scr);
   });
 }
 
@@ -1086,9 +1164,16 @@ int fftconv_b200_debug_c2r(const float* in, size_t planes, size_t m, size_t crop
                                  cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
     C2RParams p{P, out, 0, (long long)(crop * crop), 1, (int)planes, (int)crop, 0, 0,
                 1.0f / (float)(m * m), (int)round_up(planes, 2)};
-    launch_c2r(m, p, (cudaStream_t)stream, dev_info(0));
+    float2* scr = nullptr;
+    if (m == kL) {
+      FCB_CUDA(cudaMalloc(&scr, large_scratch_elems(planes) * sizeof(float2)));
+      launch_c2r_large(p, scr, large_scratch_elems(planes), (cudaStream_t)stream);
+    } else {
+      launch_c2r(m, p, (cudaStream_t)stream, dev_info(0));
+    }
     FCB_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
     cudaFree(P);
+    if (scr) cudaFree(scr);
   });
 }
 
