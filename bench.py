@@ -35,6 +35,8 @@ CONFIGS = {
     "small": (5, 32, 16, 16, 8),
     "paper": (7, 32, 96, 96, 128),
     "wide": (11, 64, 256, 256, 128),
+    # configs[4]'s first layer (f = 3 -> 96, n = 128; FFT size 128)
+    "alex1": (11, 128, 3, 96, 128),
 }
 METRIC = "ms per fprop+bprop+accGrad per layer (S=128) + direct-conv-equiv TFLOP/s"
 OPS = ("forward", "grad_input", "grad_weight")
@@ -45,7 +47,8 @@ def parse_config(name):
         n, k = (int(v) for v in name.split(":")[1].split(","))
         return (k, n, 96, 96, 128), f"kernel/input sweep point S=128 f=f'=96 n={n} k={k}"
     k, n, f, fo, S = CONFIGS[name]
-    label = {"paper": "paper sweep point", "wide": "wide layer", "small": "small layer"}[name]
+    label = {"paper": "paper sweep point", "wide": "wide layer", "small": "small layer",
+             "alex1": "AlexNet-style first layer"}[name]
     return CONFIGS[name], f"{label} S={S} f={f} f'={fo} n={n} k={k}"
 
 

@@ -54,17 +54,21 @@ __device__ __forceinline__ void class_twiddle(float2 (&z)[32]) {
 
 // ---------------------------------------------------------------- r2c K1a
 template <int C>
-__device__ __forceinline__ void r2c128_col_class(const R2CParams& p, const float* col, float2* o, int src) {
+__device__ __forceinline__ void r2c128_col_class(const float* col, float2* o, int src) {
+  // q-outer accumulation keeps one input live at a time (z + 1 load)
   float2 z[32];
   static_for<0, 32>([&](auto Y) {
     constexpr int y0 = decltype(Y)::value;
-    float2 acc = make_float2(0.f, 0.f);
-    static_for<0, 4>([&](auto Q) {
-      constexpr int q = decltype(Q)::value;
-      const int y = y0 + 32 * q;
-      if (y < src) acc = cadd(acc, rot_i<false, (C * q) & 3>(make_float2(__ldg(col + (long long)y * src), 0.f)));
-    });
-    z[y0] = acc;
+    z[y0] = make_float2(y0 < src ? col[y0] : 0.f, 0.f);
+  });
+  static_for<1, 4>([&](auto Q) {
+    constexpr int q = decltype(Q)::value;
+    if (32 * q < src)
+      static_for<0, 32>([&](auto Y) {
+        constexpr int y0 = decltype(Y)::value;
+        const int y = y0 + 32 * q;
+        if (y < src) z[y0] = cadd(z[y0], rot_i<false, (C * q) & 3>(make_float2(col[y0 + 32 * q], 0.f)));
+      });
   });
   class_twiddle<false, C>(z);
   fft_reg<32, false>(z);
@@ -74,21 +78,38 @@ __device__ __forceinline__ void r2c128_col_class(const R2CParams& p, const float
   });
 }
 
-// grid = (rows * J, 4 classes), block = 128 (one thread per column)
-__global__ void __launch_bounds__(128) r2c128_cols_kernel(const R2CParams p, int r0, float2* scr) {
+constexpr int kLColPad = kL + 1;  // odd stride of a transposed (column-contiguous) staged plane
+
+// grid = rows * J (one plane per CTA), block = 256 = (column x, class pair):
+// the plane is staged transposed in smem ([x][y], odd stride: conflict-free
+// both ways) with coalesced loads, so the column reads take immediate
+// offsets; thread (x, g) runs classes g and g + 2.
+// dynamic smem = src * 129 floats.
+__global__ void __launch_bounds__(256, 2) r2c128_cols_kernel(const R2CParams p, int r0, float2* scr) {
+  extern __shared__ float plane_s[];
   pdl_wait();
   pdl_trigger();
   const int ql = blockIdx.x;
   const int r = r0 + ql / p.J, j = ql % p.J;
-  const int x = threadIdx.x, src = p.src;
+  const int src = p.src, n2 = src * src;
+  const float* in = p.in + (long long)r * p.in_sr + (long long)j * p.in_sj;
+  for (int i = threadIdx.x; i < n2; i += 256) {
+    const int y = i / src, x = i - y * src;
+    plane_s[x * kLColPad + y] = __ldg(in + i);
+  }
+  __syncthreads();
+  const int x = threadIdx.x & 127, g = threadIdx.x >> 7;
   if (x >= src) return;
-  const float* col = p.in + (long long)r * p.in_sr + (long long)j * p.in_sj + x;
   float2* o = scr + (long long)ql * kLRows * src + x;
-  switch (blockIdx.y) {
-    case 0: r2c128_col_class<0>(p, col, o, src); break;
-    case 1: r2c128_col_class<1>(p, col, o, src); break;
-    case 2: r2c128_col_class<2>(p, col, o, src); break;
-    default: r2c128_col_class<3>(p, col, o, src); break;
+  const float* col = plane_s + x * kLColPad;
+  if (g == 0) {
+    r2c128_col_class<0>(col, o, src);
+    __syncwarp();
+    r2c128_col_class<2>(col, o, src);
+  } else {
+    r2c128_col_class<1>(col, o, src);
+    __syncwarp();
+    r2c128_col_class<3>(col, o, src);
   }
 }
 
@@ -97,59 +118,78 @@ template <int H>
 __device__ __forceinline__ void r2c128_row_class(const float2* row, float2 (&z)[32], int src) {
   static_for<0, 32>([&](auto X) {
     constexpr int x0 = decltype(X)::value;
-    float2 acc = make_float2(0.f, 0.f);
-    static_for<0, 4>([&](auto Q) {
-      constexpr int q = decltype(Q)::value;
-      if (x0 + 32 * q < src) acc = cadd(acc, rot_i<false, (H * q) & 3>(row[x0 + 32 * q]));
-    });
-    z[x0] = acc;
+    z[x0] = x0 < src ? row[x0] : make_float2(0.f, 0.f);
+  });
+  static_for<1, 4>([&](auto Q) {
+    constexpr int q = decltype(Q)::value;
+    if (32 * q < src)
+      static_for<0, 32>([&](auto X) {
+        constexpr int x0 = decltype(X)::value;
+        if (x0 + 32 * q < src) z[x0] = cadd(z[x0], rot_i<false, (H * q) & 3>(row[x0 + 32 * q]));
+      });
   });
   class_twiddle<false, H>(z);
   fft_reg<32, false>(z);
 }
 
-constexpr int kLRowPad = kL + 1;  // odd float2 stride of the staged rows
+constexpr int kLRowPad = kL + 1;                 // odd float2 stride of the staged rows
+constexpr int kLRowBuf = 16 * kLRowPad;          // float2 per staged u row (>= 128 x 16 tile)
+constexpr int kLUPerCta = 2;                     // u rows per K1b / K4a CTA
 
-// grid = (rows, kpad / 16, 65), block = 64 = (plane jl, v class h)
-__global__ void __launch_bounds__(64) r2c128_rows_kernel(const R2CParams p, int r0, const float2* scr) {
-  __shared__ float2 rows_s[16 * kLRowPad];
-  __shared__ __align__(16) float2 tile[kL * 16];  // [v][plane]
+// grid = (rows, kpad / 16, ceil(65 / 2)), block = 128 = (u row, plane jl,
+// v class h).  The 16 staged scratch rows of a u row are overwritten by
+// its [v][plane] output tile once every thread holds its FFT.
+__global__ void __launch_bounds__(128) r2c128_rows_kernel(const R2CParams p, int r0, const float2* scr) {
+  __shared__ __align__(16) float2 buf[kLUPerCta * kLRowBuf];
   pdl_wait();
   pdl_trigger();
   const int rl = blockIdx.x, r = r0 + rl;
-  const int j0 = blockIdx.y * 16, u = blockIdx.z;
+  const int j0 = blockIdx.y * 16;
   const int jv = max(0, min(16, p.J - j0));
   const int src = p.src;
-  for (int i = threadIdx.x; i < 16 * src; i += 64) {
-    const int jl = i / src, x = i - jl * src;
-    rows_s[jl * kLRowPad + x] =
-        jl < jv ? scr[((long long)(rl * p.J + j0 + jl) * kLRows + u) * src + x] : make_float2(0.f, 0.f);
-  }
+  const int ul = threadIdx.x >> 6, u = blockIdx.z * kLUPerCta + ul;
+  const int t = threadIdx.x & 63;
+  float2* rows_s = buf + ul * kLRowBuf;
+  if (u < kLRows)
+    for (int i = t; i < jv * src; i += 64) {
+      const int jl = i / src, x = i - jl * src;
+      rows_s[jl * kLRowPad + x] = scr[((long long)(rl * p.J + j0 + jl) * kLRows + u) * src + x];
+    }
   __syncthreads();
-  const int jl = threadIdx.x & 15, h = threadIdx.x >> 4;
+  const int jl = t & 15, h = t >> 4;
   float2 z[32];
-  const float2* row = rows_s + jl * kLRowPad;
-  switch (h) {
-    case 0: r2c128_row_class<0>(row, z, src); break;
-    case 1: r2c128_row_class<1>(row, z, src); break;
-    case 2: r2c128_row_class<2>(row, z, src); break;
-    default: r2c128_row_class<3>(row, z, src); break;
+  const bool act = u < kLRows && jl < jv;
+  if (act) {
+    const float2* row = rows_s + jl * kLRowPad;
+    switch (h) {
+      case 0: r2c128_row_class<0>(row, z, src); break;
+      case 1: r2c128_row_class<1>(row, z, src); break;
+      case 2: r2c128_row_class<2>(row, z, src); break;
+      default: r2c128_row_class<3>(row, z, src); break;
+    }
   }
+  __syncthreads();  // rows read: reuse as the tile
+  float2* tile = rows_s;  // [v][16]
   const float csign = p.conj ? -1.f : 1.f;
   uint32_t amx = 0;
+  if (u < kLRows) {
 #pragma unroll
-  for (int k = 0; k < 32; ++k) {
-    const float2 v = jl < jv ? make_float2(z[k].x, csign * z[k].y) : make_float2(0.f, 0.f);
-    tile[(4 * k + h) * 16 + jl] = v;
-    amx = max(amx, max(__float_as_uint(v.x) & 0x7fffffffu, __float_as_uint(v.y) & 0x7fffffffu));
+    for (int k = 0; k < 32; ++k) {
+      const float2 v = act ? make_float2(z[k].x, csign * z[k].y) : make_float2(0.f, 0.f);
+      tile[(4 * k + h) * 16 + jl] = v;
+      amx = max(amx, max(__float_as_uint(v.x) & 0x7fffffffu, __float_as_uint(v.y) & 0x7fffffffu));
+    }
   }
   __syncthreads();
-  // 128 bins x 16 planes: one 128-B line per bin
+  // 128 bins x 16 planes per u row: one 128-B line per bin
   const long long bstride = (long long)p.R * p.kpad;  // float2 per bin
-  float2* out = reinterpret_cast<float2*>(p.out) + (long long)u * kL * bstride + (long long)r * p.kpad + j0;
-  for (int i = threadIdx.x; i < kL * 8; i += 64) {
-    const int v = i >> 3, part = i & 7;
-    *reinterpret_cast<float4*>(out + v * bstride + 2 * part) = *reinterpret_cast<const float4*>(tile + v * 16 + 2 * part);
+  if (u < kLRows) {
+    float2* out = reinterpret_cast<float2*>(p.out) + (long long)u * kL * bstride + (long long)r * p.kpad + j0;
+    for (int i = t; i < kL * 8; i += 64) {
+      const int v = i >> 3, part = i & 7;
+      *reinterpret_cast<float4*>(out + v * bstride + 2 * part) =
+          *reinterpret_cast<const float4*>(tile + v * 16 + 2 * part);
+    }
   }
   if (p.amax) {
     amx = __reduce_max_sync(0xffffffffu, amx);
@@ -160,105 +200,141 @@ __global__ void __launch_bounds__(64) r2c128_rows_kernel(const R2CParams p, int 
 // ---------------------------------------------------------------- c2r K4a
 template <int H>
 __device__ __forceinline__ void c2r128_row_class(const float2* tile, int jl, float2 (&z)[32]) {
-  static_for<0, 32>([&](auto V) {
-    constexpr int v0 = decltype(V)::value;
-    float2 acc = make_float2(0.f, 0.f);
-    static_for<0, 4>([&](auto Q) {
-      constexpr int q = decltype(Q)::value;
-      acc = cadd(acc, rot_i<true, (H * q) & 3>(tile[(v0 + 32 * q) * 17 + jl]));
+  static_for<0, 32>([&](auto V) { z[decltype(V)::value] = tile[decltype(V)::value * 17 + jl]; });
+  static_for<1, 4>([&](auto Q) {
+    constexpr int q = decltype(Q)::value;
+    static_for<0, 32>([&](auto V) {
+      constexpr int v0 = decltype(V)::value;
+      z[v0] = cadd(z[v0], rot_i<true, (H * q) & 3>(tile[(v0 + 32 * q) * 17 + jl]));
     });
-    z[v0] = acc;
   });
   class_twiddle<true, H>(z);
   fft_reg<32, true>(z);
 }
 
-// grid = (rows, ceil(J / 16), 65), block = 64 = (plane jl, x' class h)
-__global__ void __launch_bounds__(64) c2r128_rows_kernel(const C2RParams p, int r0, float2* scr) {
-  __shared__ float2 tile[kL * 17];  // [v][plane], odd stride
-  __shared__ float2 outb[16 * kLRowPad];
+constexpr int kLTile = kL * 17;  // [v][16 planes] with an odd stride (>= kLRowBuf)
+static_assert(kLTile >= kLRowBuf, "K4a reuses the input tile for the output rows");
+
+// grid = (rows, ceil(J / 16), ceil(65 / 2)), block = 128 = (u row, plane jl,
+// x' class h).  The input tile of a u row is overwritten by its cropped
+// output rows once every thread holds its FFT.
+__global__ void __launch_bounds__(128) c2r128_rows_kernel(const C2RParams p, int r0, float2* scr) {
+  __shared__ float2 buf[kLUPerCta * kLTile];
   pdl_wait();
   pdl_trigger();
   const int rl = blockIdx.x, r = r0 + rl;
-  const int jg = blockIdx.y, j0 = jg * 16, u = blockIdx.z;
+  const int jg = blockIdx.y, j0 = jg * 16;
   const int jv = min(16, p.J - j0);
   const int crop = p.crop;
+  const int ul = threadIdx.x >> 6, u = blockIdx.z * kLUPerCta + ul;
+  const int t = threadIdx.x & 63;
+  float2* tile = buf + ul * kLTile;
   const float2* in = reinterpret_cast<const float2*>(p.in);
-  if (p.gm) {  // P[r][J/16][t][16]: the 128 bins x 16 planes of row u are contiguous
-    const int ngj = (p.J + 15) >> 4;
-    const float2* b = in + (((long long)r * ngj + jg) * (kL * kLRows) + (long long)u * kL) * 16;
-    for (int i = threadIdx.x; i < kL * 16; i += 64) tile[(i >> 4) * 17 + (i & 15)] = __ldg(b + i);
-  } else {  // P[t][r][ld]
-    const long long bstride = (long long)p.R * p.ld;
-    for (int i = threadIdx.x; i < kL * 16; i += 64) {
-      const int v = i >> 4, jl = i & 15;
-      tile[v * 17 + jl] = jl < jv ? __ldg(in + ((long long)u * kL + v) * bstride + (long long)r * p.ld + j0 + jl)
-                                  : make_float2(0.f, 0.f);
+  if (u < kLRows) {
+    if (p.gm) {  // P[r][J/16][t][16]: the 128 bins x 16 planes of row u are contiguous
+      const int ngj = (p.J + 15) >> 4;
+      const float4* b = reinterpret_cast<const float4*>(
+          in + (((long long)r * ngj + jg) * (kL * kLRows) + (long long)u * kL) * 16);
+      for (int i = t; i < kL * 8; i += 64) {
+        const float4 v = __ldg(b + i);
+        const int bin = i >> 3, jl = (i & 7) * 2;
+        tile[bin * 17 + jl] = make_float2(v.x, v.y);
+        tile[bin * 17 + jl + 1] = make_float2(v.z, v.w);
+      }
+    } else {  // P[t][r][ld]
+      const long long bstride = (long long)p.R * p.ld;
+      for (int i = t; i < kL * 16; i += 64) {
+        const int v = i >> 4, jl = i & 15;
+        tile[v * 17 + jl] = jl < jv ? __ldg(in + ((long long)u * kL + v) * bstride + (long long)r * p.ld + j0 + jl)
+                                    : make_float2(0.f, 0.f);
+      }
     }
   }
   __syncthreads();
-  const int jl = threadIdx.x & 15, h = threadIdx.x >> 4;
+  const int jl = t & 15, h = t >> 4;
+  const bool act = u < kLRows && jl < jv;
   float2 z[32];
-  switch (h) {
-    case 0: c2r128_row_class<0>(tile, jl, z); break;
-    case 1: c2r128_row_class<1>(tile, jl, z); break;
-    case 2: c2r128_row_class<2>(tile, jl, z); break;
-    default: c2r128_row_class<3>(tile, jl, z); break;
+  if (act) {
+    switch (h) {
+      case 0: c2r128_row_class<0>(tile, jl, z); break;
+      case 1: c2r128_row_class<1>(tile, jl, z); break;
+      case 2: c2r128_row_class<2>(tile, jl, z); break;
+      default: c2r128_row_class<3>(tile, jl, z); break;
+    }
   }
+  __syncthreads();  // tile read: reuse it for the output rows [plane][x']
+  float2* outb = tile;
+  if (act) {
 #pragma unroll
-  for (int k = 0; k < 32; ++k)
-    if (4 * k + h < crop) outb[jl * kLRowPad + 4 * k + h] = z[k];
-  __syncthreads();
-  for (int i = threadIdx.x; i < jv * crop; i += 64) {
-    const int l = i / crop, x = i - l * crop;
-    scr[((long long)(rl * p.J + j0 + l) * kLRows + u) * crop + x] = outb[l * kLRowPad + x];
+    for (int k = 0; k < 32; ++k)
+      if (4 * k + h < crop) outb[jl * kLRowPad + 4 * k + h] = z[k];
   }
+  __syncthreads();
+  if (u < kLRows)
+    for (int i = t; i < jv * crop; i += 64) {
+      const int l = i / crop, x = i - l * crop;
+      scr[((long long)(rl * p.J + j0 + l) * kLRows + u) * crop + x] = outb[l * kLRowPad + x];
+    }
 }
 
 // ---------------------------------------------------------------- c2r K4b
 template <int C>
 __device__ __forceinline__ void c2r128_col_class(const C2RParams& p, const float2* col, float* o, int crop) {
   float2 z[32];
-  static_for<0, 32>([&](auto U) {
-    constexpr int u0 = decltype(U)::value;
-    float2 acc = make_float2(0.f, 0.f);
-    static_for<0, 4>([&](auto Q) {
-      constexpr int q = decltype(Q)::value;
+  static_for<0, 32>([&](auto U) { z[decltype(U)::value] = col[decltype(U)::value]; });
+  static_for<1, 4>([&](auto Q) {
+    constexpr int q = decltype(Q)::value;
+    static_for<0, 32>([&](auto U) {
+      constexpr int u0 = decltype(U)::value;
       constexpr int u = u0 + 32 * q;
-      const float2 v = u < kLRows ? __ldg(col + (long long)u * crop) : cconj(__ldg(col + (long long)(kL - u) * crop));
-      acc = cadd(acc, rot_i<true, (C * q) & 3>(v));
+      const float2 v = u < kLRows ? col[u] : cconj(col[kL - u]);
+      z[u0] = cadd(z[u0], rot_i<true, (C * q) & 3>(v));
     });
-    z[u0] = acc;
   });
   class_twiddle<true, C>(z);
   fft_reg<32, true>(z);
   const float scale = p.scale;
-#pragma unroll
-  for (int k = 0; k < 32; ++k) {
-    const int y = 4 * k + C;
-    if (y < crop) {
-      float* d = o + (long long)y * crop;
-      *d = p.accum ? *d + scale * z[k].x : scale * z[k].x;
-    }
-  }
+  const bool accum = p.accum;
+  const long long step = 4LL * crop;
+  float* d = o + (long long)C * crop;  // walks rows y = 4k + C
+  static_for<0, 32>([&](auto K) {
+    constexpr int k = decltype(K)::value;
+    if (4 * k + C < crop) *d = accum ? *d + scale * z[k].x : scale * z[k].x;
+    d += step;
+  });
 }
 
-// grid = (rows * J, ceil(crop / 32)), block = 128 = (column lane, y class)
-__global__ void __launch_bounds__(128) c2r128_cols_kernel(const C2RParams p, int r0, const float2* scr) {
+// grid = rows * J (one plane per CTA), block = 256 = (column x', class
+// pair): the plane's 65 x crop scratch rows are staged transposed in smem
+// ([x'][u], stride 65: conflict-free 64-bit accesses per half-warp) with
+// coalesced loads; thread (x', g) runs classes g and g + 2.
+// dynamic smem = crop * 65 float2.
+__global__ void __launch_bounds__(256, 2) c2r128_cols_kernel(const C2RParams p, int r0, const float2* scr) {
+  extern __shared__ float2 zs[];
   pdl_wait();
   pdl_trigger();
   const int ql = blockIdx.x;
   const int r = r0 + ql / p.J, j = ql % p.J;
-  const int crop = p.crop;
-  const int x = blockIdx.y * 32 + (threadIdx.x & 31);
+  const int crop = p.crop, nz = kLRows * crop;
+  const float2* src = scr + (long long)ql * nz;
+  for (int i = threadIdx.x; i < nz; i += 256) {
+    const int u = i / crop, x = i - u * crop;
+    zs[x * kLRows + u] = src[i];
+  }
+  __syncthreads();
+  const int x = threadIdx.x & 127, g = threadIdx.x >> 7;
   if (x >= crop) return;
-  const float2* col = scr + (long long)ql * kLRows * crop + x;
   float* o = p.out + (long long)r * p.out_sr + (long long)j * p.out_sj + x;
-  switch (threadIdx.x >> 5) {
-    case 0: c2r128_col_class<0>(p, col, o, crop); break;
-    case 1: c2r128_col_class<1>(p, col, o, crop); break;
-    case 2: c2r128_col_class<2>(p, col, o, crop); break;
-    default: c2r128_col_class<3>(p, col, o, crop); break;
+  const float2* col = zs + x * kLRows;
+  // __syncwarp between the classes keeps their register live ranges apart
+  if (g == 0) {
+    c2r128_col_class<0>(p, col, o, crop);
+    __syncwarp();
+    c2r128_col_class<2>(p, col, o, crop);
+  } else {
+    c2r128_col_class<1>(p, col, o, crop);
+    __syncwarp();
+    c2r128_col_class<3>(p, col, o, crop);
   }
 }
 

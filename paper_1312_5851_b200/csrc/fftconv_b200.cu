@@ -340,9 +340,11 @@ static int launch_r2c_large(const R2CParams& p, float2* scr, size_t scr_n, cudaS
   int nl = 0;
   for (int r0 = 0; r0 < p.R; r0 += rpc) {
     const int rows = std::min(rpc, p.R - r0);
-    launch_pdl(r2c128_cols_kernel, dim3(rows * p.J, 4), dim3(128), 0, st, p, r0, scr);
-    launch_pdl(r2c128_rows_kernel, dim3(rows, p.kpad / 16, kLRows), dim3(64), 0, st, p, r0,
-               (const float2*)scr);
+    const int smem = p.src * kLColPad * (int)sizeof(float);
+    smem_optin(r2c128_cols_kernel, smem);
+    launch_pdl(r2c128_cols_kernel, dim3(rows * p.J), dim3(256), smem, st, p, r0, scr);
+    launch_pdl(r2c128_rows_kernel, dim3(rows, p.kpad / 16, (kLRows + kLUPerCta - 1) / kLUPerCta), dim3(128), 0,
+               st, p, r0, (const float2*)scr);
     nl += 2;
   }
   return nl;
@@ -353,9 +355,11 @@ static int launch_c2r_large(const C2RParams& p, float2* scr, size_t scr_n, cudaS
   int nl = 0;
   for (int r0 = 0; r0 < p.R; r0 += rpc) {
     const int rows = std::min(rpc, p.R - r0);
-    launch_pdl(c2r128_rows_kernel, dim3(rows, (p.J + 15) / 16, kLRows), dim3(64), 0, st, p, r0, scr);
-    launch_pdl(c2r128_cols_kernel, dim3(rows * p.J, (p.crop + 31) / 32), dim3(128), 0, st, p, r0,
-               (const float2*)scr);
+    launch_pdl(c2r128_rows_kernel, dim3(rows, (p.J + 15) / 16, (kLRows + kLUPerCta - 1) / kLUPerCta),
+               dim3(128), 0, st, p, r0, scr);
+    const int smem = kLRows * p.crop * (int)sizeof(float2);
+    smem_optin(c2r128_cols_kernel, smem);
+    launch_pdl(c2r128_cols_kernel, dim3(rows * p.J), dim3(256), smem, st, p, r0, (const float2*)scr);
     nl += 2;
   }
   return nl;

@@ -169,6 +169,11 @@ def parse_network(text: str) -> NetworkSpec:
 PRESETS = {  # layers.hpp:321-348
     "reference-net": (128, "conv 11 32 3 96\nrelu\nconv 7 32 96 256\nrelu\npool\nconv 5 16 256 384\nrelu\n"
                            "conv 5 16 384 384\nrelu\nconv 3 16 384 384\nrelu\npool\nfc 1000\n"),
+    # BASELINE configs[4] ("AlexNet-style 5-conv-layer stack, first layer
+    # f = 3 -> 96, n = 128") in the reference grammar: AlexNet's map counts
+    # and kernel sizes, fit_to between layers as in the reference preset
+    "alexnet-128": (128, "conv 11 128 3 96\nrelu\npool\nconv 5 64 96 256\nrelu\npool\nconv 3 32 256 384\nrelu\n"
+                         "conv 3 32 384 384\nrelu\nconv 3 32 384 256\nrelu\npool\nfc 1000\n"),
     "reference-net-small": (8, "conv 11 32 3 12\nrelu\nconv 7 32 12 32\nrelu\npool\nconv 5 16 32 48\nrelu\n"
                                "conv 5 16 48 48\nrelu\nconv 3 16 48 48\nrelu\npool\nfc 1000\n"),
 }
