@@ -156,7 +156,6 @@ def run_reference_arm(args, cfg, label):
         "config": {"workload": label, "k": k, "n": n, "f": f, "f_prime": fo, "S": S,
                    "parallelism": "reference CPU (std::thread parallel_for)"},
         "impl": "reference",
-        "gemm_kind": kind,
         "tflops_equiv": 3 * E / (ms * 1e-3) / 1e12,
         "cpu_baseline": {"value": ms, "unit": "ms", "cores": threads, "kind": "reference",
                          "sample": f"reference run_op_bench<float> (FFT method) fprop+bprop+accGrad on the "
@@ -455,6 +454,7 @@ def main():
                    "parallelism": f"dp{world} (minibatch-sharded, NCCL all-reduce of gw)" if world > 1 else "dp1",
                    "l2": "flushed between timed steps (256 MiB write)"},
         "tflops_equiv": 3 * E / (ms * 1e-3) / 1e12,
+        "gemm_kind": kind,
         "per_op_ms": {op: sum(stage_ms[op]) for op in OPS},
         "roofline": roofline,
         "pass_roofline": pass_roof,

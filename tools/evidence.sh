@@ -1,0 +1,21 @@
+#!/bin/bash
+# Round evidence on one B200: GPU tests, bench lines, launch list, ncu --set full
+# captures (summarised by tools/ncu_summarize.py afterwards, in the container).
+#   gpurun --timeout 2400 -- 'bash tools/evidence.sh v6'
+V=${1:-vX}
+O=gpurun_out/ev_$V
+mkdir -p $O
+timeout 1500 python -m pytest tests -m gpu -q -x > $O/pytest_gpu.log 2>&1; tail -3 $O/pytest_gpu.log
+timeout 400 python bench.py > $O/bench_paper.json 2> $O/bench_paper.err
+timeout 400 python bench.py --config wide > $O/bench_wide.json 2> $O/bench_wide.err
+timeout 400 python bench.py --impl reference > $O/bench_reference_arm.json 2> $O/bench_reference_arm.err
+timeout 400 python bench.py --config stack > $O/bench_stack.json 2> $O/bench_stack.err
+timeout 400 python bench.py --config stack:alexnet-128 --steps 5 --warmup 3 > $O/bench_stack_alexnet.json 2> $O/bench_stack_alexnet.err
+timeout 600 python bench.py --config alex1 > $O/bench_alex1.json 2> $O/bench_alex1.err
+timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_paper.csv \
+  python bench.py --steps 2 --warmup 1 > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:'r2c|cgemm|c2r' -s 9 -c 9 \
+  -o $O/prof_paper python tools/profile_step.py --config paper > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'r2c|cgemm|c2r' -s 9 -c 9 \
+  -o $O/prof_wide python tools/profile_step.py --config wide > /dev/null 2>&1
+ls -la $O

@@ -25,7 +25,7 @@ SCALE = {"us": 1.0, "ms": 1e3, "ns": 1e-3, "byte": 1e-6, "Kbyte": 1e-3, "Mbyte":
 
 
 def kernel_key(name):
-    m = re.search(r"(r2c_tma_kernel|c2r_tma_kernel|cgemm_bins_tcgen05|r2c_planes_kernel|c2r_planes_kernel)", name)
+    m = re.search(r"(r2c_tma_kernel|c2r_tma_kernel|cgemm_bins_tcgen05|r2c_planes_kernel|c2r_planes_kernel|r2c128_cols_kernel|r2c128_rows_kernel|c2r128_rows_kernel|c2r128_cols_kernel)", name)
     return m.group(1) if m else name
 
 
