@@ -469,7 +469,12 @@ struct TC2R {
   static constexpr int P1W = ceil32_i(P1), P2W = ceil32_i(P2);
   static constexpr int NPIPE = (!BIG && S % 2 == 0) ? 2 : 1;
   static constexpr int THREADS = 32 + NPIPE * (P1W + P2W);
-  static constexpr int SMEM = S * STAGE + 4 * S * 8 + 128;
+  static constexpr int TW = S * STAGE + 4 * S * 8;  // inverse twiddle table e^(+2 pi i k / M), M float2
+  static constexpr int SMEM = TW + M * 8 + 128;
+  // small crops (weight gradients): pass 2 evaluates each output as a direct
+  // Hermitian DFT over u, one (plane, row, column) per item, instead of one
+  // FFT per column (pair) that would leave most pass-2 threads idle
+  static constexpr int DFT_MAX_ITEMS = 4;  // per pass-2 thread
   static constexpr uint32_t BOX_BYTES = 2 * G * 4 * M;  // one u row
   static_assert(G * M * M * 4 <= STAGE, "a staged output tile must fit a stage");
 };
@@ -486,9 +491,13 @@ __global__ void __launch_bounds__(TC2R<M>::THREADS, 1)
   uint64_t* mid = full + S;
   uint64_t* empty = mid + S;  // pass 2 read the stage (direct-store mode)
   uint64_t* outb = empty + S;  // pass 2 wrote the output tile (bulk mode)
+  float2* twt = reinterpret_cast<float2*>(smem + T::TW);
   const int ngj = (p.J + G - 1) / G;
   const int ngroups = p.R * ngj;
   const int crop = p.crop;
+  const bool dft2 = crop <= M / 4 && G * crop * crop <= T::DFT_MAX_ITEMS * T::P2W;
+  if (threadIdx.x == 32)
+    static_for<0, M>([&](auto K) { twt[decltype(K)::value] = tw128c<true, decltype(K)::value * (128 / M)>(); });
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
@@ -623,7 +632,60 @@ __global__ void __launch_bounds__(TC2R<M>::THREADS, 1)
       const int jv = min(G, p.J - j0);
       const float2* inter = reinterpret_cast<const float2*>(smem + s * T::STAGE);
       mbar_wait(&mid[s], (i / S) & 1);
-      if constexpr (!T::BIG) {
+      if (dft2) {
+        // x[y] = Re Z[0] + (-1)^y Re Z[M/2] + 2 sum_{0<u<M/2} Re(Z[u] e^(2 pi i u y / M))
+        // (the imaginary parts of Z[0] and Z[M/2] are dropped, as c2r does);
+        // items y-major so a warp shares few y (twiddle-table broadcasts)
+        const int per_y = jv * crop, items = per_y * crop;
+        float res[T::DFT_MAX_ITEMS];
+#pragma unroll
+        for (int q = 0; q < T::DFT_MAX_ITEMS; ++q) {
+          const int it = t + q * T::P2W;
+          res[q] = 0.f;
+          if (it < items) {
+            const int y = it / per_y, rem = it - y * per_y;
+            const int jl = rem / crop, c = rem - jl * crop;
+            const float2* col = inter + jl * PS + c;
+            float acc = 0.f;
+            static_for<1, M / 2>([&](auto U) {
+              constexpr int u = decltype(U)::value;
+              const float2 z = col[u * CP];
+              const float2 w = twt[(u * y) & (M - 1)];
+              acc = fmaf(z.x, w.x, fmaf(-z.y, w.y, acc));
+            });
+            const float e = col[0].x + ((y & 1) ? -col[(M / 2) * CP].x : col[(M / 2) * CP].x);
+            res[q] = (e + 2.f * acc) * scale;
+          }
+        }
+        if (p.bulk) {
+          named_bar_sync(1 + T::NPIPE + pipe, T::P2W);  // stage read: reuse it as the output tile
+          float* tile = reinterpret_cast<float*>(smem + s * T::STAGE);
+#pragma unroll
+          for (int q = 0; q < T::DFT_MAX_ITEMS; ++q) {
+            const int it = t + q * T::P2W;
+            if (it < items) {
+              const int y = it / per_y, rem = it - y * per_y;
+              const int jl = rem / crop, c = rem - jl * crop;
+              tile[jl * crop * crop + y * crop + c] = res[q];
+            }
+          }
+          fence_proxy_async_smem();
+          mbar_arrive(&outb[s]);
+        } else {
+          mbar_arrive(&empty[s]);
+#pragma unroll
+          for (int q = 0; q < T::DFT_MAX_ITEMS; ++q) {
+            const int it = t + q * T::P2W;
+            if (it < items) {
+              const int y = it / per_y, rem = it - y * per_y;
+              const int jl = rem / crop, c = rem - jl * crop;
+              float* d = p.out + (long long)r * p.out_sr + (long long)(j0 + jl) * p.out_sj + y * crop + c;
+              *d = res[q] + (p.accum ? *d : 0.f);
+            }
+          }
+        }
+        if (t == 0) XTRACE(4, i);
+      } else if constexpr (!T::BIG) {
         // (plane, column-pair) items packed densely over the valid planes;
         // columns (c, c + H) form one complex inverse FFT
         const int H = (crop + 1) >> 1;
