@@ -93,6 +93,7 @@ __global__ void __launch_bounds__(256, 2) r2c128_cols_kernel(const R2CParams p, 
   const int r = r0 + ql / p.J, j = ql % p.J;
   const int src = p.src, n2 = src * src;
   const float* in = p.in + (long long)r * p.in_sr + (long long)j * p.in_sj;
+#pragma unroll 8
   for (int i = threadIdx.x; i < n2; i += 256) {
     const int y = i / src, x = i - y * src;
     plane_s[x * kLColPad + y] = __ldg(in + i);
@@ -151,6 +152,7 @@ __global__ void __launch_bounds__(128) r2c128_rows_kernel(const R2CParams p, int
   const int t = threadIdx.x & 63;
   float2* rows_s = buf + ul * kLRowBuf;
   if (u < kLRows)
+#pragma unroll 8
     for (int i = t; i < jv * src; i += 64) {
       const int jl = i / src, x = i - jl * src;
       rows_s[jl * kLRowPad + x] = scr[((long long)(rl * p.J + j0 + jl) * kLRows + u) * src + x];
@@ -185,6 +187,7 @@ __global__ void __launch_bounds__(128) r2c128_rows_kernel(const R2CParams p, int
   const long long bstride = (long long)p.R * p.kpad;  // float2 per bin
   if (u < kLRows) {
     float2* out = reinterpret_cast<float2*>(p.out) + (long long)u * kL * bstride + (long long)r * p.kpad + j0;
+#pragma unroll 8
     for (int i = t; i < kL * 8; i += 64) {
       const int v = i >> 3, part = i & 7;
       *reinterpret_cast<float4*>(out + v * bstride + 2 * part) =
@@ -235,6 +238,7 @@ __global__ void __launch_bounds__(128) c2r128_rows_kernel(const C2RParams p, int
       const int ngj = (p.J + 15) >> 4;
       const float4* b = reinterpret_cast<const float4*>(
           in + (((long long)r * ngj + jg) * (kL * kLRows) + (long long)u * kL) * 16);
+#pragma unroll 8
       for (int i = t; i < kL * 8; i += 64) {
         const float4 v = __ldg(b + i);
         const int bin = i >> 3, jl = (i & 7) * 2;
@@ -243,6 +247,7 @@ __global__ void __launch_bounds__(128) c2r128_rows_kernel(const C2RParams p, int
       }
     } else {  // P[t][r][ld]
       const long long bstride = (long long)p.R * p.ld;
+#pragma unroll 8
       for (int i = t; i < kL * 16; i += 64) {
         const int v = i >> 4, jl = i & 15;
         tile[v * 17 + jl] = jl < jv ? __ldg(in + ((long long)u * kL + v) * bstride + (long long)r * p.ld + j0 + jl)
@@ -271,6 +276,7 @@ __global__ void __launch_bounds__(128) c2r128_rows_kernel(const C2RParams p, int
   }
   __syncthreads();
   if (u < kLRows)
+#pragma unroll 8
     for (int i = t; i < jv * crop; i += 64) {
       const int l = i / crop, x = i - l * crop;
       scr[((long long)(rl * p.J + j0 + l) * kLRows + u) * crop + x] = outb[l * kLRowPad + x];
@@ -317,6 +323,7 @@ __global__ void __launch_bounds__(256, 2) c2r128_cols_kernel(const C2RParams p, 
   const int r = r0 + ql / p.J, j = ql % p.J;
   const int crop = p.crop, nz = kLRows * crop;
   const float2* src = scr + (long long)ql * nz;
+#pragma unroll 8
   for (int i = threadIdx.x; i < nz; i += 256) {
     const int u = i / crop, x = i - u * crop;
     zs[x * kLRows + u] = src[i];
