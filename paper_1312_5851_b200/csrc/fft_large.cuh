@@ -91,15 +91,14 @@ __global__ void __launch_bounds__(256, 2) r2c128_cols_kernel(const R2CParams p, 
   pdl_trigger();
   const int ql = blockIdx.x;
   const int r = r0 + ql / p.J, j = ql % p.J;
-  const int src = p.src, n2 = src * src;
+  const int src = p.src;
   const float* in = p.in + (long long)r * p.in_sr + (long long)j * p.in_sj;
+  const int x = threadIdx.x & 127, g = threadIdx.x >> 7;
+  if (x < src) {  // row y of the plane: lanes = consecutive columns (coalesced)
 #pragma unroll 8
-  for (int i = threadIdx.x; i < n2; i += 256) {
-    const int y = i / src, x = i - y * src;
-    plane_s[x * kLColPad + y] = __ldg(in + i);
+    for (int y = g; y < src; y += 2) plane_s[x * kLColPad + y] = __ldg(in + y * src + x);
   }
   __syncthreads();
-  const int x = threadIdx.x & 127, g = threadIdx.x >> 7;
   if (x >= src) return;
   float2* o = scr + (long long)ql * kLRows * src + x;
   const float* col = plane_s + x * kLColPad;
@@ -152,10 +151,11 @@ __global__ void __launch_bounds__(128) r2c128_rows_kernel(const R2CParams p, int
   const int t = threadIdx.x & 63;
   float2* rows_s = buf + ul * kLRowBuf;
   if (u < kLRows)
-#pragma unroll 8
-    for (int i = t; i < jv * src; i += 64) {
-      const int jl = i / src, x = i - jl * src;
-      rows_s[jl * kLRowPad + x] = scr[((long long)(rl * p.J + j0 + jl) * kLRows + u) * src + x];
+    for (int jl = 0; jl < jv; ++jl) {
+      const float2* row = scr + ((long long)(rl * p.J + j0 + jl) * kLRows + u) * src;
+#pragma unroll
+      for (int x = t; x < kL; x += 64)
+        if (x < src) rows_s[jl * kLRowPad + x] = row[x];
     }
   __syncthreads();
   const int jl = t & 15, h = t >> 4;
@@ -276,10 +276,11 @@ __global__ void __launch_bounds__(128) c2r128_rows_kernel(const C2RParams p, int
   }
   __syncthreads();
   if (u < kLRows)
-#pragma unroll 8
-    for (int i = t; i < jv * crop; i += 64) {
-      const int l = i / crop, x = i - l * crop;
-      scr[((long long)(rl * p.J + j0 + l) * kLRows + u) * crop + x] = outb[l * kLRowPad + x];
+    for (int l = 0; l < jv; ++l) {
+      float2* row = scr + ((long long)(rl * p.J + j0 + l) * kLRows + u) * crop;
+#pragma unroll
+      for (int x = t; x < kL; x += 64)
+        if (x < crop) row[x] = outb[l * kLRowPad + x];
     }
 }
 
@@ -321,15 +322,14 @@ __global__ void __launch_bounds__(256, 2) c2r128_cols_kernel(const C2RParams p, 
   pdl_trigger();
   const int ql = blockIdx.x;
   const int r = r0 + ql / p.J, j = ql % p.J;
-  const int crop = p.crop, nz = kLRows * crop;
-  const float2* src = scr + (long long)ql * nz;
+  const int crop = p.crop;
+  const float2* src = scr + (long long)ql * kLRows * crop;
+  const int x = threadIdx.x & 127, g = threadIdx.x >> 7;
+  if (x < crop) {  // row u of the scratch plane: lanes = consecutive columns
 #pragma unroll 8
-  for (int i = threadIdx.x; i < nz; i += 256) {
-    const int u = i / crop, x = i - u * crop;
-    zs[x * kLRows + u] = src[i];
+    for (int u = g; u < kLRows; u += 2) zs[x * kLRows + u] = src[u * crop + x];
   }
   __syncthreads();
-  const int x = threadIdx.x & 127, g = threadIdx.x >> 7;
   if (x >= crop) return;
   float* o = p.out + (long long)r * p.out_sr + (long long)j * p.out_sj + x;
   const float2* col = zs + x * kLRows;
