@@ -512,7 +512,7 @@ def run_stack(args):
     for _ in range(args.warmup):
         layers.run_iteration(spec, params, batch, ws=ws)
     cats = {"update_output_ms": [], "update_grad_input_ms": [], "acc_grad_ms": []}
-    wall = []
+    wall, launches = [], []
     sampler = ClockSampler(0)
     sampler.start()
     for i in range(args.steps):
@@ -521,6 +521,7 @@ def run_stack(args):
         t0 = time.perf_counter()
         r = layers.run_iteration(spec, params, batch, ws=ws)
         wall.append((time.perf_counter() - t0) * 1e3)
+        launches.append(r.gpu_launches)
         for k in cats:
             cats[k].append(getattr(r.times, k))
     clocks = sampler.stop()
@@ -528,7 +529,7 @@ def run_stack(args):
     ms = sum(per.values())
     line = dict(base, value=ms, ms_per_step=ms, per_category_ms=per,
                 wall_ms_incl_param_upload=statistics.mean(wall), loss=r.loss, grad_checksum=r.grad_checksum,
-                clocks=clocks, gpu_launches=None,
+                clocks=clocks, gpu_launches=sum(launches),
                 note="value = device time of the three reference categories (CUDA events); conv stages on the "
                      "B200 kernels, relu/pool/fit_to on the layer-stack kernels, fc on fp32 cuBLAS")
     print(json.dumps(line), flush=True)

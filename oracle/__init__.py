@@ -258,6 +258,7 @@ def ref_lib():
     L.ref_resolve_threads.restype = C.c_uint
     L.ref_random_verify_configs.argtypes = [_sz, _u64, _p]
     L.ref_run_iteration_f32.argtypes = [_p, _sz, _sz, _u64, C.c_int, C.c_uint, _p, _sz, C.POINTER(_sz), _p]
+    L.ref_run_iteration_f64.argtypes = [_p, _sz, _sz, _u64, C.c_int, C.c_uint, _p, _sz, C.POINTER(_sz), _p]
     L.ref_cost_model.argtypes = [_sz, _sz, _sz, _sz, _sz, C.c_double, C.c_int, _p]
     return L
 
@@ -340,21 +341,21 @@ def ref_run_op_bench(k, n, f, fo, S, op, method, iters, warmup, threads, seed):
     return dict(zip(("mean_ms", "std_ms", "min_ms", "median_ms", "checksum"), (float(v) for v in out)))
 
 
-def ref_run_iteration(stages, S: int, seed: int, engine: int = 1, threads: int = 0):
-    """reference run_iteration<float> (layers.hpp:441-609) on its own
+def ref_run_iteration(stages, S: int, seed: int, engine: int = 1, threads: int = 0, dtype=np.float32):
+    """reference run_iteration<float|double> (layers.hpp:441-609) on its own
     init_params / make_batch.  stages: records (kind, k, n, f, f'|fc outputs),
     kind 0 conv, 1 relu, 2 pool, 3 fc.  Returns (flat grads, scalars dict)."""
     L = ref_lib()
+    fn = L.ref_run_iteration_f64 if np.dtype(dtype) == np.float64 else L.ref_run_iteration_f32
     rec = np.ascontiguousarray(np.asarray(stages, dtype=np.uint64).reshape(-1, 5))
     n = C.c_size_t(0)
     sc = np.zeros(6, dtype=np.float64)
     th = int(L.ref_resolve_threads(threads))
-    code = L.ref_run_iteration_f32(_ptr(rec), rec.shape[0], S, seed, engine, th, None, 0, C.byref(n), _ptr(sc))
+    code = fn(_ptr(rec), rec.shape[0], S, seed, engine, th, None, 0, C.byref(n), _ptr(sc))
     if code:
         raise OracleError(code, L.ref_last_error().decode())
-    g = np.zeros(n.value, dtype=np.float32)
-    code = L.ref_run_iteration_f32(_ptr(rec), rec.shape[0], S, seed, engine, th, _ptr(g), g.size, C.byref(n),
-                                   _ptr(sc))
+    g = np.zeros(n.value, dtype=np.dtype(dtype))
+    code = fn(_ptr(rec), rec.shape[0], S, seed, engine, th, _ptr(g), g.size, C.byref(n), _ptr(sc))
     if code:
         raise OracleError(code, L.ref_last_error().decode())
     keys = ("loss", "grad_checksum", "update_output_ms", "update_grad_input_ms", "acc_grad_ms",

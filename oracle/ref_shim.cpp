@@ -294,9 +294,11 @@ void ref_random_verify_configs(size_t count, uint64_t seed, uint64_t* out) {
 // available; the length needed goes to *grads_len).  scalars: loss,
 // grad_checksum, update_output_ms, update_grad_input_ms, acc_grad_ms,
 // grad_input_calls.
-int ref_run_iteration_f32(const uint64_t* stages, size_t nstages, size_t S, uint64_t seed,
-                          int engine, unsigned threads, float* out_grads, size_t grads_cap,
-                          size_t* grads_len, double* scalars) {
+extern "C++" {
+template <typename T>
+static int ref_run_iteration_t(const uint64_t* stages, size_t nstages, size_t S, uint64_t seed, int engine,
+                               unsigned threads, T* out_grads, size_t grads_cap, size_t* grads_len,
+                               double* scalars) {
   return guarded([&] {
     fftconv::NetworkSpec net;
     for (size_t i = 0; i < nstages; ++i) {
@@ -312,9 +314,9 @@ int ref_run_iteration_f32(const uint64_t* stages, size_t nstages, size_t S, uint
       net.input_image = net.stages.front().conv.image;
     }
     net.validate();
-    auto params = fftconv::init_params<float>(net, seed);
-    auto batch = fftconv::make_batch<float>(net, S, seed);
-    auto r = fftconv::run_iteration<float>(
+    auto params = fftconv::init_params<T>(net, seed);
+    auto batch = fftconv::make_batch<T>(net, S, seed);
+    auto r = fftconv::run_iteration<T>(
         net, params, batch, engine ? fftconv::Engine::fft : fftconv::Engine::direct, nullptr, threads);
     size_t n = 0;
     for (const auto& g : r.conv_weight_grads) n += g.size();
@@ -323,12 +325,12 @@ int ref_run_iteration_f32(const uint64_t* stages, size_t nstages, size_t S, uint
     if (out_grads && grads_cap >= n) {
       size_t o = 0;
       for (const auto& g : r.conv_weight_grads) {
-        std::memcpy(out_grads + o, g.data().data(), g.size() * sizeof(float));
+        std::memcpy(out_grads + o, g.data().data(), g.size() * sizeof(T));
         o += g.size();
       }
-      std::memcpy(out_grads + o, r.fc_weight_grad.data(), r.fc_weight_grad.size() * sizeof(float));
+      std::memcpy(out_grads + o, r.fc_weight_grad.data(), r.fc_weight_grad.size() * sizeof(T));
       o += r.fc_weight_grad.size();
-      std::memcpy(out_grads + o, r.fc_bias_grad.data(), r.fc_bias_grad.size() * sizeof(float));
+      std::memcpy(out_grads + o, r.fc_bias_grad.data(), r.fc_bias_grad.size() * sizeof(T));
     }
     scalars[0] = r.loss;
     scalars[1] = r.grad_checksum;
@@ -337,6 +339,23 @@ int ref_run_iteration_f32(const uint64_t* stages, size_t nstages, size_t S, uint
     scalars[4] = r.times.acc_grad_ms;
     scalars[5] = (double)r.grad_input_calls;
   });
+}
+}  // extern "C++"
+
+int ref_run_iteration_f32(const uint64_t* stages, size_t nstages, size_t S, uint64_t seed,
+                          int engine, unsigned threads, float* out_grads, size_t grads_cap,
+                          size_t* grads_len, double* scalars) {
+  return ref_run_iteration_t<float>(stages, nstages, S, seed, engine, threads, out_grads, grads_cap, grads_len,
+                                    scalars);
+}
+
+// The same iteration in double (run_iteration<double>): the precision
+// reference for deep stacks, where two fp32 implementations drift apart.
+int ref_run_iteration_f64(const uint64_t* stages, size_t nstages, size_t S, uint64_t seed,
+                          int engine, unsigned threads, double* out_grads, size_t grads_cap,
+                          size_t* grads_len, double* scalars) {
+  return ref_run_iteration_t<double>(stages, nstages, S, seed, engine, threads, out_grads, grads_cap, grads_len,
+                                     scalars);
 }
 
 // cost_model.hpp:39-110: op 0/1/2 -> {direct, transform, pointwise, inverse}

@@ -230,9 +230,38 @@ class IterationResult:  # layers.hpp:426-437
     fc_bias_grad: object = None
     grad_input_calls: int = 0
     grad_checksum: float = 0.0
+    gpu_launches: int = 0           # our kernels (conv operators + layer stages; fc is cuBLAS)
 
 
 # ---------------------------------------------------------------- device stages
+_LAUNCHES = [0]  # our kernel launches since the last reset (run_iteration reports them)
+
+
+def _launched(n: int = 1) -> None:
+    _LAUNCHES[0] += n
+
+
+class _CountingWorkspace:
+    """Forwards the three operators and adds each call's launch count."""
+
+    def __init__(self, ws):
+        self.ws = ws
+
+    def _run(self, fn, *a):
+        r = fn(*a)
+        _launched(self.ws.last_launch_count())
+        return r
+
+    def forward(self, x, w):
+        return self._run(self.ws.forward, x, w)
+
+    def grad_input(self, gy, w):
+        return self._run(self.ws.grad_input, gy, w)
+
+    def grad_weight(self, gy, x):
+        return self._run(self.ws.grad_weight, gy, x)
+
+
 def _stream_ptr(torch):
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
@@ -252,6 +281,7 @@ def fit_to(t, size: int):
     out = torch.empty((S, M, size, size), dtype=torch.float32, device=t.device)
     raise_for_status(_native.lib().fftconv_b200_fit_to(_ptr(t), S * M, R, Cc, _ptr(out), size,
                                                         _stream_ptr(torch)), _native.last_error(None))
+    _launched()
     return out
 
 
@@ -261,6 +291,7 @@ def relu_forward(x):
     y = torch.empty_like(x)
     raise_for_status(_native.lib().fftconv_b200_relu_forward(_ptr(x), _ptr(y), x.numel(), _stream_ptr(torch)),
                      _native.last_error(None))
+    _launched()
     return y
 
 
@@ -272,6 +303,7 @@ def relu_backward(gy, x):
     gx = torch.empty_like(x)
     raise_for_status(_native.lib().fftconv_b200_relu_backward(_ptr(gy), _ptr(x), _ptr(gx), x.numel(),
                                                                _stream_ptr(torch)), _native.last_error(None))
+    _launched()
     return gx
 
 
@@ -284,6 +316,7 @@ def maxpool_forward(x):
     arg = torch.empty((S, M, R // 2, Cc // 2), dtype=torch.int32, device=x.device)
     raise_for_status(_native.lib().fftconv_b200_maxpool_forward(_ptr(x), S * M, R, Cc, _ptr(y), _ptr(arg),
                                                                  _stream_ptr(torch)), _native.last_error(None))
+    _launched()
     return y, arg, (S, M, R, Cc)
 
 
@@ -297,6 +330,7 @@ def maxpool_backward(gy, rec):
     gx = torch.empty(shape, dtype=torch.float32, device=gy.device)
     raise_for_status(_native.lib().fftconv_b200_maxpool_backward(_ptr(gy), _ptr(arg), S * M, R, Cc, _ptr(gx),
                                                                   _stream_ptr(torch)), _native.last_error(None))
+    _launched()
     return gx
 
 
@@ -318,6 +352,8 @@ def run_iteration(spec: NetworkSpec, params: NetworkParams, batch, ws: ConvWorks
     S = x.shape[0]
     if ws is None:
         ws = ConvWorkspace(spec.conv_configs(S), device=device)
+    ws = _CountingWorkspace(ws)
+    _LAUNCHES[0] = 0
     w_dev = [torch.from_numpy(np.ascontiguousarray(w)).to(dev) for w in params.conv]
     if sh.has_fc:
         fc_w = torch.from_numpy(np.ascontiguousarray(params.fc_weights)).to(dev)
@@ -404,6 +440,7 @@ def run_iteration(spec: NetworkSpec, params: NetworkParams, batch, ws: ConvWorks
         checksum = sum(float(g.double().sum()) for g in conv_grads)
         if sh.has_fc:
             checksum += float(fc_gw.double().sum()) + float(fc_gb.double().sum())
-        return IterationResult(times, float(loss_t), conv_grads, fc_gw, fc_gb, grad_input_calls, checksum)
+        return IterationResult(times, float(loss_t), conv_grads, fc_gw, fc_gb, grad_input_calls, checksum,
+                               _LAUNCHES[0])
     finally:
         torch.backends.cuda.matmul.allow_tf32 = prev_tf32

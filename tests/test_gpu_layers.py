@@ -88,6 +88,8 @@ def test_run_iteration_matches_reference(dev):
     res = layers.run_iteration(spec, params, batch)
     ref_flat, ref = oracle.ref_run_iteration(spec.records(), S, seed, engine=1)
     assert res.grad_input_calls == int(ref["grad_input_calls"]) == 4
+    # 5 fprop + 5 accGrad + 4 bprop operator calls (>= 3 launches each) + the layer stages
+    assert res.gpu_launches >= 3 * (5 + 5 + 4)
     assert abs(res.loss - ref["loss"]) <= 1e-5 * abs(ref["loss"])
     off = 0
     for g in res.conv_weight_grads:
@@ -100,3 +102,28 @@ def test_run_iteration_matches_reference(dev):
     assert _rel(res.fc_bias_grad.cpu().numpy(), ref_flat[off:]) <= 1e-6
     assert abs(res.grad_checksum - ref["grad_checksum"]) <= 1e-4 * abs(ref["grad_checksum"])
     assert res.times.total_ms() > 0
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="reference library not built")
+def test_alexnet128_iteration_matches_reference(dev):
+    """BASELINE configs[4]'s stack (first layer n = 128: FFT size 128) at a
+    small batch.  Five conv layers of fp32 backprop drift: the reference's
+    own run_iteration<float> is 1.7e-3 from run_iteration<double> at layer 1
+    (measured), so the bar is "no further from the fp64 reference than the
+    reference's fp32 path", per layer."""
+    spec = layers.preset_network("alexnet-128")
+    seed, S = 77, 1
+    params = layers.init_params(spec, seed)
+    batch = layers.make_batch(spec, S, seed)
+    res = layers.run_iteration(spec, params, batch)
+    g32, r32 = oracle.ref_run_iteration(spec.records(), S, seed, engine=1)
+    g64, r64 = oracle.ref_run_iteration(spec.records(), S, seed, engine=1, dtype=np.float64)
+    assert res.grad_input_calls == int(r64["grad_input_calls"]) == 4
+    assert abs(res.loss - r64["loss"]) <= 1e-4 * abs(r64["loss"])
+    off = 0
+    for g in res.conv_weight_grads:
+        n = g.numel()
+        ours = _rel(g.cpu().numpy().reshape(-1), g64[off:off + n])
+        ref = _rel(g32[off:off + n], g64[off:off + n])
+        assert ours <= max(ref, 1e-4), (ours, ref)
+        off += n
