@@ -351,14 +351,17 @@ def main():
                 ach = alg[op][i] / (t_ms * 1e-3) / 1e9
                 stages.append({"op": op, "kernel": kname[i], "ms": t_ms, "bound": "hbm", "achieved": ach,
                                "peak": hbm_gbs, "unit": "GB/s", "frac": ach / hbm_gbs, "alg_bytes": alg[op][i]})
-    # dominant kernel = largest total time across the step
+    # dominant kernel = largest total time across the step (the m = 128
+    # transforms are two kernels each, fft_large.cuh)
+    m_fft = 1 << max(0, (n - 1).bit_length())
+    xf_names = ({"r2c": "r2c128_cols_kernel+r2c128_rows_kernel", "c2r": "c2r128_rows_kernel+c2r128_cols_kernel"}
+                if m_fft == 128 else {"r2c": "r2c_tma_kernel", "c2r": "c2r_tma_kernel"})
     tot = {}
     for s_ in stages:
-        key = {"r2c": "r2c_tma_kernel", "c2r": "c2r_tma_kernel"}.get(s_["kernel"][:3], s_["kernel"])
+        key = xf_names.get(s_["kernel"][:3], s_["kernel"])
         tot[key] = tot.get(key, 0.0) + s_["ms"]
     dom = max(tot, key=tot.get)
-    dom_st = [s_ for s_ in stages if {"r2c": "r2c_tma_kernel", "c2r": "c2r_tma_kernel"}.get(
-        s_["kernel"][:3], s_["kernel"]) == dom]
+    dom_st = [s_ for s_ in stages if xf_names.get(s_["kernel"][:3], s_["kernel"]) == dom]
     dom_ms = statistics.mean(s_["ms"] for s_ in dom_st)
     if dom == "cgemm_bins_tcgen05" and dom_st[0]["bound"] == "tensor":
         alg_per_launch = statistics.mean(s_["alg_flops"] for s_ in dom_st)

@@ -163,9 +163,10 @@ int fftconv_b200_fit_to(const float* x, size_t planes, size_t rows, size_t cols,
 
 /* Forward 2-D real transforms of `planes` square src x src planes
  * (zero-padded to m x m, m = next_pow2 >= src) into the half spectrum
- * out[p][u][v] (u in [0, m/2], v in [0, m)), complex interleaved.  This is
- * the transpose of the reference HalfSpectrum packing (fft.hpp:105-152):
- * reference packed_bin(u, v) for v <= m/2 equals out[v][u] here. */
+ * out[p][u][v] = F[u][v] (u in [0, m/2], v in [0, m)), complex interleaved.
+ * The reference HalfSpectrum (fft.hpp:105-152) keeps the other half,
+ * F[u][v] for v <= m/2; the two are related by F[u][v] =
+ * conj(F[(m-u)%m][(m-v)%m]) (paper_1312_5851_b200/spectra.py repacks). */
 int fftconv_b200_debug_r2c(const float* in, size_t planes, size_t src, size_t m, float* out,
                            void* stream);
 /* Inverse of the above with top-left crop x crop, scaled by 1/m^2. */
