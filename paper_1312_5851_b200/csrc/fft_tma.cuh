@@ -150,14 +150,13 @@ __device__ __forceinline__ GroupRef r2c_group(const R2CPair& P, int ngA, int g) 
   return {&p, which, r, (gl - r * ngj) * G};
 }
 
-// max(|Re|, |Im|) over N complex values as float bits (non-negative floats
-// order like their bit patterns; NaN bits exceed every finite value).
+// max(|Re|, |Im|) over N complex values (FMNMX with |.| operands; NaNs are
+// skipped, they still propagate through the GEMM itself).
 template <int N>
-__device__ __forceinline__ uint32_t absmax_bits(const float2 (&v)[N]) {
-  uint32_t m = 0;
+__device__ __forceinline__ float absmax_f(const float2 (&v)[N]) {
+  float m = 0.f;
 #pragma unroll
-  for (int i = 0; i < N; ++i)
-    m = max(m, max(__float_as_uint(v[i].x) & 0x7fffffffu, __float_as_uint(v[i].y) & 0x7fffffffu));
+  for (int i = 0; i < N; ++i) m = fmaxf(m, fmaxf(fabsf(v[i].x), fabsf(v[i].y)));
   return m;
 }
 
@@ -354,7 +353,7 @@ __global__ void __launch_bounds__(TR2C<M>::THREADS, 1)
     const int t = threadIdx.x - 32 - T::NPIPE * T::P1W - pipe * T::P2W;
     const int bar = 1 + T::NPIPE + pipe;
     const bool act = t < T::P2;
-    uint32_t amx[2] = {0u, 0u};  // running max |component| (float bits) per operand
+    float amx[2] = {0.f, 0.f};  // running max |component| per operand
 #pragma unroll 1
     for (int i = pipe;; i += T::NPIPE) {
       const int g = blockIdx.x + i * gridDim.x;
@@ -383,7 +382,7 @@ __global__ void __launch_bounds__(TR2C<M>::THREADS, 1)
           if (act) {  // invalid (K padding) planes store exact zeros
             if (FCB_XFORM_EXP != 1) fft_reg_nz<M, NZ, false>(w);
             tile_row<M>(tile + (u * M) * G + jl, G, w, csign);
-            amx[q.which] = max(amx[q.which], absmax_bits<M>(w));
+            amx[q.which] = fmaxf(amx[q.which], absmax_f<M>(w));
           }
         };
         using FT = std::true_type;
@@ -410,7 +409,7 @@ __global__ void __launch_bounds__(TR2C<M>::THREADS, 1)
         if (act) {
           if (FCB_XFORM_EXP != 1) fft_reg<32, false>(z);
           tile_row<32>(tile + (u * M + h) * G + jl, 2 * G, z, csign);
-          amx[q.which] = max(amx[q.which], absmax_bits<32>(z));
+          amx[q.which] = fmaxf(amx[q.which], absmax_f<32>(z));
         }
       }
       fence_proxy_async_smem();  // the tile is read by the TMA store (async proxy)
@@ -419,7 +418,8 @@ __global__ void __launch_bounds__(TR2C<M>::THREADS, 1)
     }
 #pragma unroll
     for (int w = 0; w < 2; ++w) {
-      const uint32_t v = __reduce_max_sync(0xffffffffu, amx[w]);
+      // non-negative floats order like their bit patterns
+      const uint32_t v = __reduce_max_sync(0xffffffffu, __float_as_uint(amx[w]));
       if ((threadIdx.x & 31) == 0 && w < P.n && P.op[w].amax)
         atomicMax(P.op[w].amax, ((unsigned long long)P.op[w].epoch << 32) | v);
     }
