@@ -67,13 +67,18 @@ void fftconv_b200_ws_destroy(fftconv_b200_ws* ws);
 const char* fftconv_b200_last_error(const fftconv_b200_ws* ws);
 
 /* Precision scheme of the per-bin complex GEMM (K3), process-wide.  Both
- * keep fp32-level accuracy (rel. L2 ~1e-6 against the fp64 oracle):
- *   FFTCONV_B200_GEMM_F16X3  (default) operands scaled by a power of two
- *       from their max magnitude (found by K1) and split into fp16
- *       hi + mid; D = hi.hi + hi.mid + mid.hi on kind::f16 tensor cores;
- *   FFTCONV_B200_GEMM_TF32X3 x = tf32 hi + lo, D = hi.hi + hi.lo + lo.hi
- *       on kind::tf32 (half the fp16 rate; also used at FFT sizes m < 4).
- * The environment variable FFTCONV_B200_GEMM=tf32 selects the latter at
+ * keep fp32-level accuracy on the reference's workloads (rel. L2 ~1e-6
+ * against the fp64 oracle):
+ *   FFTCONV_B200_GEMM_TF32X3 (default) x = tf32 hi + lo, D = hi.hi + hi.lo
+ *       + lo.hi on kind::tf32 -- per-element exponents, the fp32 range;
+ *   FFTCONV_B200_GEMM_F16X3 each operand scaled by one power of two from
+ *       its max magnitude (found by K1) and split into fp16 hi + mid;
+ *       D = hi.hi + hi.mid + mid.hi on kind::f16 (twice the tf32 rate).
+ *       Components below ~2^-24 of their operand's maximum lose relative
+ *       precision (absolute error ~2^-38 of the maximum), so operands whose
+ *       rows span more than ~1e6 in magnitude should stay on 3xTF32.
+ *       m < 4 always uses 3xTF32.
+ * The environment variable FFTCONV_B200_GEMM=f16x3 selects the latter at
  * load time.  Returns the previous kind, or -1 for an unknown kind. */
 #define FFTCONV_B200_GEMM_F16X3 0
 #define FFTCONV_B200_GEMM_TF32X3 1

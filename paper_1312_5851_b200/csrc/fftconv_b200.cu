@@ -388,12 +388,14 @@ static GemmGeom gemm_geom(size_t M, size_t N, const DevInfo& di, bool f16) {
 // D[t] = A[t] . conj(B[t])^T per bin; im_sign = -1 returns conj(D) (the
 // accGrad orientation, conj(A) . B).  A: F[t][M][2*kpad], B: F[t][N][2*kpad].
 
-// GEMM operand precision: fp16x3 (default) or 3xTF32 (FFTCONV_B200_GEMM=tf32,
-// fftconv_b200_set_gemm_kind); fp16x3 needs the operands' max-magnitude words
-// (amax_a / amax_b from K1), so callers without them get 3xTF32.
+// GEMM operand precision: 3xTF32 (default, per-element fp32 range) or
+// fp16x3 (FFTCONV_B200_GEMM=f16x3, fftconv_b200_set_gemm_kind: faster where
+// the GEMM is tensor-bound, per-operand scaling); fp16x3 needs the operands'
+// max-magnitude words (amax_a / amax_b from K1), so callers without them get
+// 3xTF32.
 static int g_gemm_kind = [] {
   const char* e = getenv("FFTCONV_B200_GEMM");
-  return (e && std::string(e) == "tf32") ? FFTCONV_B200_GEMM_TF32X3 : FFTCONV_B200_GEMM_F16X3;
+  return (e && std::string(e) == "f16x3") ? FFTCONV_B200_GEMM_F16X3 : FFTCONV_B200_GEMM_TF32X3;
 }();
 
 static void launch_gemm(const float* A, const float* B, float* out, size_t bins, size_t M,
