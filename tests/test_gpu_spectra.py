@@ -61,3 +61,30 @@ def test_size_errors(dev):
         ifft_2d_real_batch(HalfSpectrum.zeros(1, 1, 8), m=16)
     with pytest.raises(SizeError):
         HalfSpectrum.zeros(0, 1, 8)
+
+
+def test_parseval_and_packed_columns(dev):
+    """fft_test.cpp:201-227: energy is preserved (sum |x|^2 = sum |X|^2 / m^2
+    over the full spectrum, unpacked columns counted twice) and the packing
+    keeps m/2 + 1 columns."""
+    m = 32
+    t = oracle.fill_uniform((2, 2, m, m), 11, 1)
+    s = fft_2d_real_batch(t)
+    assert s.packed_cols() == m // 2 + 1 and s.rows() == m and s.plane_size() == m * (m // 2 + 1)
+    X = s.data.cpu().numpy().astype(np.complex128)
+    w = np.full(m // 2 + 1, 2.0)
+    w[0] = w[-1] = 1.0  # DC and Nyquist columns are their own mirrors
+    energy = (np.abs(X) ** 2 * w).sum(axis=(2, 3)) / (m * m)
+    ref = (t.astype(np.float64) ** 2).sum(axis=(2, 3))
+    assert np.allclose(energy, ref, rtol=2e-6)
+
+
+def test_linearity(dev):
+    """fft_test.cpp:100-113: F(a x + b y) = a F(x) + b F(y)."""
+    m = 16
+    x = oracle.fill_uniform((1, 3, m, m), 21, 1)
+    y = oracle.fill_uniform((1, 3, m, m), 22, 1)
+    a, b = np.float32(0.75), np.float32(-2.5)
+    lhs = fft_2d_real_batch(a * x + b * y).data.cpu().numpy()
+    rhs = a * fft_2d_real_batch(x).data.cpu().numpy() + b * fft_2d_real_batch(y).data.cpu().numpy()
+    assert np.linalg.norm(lhs - rhs) <= 1e-5 * np.linalg.norm(rhs)
