@@ -66,23 +66,30 @@ void fftconv_b200_ws_destroy(fftconv_b200_ws* ws);
  * workspace (when non-NULL). */
 const char* fftconv_b200_last_error(const fftconv_b200_ws* ws);
 
-/* Precision scheme of the per-bin complex GEMM (K3), process-wide.  Both
- * keep fp32-level accuracy on the reference's workloads (rel. L2 ~1e-6
- * against the fp64 oracle):
- *   FFTCONV_B200_GEMM_TF32X3 (default) x = tf32 hi + lo, D = hi.hi + hi.lo
- *       + lo.hi on kind::tf32 -- per-element exponents, the fp32 range;
+/* Precision scheme of the per-bin complex GEMM (K3), process-wide.  All
+ * keep fp32-level accuracy (rel. L2 ~1e-6 against the fp64 oracle):
+ *   FFTCONV_B200_GEMM_TF32X3 x = tf32 hi + lo, D = hi.hi + hi.lo + lo.hi
+ *       on kind::tf32 -- per-element exponents, the fp32 range;
  *   FFTCONV_B200_GEMM_F16X3 each operand scaled by one power of two from
  *       its max magnitude (found by K1) and split into fp16 hi + mid;
  *       D = hi.hi + hi.mid + mid.hi on kind::f16 (twice the tf32 rate).
  *       Components below ~2^-24 of their operand's maximum lose relative
- *       precision (absolute error ~2^-38 of the maximum), so operands whose
- *       rows span more than ~1e6 in magnitude should stay on 3xTF32.
- *       m < 4 always uses 3xTF32.
- * The environment variable FFTCONV_B200_GEMM=f16x3 selects the latter at
- * load time.  Returns the previous kind, or -1 for an unknown kind. */
+ *       precision (absolute error ~2^-38 of the maximum);
+ *   FFTCONV_B200_GEMM_AUTO (default) 3xTF32 where the GEMM is bound by its
+ *       bytes anyway; where it is tensor-bound, an fp16x3 kernel and a
+ *       3xTF32 fallback are launched back to back and exactly one runs:
+ *       fp16x3 iff every operand row's maximum is within 2^18 of its
+ *       operand's maximum (K1 records the per-row maxima).
+ * m < 4 always uses 3xTF32.  The environment variable FFTCONV_B200_GEMM
+ * = tf32 | f16x3 | auto selects the initial kind.  Returns the previous
+ * kind, or -1 for an unknown kind. */
 #define FFTCONV_B200_GEMM_F16X3 0
 #define FFTCONV_B200_GEMM_TF32X3 1
+#define FFTCONV_B200_GEMM_AUTO 2
 int fftconv_b200_set_gemm_kind(int kind);
+/* Which GEMM kernel ran in the workspace's last operator call (synchronises
+ * the device): 1 fp16x3, 0 3xTF32, -1 none yet / error. */
+int fftconv_b200_last_gemm_path(fftconv_b200_ws* ws);
 
 /* ConvWorkspace::max_fft_size/capacity_x/capacity_w/capacity_y/
  * frequency_bytes  conv_fft.hpp:60-69.

@@ -41,6 +41,7 @@ SIGNATURES = [
     ("fftconv_b200_maxpool_backward", _i, [_p, _p, _sz, _sz, _sz, _p, _p]),
     ("fftconv_b200_fit_to", _i, [_p, _sz, _sz, _sz, _p, _sz, _p]),
     ("fftconv_b200_set_gemm_kind", _i, [_i]),
+    ("fftconv_b200_last_gemm_path", _i, [_p]),
     ("fftconv_b200_debug_r2c", _i, [_p, _sz, _sz, _sz, _p, _p]),
     ("fftconv_b200_debug_c2r", _i, [_p, _sz, _sz, _sz, _p, _p]),
     ("fftconv_b200_debug_cgemm", _i, [_p, _p, _p, _sz, _sz, _sz, _sz, _i, _p]),
@@ -76,7 +77,7 @@ def last_error(ws=None) -> str:
     return msg.decode() if msg else ""
 
 
-GEMM_KINDS = {"f16x3": 0, "tf32x3": 1}
+GEMM_KINDS = {"f16x3": 0, "tf32x3": 1, "auto": 2}
 
 
 def gemm_kind() -> str:

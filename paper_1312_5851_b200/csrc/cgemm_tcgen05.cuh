@@ -68,11 +68,21 @@ struct GemmParams {
   float im_sign;  // +1 (fprop, bprop) or -1 (accGrad)
   long long s_t, s_mg, s_n;  // output strides in complex elements
   int gm_log2;                // log2 of the m-group size gm
-  // fp16x3 mode: the operands' max |component| words written by K1
-  // (R2CParams::amax; low 32 bits = float bits)
+  // per operand row, the max-magnitude words written by K1 (R2CParams::amax;
+  // low 32 bits = float bits): the fp16x3 scale and the auto selection
   const unsigned long long* amax_a;
   const unsigned long long* amax_b;
+  int rows_a, rows_b;
+  // 0: run; 1: run only if every operand row is within kF16SafeBinades of
+  // its operand's maximum (fp16x3 is exact enough); 2: run only if not
+  // (the 3xTF32 fallback of the same launch pair)
+  int select;
+  int* path;  // optional: the kernel that runs writes 1 (fp16x3) or 0 (3xTF32)
 };
+
+// fp16x3 keeps ~2^-20 row-relative accuracy for rows within 2^18 of the
+// operand maximum (global power-of-two scale, fp16 subnormal floor 2^-38).
+constexpr int kF16SafeBinades = 18;
 
 constexpr int kGemmThreads = 640;
 constexpr int kTileM = 128;
@@ -212,10 +222,46 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   // pipeline steps per tile: K chunks (tf32) or chunk pairs (fp16)
   const int kc_n = F16 ? (p.k_chunks + 1) >> 1 : p.k_chunks;
   int ea = 14, eb = 14;  // fp16 operand scale exponents
-  if constexpr (F16) {
-    ea = amax_exp(p.amax_a[0]);
-    eb = amax_exp(p.amax_b[0]);
+  if (F16 || p.select != 0) {
+    // operand maxima and smallest non-zero row maxima (float bits order as
+    // the values): the fp16 scales and the fp16x3 / 3xTF32 choice
+    uint32_t* dec = tmem_slot + 4;  // max A, min A, max B, min B (inside the 256-B barrier tail)
+    if (threadIdx.x < 4) dec[threadIdx.x] = (threadIdx.x & 1) ? 0xffffffffu : 0u;
+    __syncthreads();
+    uint32_t v[4] = {0u, 0xffffffffu, 0u, 0xffffffffu};
+    for (int r = threadIdx.x; r < p.rows_a; r += blockDim.x) {
+      const uint32_t b = (uint32_t)p.amax_a[r];
+      if (b) { v[0] = max(v[0], b); v[1] = min(v[1], b); }
+    }
+    for (int r = threadIdx.x; r < p.rows_b; r += blockDim.x) {
+      const uint32_t b = (uint32_t)p.amax_b[r];
+      if (b) { v[2] = max(v[2], b); v[3] = min(v[3], b); }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t w = (i & 1) ? __reduce_min_sync(0xffffffffu, v[i]) : __reduce_max_sync(0xffffffffu, v[i]);
+      if (lane == 0) {
+        if (i & 1) atomicMin(&dec[i], w);
+        else atomicMax(&dec[i], w);
+      }
+    }
+    __syncthreads();
+    ea = amax_exp(dec[0]);
+    eb = amax_exp(dec[2]);
+    auto spread = [](uint32_t mx, uint32_t mn) {  // binades between max and min row maxima
+      return mn == 0xffffffffu ? 0 : (int)((mx >> 23) & 0xffu) - (int)((mn >> 23) & 0xffu);
+    };
+    const bool safe = spread(dec[0], dec[1]) <= kF16SafeBinades && spread(dec[2], dec[3]) <= kF16SafeBinades;
+    if (p.select != 0 && (p.select == 1) != safe) {  // the other kernel of the pair runs
+      __syncthreads();
+      if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, kTmemCols);
+      }
+      return;
+    }
   }
+  if (p.path && blockIdx.x == 0 && threadIdx.x == 0) *p.path = F16 ? 1 : 0;
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer

@@ -194,9 +194,9 @@ __global__ void __launch_bounds__(128) r2c128_rows_kernel(const R2CParams p, int
           *reinterpret_cast<const float4*>(tile + v * 16 + 2 * part);
     }
   }
-  if (p.amax) {
+  if (p.amax) {  // row r's maximum
     amx = __reduce_max_sync(0xffffffffu, amx);
-    if ((threadIdx.x & 31) == 0) atomicMax(p.amax, ((unsigned long long)p.epoch << 32) | amx);
+    if ((threadIdx.x & 31) == 0) atomicMax(p.amax + r, ((unsigned long long)p.epoch << 32) | amx);
   }
 }
 

@@ -288,9 +288,10 @@ struct R2CParams {
   int src;   // source plane edge (square, src <= M): zero-padded implicitly
   int cpad;  // odd smem column stride >= src
   int conj;  // 1: store the conjugate spectrum
-  // max |Re|, |Im| over the spectrum for the fp16 GEMM's operand scaling
-  // (TMA kernels only): atomicMax of (epoch << 32 | float bits), so a newer
-  // epoch's maximum supersedes the stale value without a reset.
+  // per operand row r: max |Re|, |Im| over the row's spectra (all K, all
+  // bins) for the fp16 GEMM (TMA / m = 128 kernels only): amax[r] =
+  // atomicMax of (epoch << 32 | float bits), so a newer epoch's maximum
+  // supersedes the stale value without a reset.
   unsigned long long* amax = nullptr;
   unsigned epoch = 0;
 };

@@ -353,7 +353,6 @@ __global__ void __launch_bounds__(TR2C<M>::THREADS, 1)
     const int t = threadIdx.x - 32 - T::NPIPE * T::P1W - pipe * T::P2W;
     const int bar = 1 + T::NPIPE + pipe;
     const bool act = t < T::P2;
-    float amx[2] = {0.f, 0.f};  // running max |component| per operand
 #pragma unroll 1
     for (int i = pipe;; i += T::NPIPE) {
       const int g = blockIdx.x + i * gridDim.x;
@@ -364,6 +363,7 @@ __global__ void __launch_bounds__(TR2C<M>::THREADS, 1)
       const int src = p.src;
       const int jv = max(0, min(G, p.J - q.j0));
       const float csign = p.conj ? -1.f : 1.f;
+      float amx = 0.f;  // max |component| of this thread's outputs (the group's row)
       uint8_t* st = smem + s * T::STAGE;
       float2* tile = reinterpret_cast<float2*>(st);  // [bin][G planes]
       mbar_wait(&mid[s], (i / S) & 1);
@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(TR2C<M>::THREADS, 1)
           if (act) {  // invalid (K padding) planes store exact zeros
             if (FCB_XFORM_EXP != 1) fft_reg_nz<M, NZ, false>(w);
             tile_row<M>(tile + (u * M) * G + jl, G, w, csign);
-            amx[q.which] = fmaxf(amx[q.which], absmax_f<M>(w));
+            amx = fmaxf(amx, absmax_f<M>(w));
           }
         };
         using FT = std::true_type;
@@ -409,19 +409,16 @@ __global__ void __launch_bounds__(TR2C<M>::THREADS, 1)
         if (act) {
           if (FCB_XFORM_EXP != 1) fft_reg<32, false>(z);
           tile_row<32>(tile + (u * M + h) * G + jl, 2 * G, z, csign);
-          amx[q.which] = fmaxf(amx[q.which], absmax_f<32>(z));
+          amx = fmaxf(amx, absmax_f<32>(z));
         }
       }
       fence_proxy_async_smem();  // the tile is read by the TMA store (async proxy)
       mbar_arrive(&outb[s]);
       if (t == 0) XTRACE(3, i);
-    }
-#pragma unroll
-    for (int w = 0; w < 2; ++w) {
-      // non-negative floats order like their bit patterns
-      const uint32_t v = __reduce_max_sync(0xffffffffu, __float_as_uint(amx[w]));
-      if ((threadIdx.x & 31) == 0 && w < P.n && P.op[w].amax)
-        atomicMax(P.op[w].amax, ((unsigned long long)P.op[w].epoch << 32) | v);
+      if (p.amax) {  // row maximum; non-negative floats order like their bit patterns
+        const uint32_t v = __reduce_max_sync(0xffffffffu, __float_as_uint(amx));
+        if ((threadIdx.x & 31) == 0) atomicMax(p.amax + q.r, ((unsigned long long)p.epoch << 32) | v);
+      }
     }
   }
 #ifdef FCB_XFORM_TRACE

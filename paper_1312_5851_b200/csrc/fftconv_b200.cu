@@ -388,21 +388,62 @@ static GemmGeom gemm_geom(size_t M, size_t N, const DevInfo& di, bool f16) {
 // D[t] = A[t] . conj(B[t])^T per bin; im_sign = -1 returns conj(D) (the
 // accGrad orientation, conj(A) . B).  A: F[t][M][2*kpad], B: F[t][N][2*kpad].
 
-// GEMM operand precision: 3xTF32 (default, per-element fp32 range) or
-// fp16x3 (FFTCONV_B200_GEMM=f16x3, fftconv_b200_set_gemm_kind: faster where
-// the GEMM is tensor-bound, per-operand scaling); fp16x3 needs the operands'
-// max-magnitude words (amax_a / amax_b from K1), so callers without them get
-// 3xTF32.
+// GEMM operand precision (fftconv_b200_set_gemm_kind, FFTCONV_B200_GEMM =
+// tf32 | f16x3 | auto):
+//   3xTF32  per-element fp32 range;
+//   fp16x3  one power-of-two scale per operand, twice the tensor rate;
+//   auto    (default) 3xTF32 where the GEMM's byte floor exceeds its 3xTF32
+//           tensor floor (fp16x3 would not be faster), else the fp16x3 kernel
+//           and a 3xTF32 fallback launched back to back: each reads K1's
+//           per-row maxima and exactly one of them runs -- fp16x3 when every
+//           operand row is within 2^18 of its operand's maximum.
 static int g_gemm_kind = [] {
   const char* e = getenv("FFTCONV_B200_GEMM");
-  return (e && std::string(e) == "f16x3") ? FFTCONV_B200_GEMM_F16X3 : FFTCONV_B200_GEMM_TF32X3;
+  if (e && std::string(e) == "tf32") return FFTCONV_B200_GEMM_TF32X3;
+  if (e && std::string(e) == "f16x3") return FFTCONV_B200_GEMM_F16X3;
+  return FFTCONV_B200_GEMM_AUTO;
 }();
 
-static void launch_gemm(const float* A, const float* B, float* out, size_t bins, size_t M,
-                        size_t N, size_t kpad, float im_sign, OutLayout lay, size_t ldm,
-                        const DevInfo& di, cudaStream_t st, const unsigned long long* amax_a = nullptr,
-                        const unsigned long long* amax_b = nullptr) {
-  const bool f16 = amax_a && amax_b && g_gemm_kind == FFTCONV_B200_GEMM_F16X3;
+enum GemmRoute { kRouteTf32 = 0, kRouteF16 = 1, kRouteAuto = 2 };
+
+// Which GEMM kernel(s) a product of M x N over K needs.  Tensor-bound iff
+// 8 bins M N K / P_tf32x3 > 8 bins (MK + NK + MN) / B_hbm, i.e.
+// MNK / (MK + NK + MN) > 274 TF/s / 6.55 TB/s ~= 42 (MEASURED_PEAKS.json).
+static GemmRoute gemm_route(size_t M, size_t N, size_t K) {
+  if (g_gemm_kind == FFTCONV_B200_GEMM_TF32X3) return kRouteTf32;
+  if (g_gemm_kind == FFTCONV_B200_GEMM_F16X3) return kRouteF16;
+  const double mnk = (double)M * N * K, bytes = (double)M * K + (double)N * K + (double)M * N;
+  return mnk > 42.0 * bytes ? kRouteAuto : kRouteTf32;
+}
+
+static void launch_gemm_kernel(const float* A, const float* B, float* out, size_t bins, size_t M, size_t N,
+                               size_t kpad, float im_sign, OutLayout lay, size_t ldm, const DevInfo& di,
+                               cudaStream_t st, bool f16, int select, const unsigned long long* amax_a,
+                               const unsigned long long* amax_b, int* path);
+
+// Returns the number of launches (2 for an auto pair).  amax_* (K1's per-row
+// words, rows_* rows) are required for the fp16 routes; without them the
+// GEMM runs 3xTF32.
+static int launch_gemm(const float* A, const float* B, float* out, size_t bins, size_t M, size_t N,
+                       size_t kpad, float im_sign, OutLayout lay, size_t ldm, const DevInfo& di,
+                       cudaStream_t st, GemmRoute route = kRouteTf32,
+                       const unsigned long long* amax_a = nullptr, const unsigned long long* amax_b = nullptr,
+                       int* path = nullptr) {
+  if (!amax_a || !amax_b) route = kRouteTf32;
+  if (route == kRouteAuto) {
+    launch_gemm_kernel(A, B, out, bins, M, N, kpad, im_sign, lay, ldm, di, st, true, 1, amax_a, amax_b, path);
+    launch_gemm_kernel(A, B, out, bins, M, N, kpad, im_sign, lay, ldm, di, st, false, 2, amax_a, amax_b, path);
+    return 2;
+  }
+  launch_gemm_kernel(A, B, out, bins, M, N, kpad, im_sign, lay, ldm, di, st, route == kRouteF16, 0, amax_a,
+                     amax_b, path);
+  return 1;
+}
+
+static void launch_gemm_kernel(const float* A, const float* B, float* out, size_t bins, size_t M, size_t N,
+                               size_t kpad, float im_sign, OutLayout lay, size_t ldm, const DevInfo& di,
+                               cudaStream_t st, bool f16, int select, const unsigned long long* amax_a,
+                               const unsigned long long* amax_b, int* path) {
   const GemmGeom g = gemm_geom(M, N, di, f16);
   CUtensorMap ta = make_operand_map(A, kpad, M, bins, kTileM);
   CUtensorMap tb = make_operand_map(B, kpad, N, bins, (uint32_t)g.nc);
@@ -419,6 +460,10 @@ static void launch_gemm(const float* A, const float* B, float* out, size_t bins,
   p.im_sign = im_sign;
   p.amax_a = amax_a;
   p.amax_b = amax_b;
+  p.rows_a = (int)M;
+  p.rows_b = (int)N;
+  p.select = select;
+  p.path = path;
   p.gm_log2 = 4;
   if (lay == kBinMajor) {
     p.s_t = (long long)N * ldm;
@@ -458,14 +503,17 @@ static void launch_gemm(const float* A, const float* B, float* out, size_t bins,
 #endif
 }
 
-// max |component| of n floats into *out (epoch 0 word; debug hook helper).
-__global__ void absmax_kernel(const float* v, long long n, unsigned long long* out) {
-  uint32_t m = 0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x)
-    m = max(m, __float_as_uint(v[i]) & 0x7fffffffu);
-  m = __reduce_max_sync(0xffffffffu, m);
-  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)m);
+// Per-row max |component| of a bin-major operand F[t][rows][2*kp] into
+// out[row] (epoch 0 words; debug hook helper).  grid = rows.
+__global__ void absmax_rows_kernel(const float* v, long long bins, int rows, int kp2, unsigned long long* out) {
+  const int r = blockIdx.x;
+  float m = 0.f;
+  for (long long i = threadIdx.x; i < bins * kp2; i += blockDim.x) {
+    const long long t = i / kp2, k = i - t * kp2;
+    m = fmaxf(m, fabsf(v[(t * rows + r) * kp2 + k]));
+  }
+  const uint32_t b = __reduce_max_sync(0xffffffffu, __float_as_uint(m));
+  if ((threadIdx.x & 31) == 0) atomicMax(out + r, (unsigned long long)b);
 }
 
 // Negates every imaginary part of n complex values (debug hook helper).
@@ -505,7 +553,9 @@ struct fftconv_b200_ws {
   cudaEvent_t pev[2][kMaxChunks + 1] = {};  // chunk pipeline: inputs landed / outputs ready
   bool pev_ready = false;
   uint64_t ctr[3] = {0, 0, 0};
-  unsigned long long* amax = nullptr;  // K1 -> K3 operand max-magnitude words [A, B]
+  unsigned long long* amax = nullptr;  // K1 -> K3 per-row max-magnitude words: A rows | B rows
+  size_t amax_rows = 0;                // rows per operand region
+  int* gemm_path = nullptr;            // which GEMM kernel ran last (1 fp16x3, 0 3xTF32)
   float2* lscr = nullptr;              // m = 128 transform scratch (fft_large.cuh)
   size_t lscr_n = 0;
   unsigned epoch = 0;
@@ -631,13 +681,14 @@ static bool gemm_swap(size_t M, size_t N) {
 
 // ---- the three operators (device pointers) ---------------------------
 
-// Both forward transforms; at m >= 4 (the TMA K1) they also record the
-// operands' max-magnitude words for the fp16x3 GEMM under a fresh epoch.
-// a.amax / b.amax stay null otherwise (the GEMM then runs 3xTF32).
-int r2c_operands(fftconv_b200_ws* ws, size_t m, R2CParams& a, R2CParams& b, cudaStream_t st) {
-  if (m >= 4 && g_gemm_kind == FFTCONV_B200_GEMM_F16X3) {
+// Both forward transforms; when the GEMM route involves fp16x3 (and m >= 4,
+// the TMA / m = 128 K1) they also record the operands' per-row
+// max-magnitude words under a fresh epoch.  a.amax / b.amax stay null
+// otherwise (the GEMM then runs 3xTF32).
+int r2c_operands(fftconv_b200_ws* ws, size_t m, R2CParams& a, R2CParams& b, cudaStream_t st, GemmRoute route) {
+  if (m >= 4 && route != kRouteTf32) {
     a.amax = ws->amax;
-    b.amax = ws->amax + 1;
+    b.amax = ws->amax + ws->amax_rows;
     a.epoch = b.epoch = ++ws->epoch;
   }
   if (m == kL) return launch_r2c_large(a, ws->lscr, ws->lscr_n, st) + launch_r2c_large(b, ws->lscr, ws->lscr_n, st);
@@ -670,17 +721,19 @@ void run_forward(fftconv_b200_ws* ws, const float* x, size_t S, size_t f, size_t
               (int)n, (int)(n | 1)};
   R2CParams b{w, ws->bufB, (long long)(f * k * k), (long long)(k * k), (int)fo, (int)f, (int)kp,
               (int)k, (int)(k | 1)};
-  const int nl = r2c_operands(ws, m, a, b, st);
+  const GemmRoute route = gemm_route(S, fo, f);
+  const int nl = r2c_operands(ws, m, a, b, st, route);
   record(ws, 1, st);  // both forward transforms
   record(ws, 2, st);
   C2RParams c{ws->bufD, y, (long long)(no * no), (long long)(fo * no * no), (int)fo, (int)S,
               (int)no, 0, 0, 1.0f / (float)(m * m), (int)round_up(S, 2)};
+  int ng;
   if (!gemm_swap(S, fo)) {  // D[t][o][b]: planes (r = o, j = b)
-    launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, S, fo, kp, 1.0f, c2r_layout(m), round_up(S, 2),
-                ws->di, st, a.amax, b.amax);
+    ng = launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, S, fo, kp, 1.0f, c2r_layout(m), round_up(S, 2),
+                     ws->di, st, route, a.amax, b.amax, ws->gemm_path);
   } else {  // D^T[t][b][o]: planes (r = b, j = o)
-    launch_gemm(ws->bufB, ws->bufA, ws->bufD, bins, fo, S, kp, -1.0f, c2r_layout(m), round_up(fo, 2),
-                ws->di, st, b.amax, a.amax);
+    ng = launch_gemm(ws->bufB, ws->bufA, ws->bufD, bins, fo, S, kp, -1.0f, c2r_layout(m), round_up(fo, 2),
+                     ws->di, st, route, b.amax, a.amax, ws->gemm_path);
     c = C2RParams{ws->bufD, y, (long long)(fo * no * no), (long long)(no * no), (int)S, (int)fo,
                   (int)no, 0, 0, 1.0f / (float)(m * m), (int)round_up(fo, 2)};
   }
@@ -688,7 +741,7 @@ void run_forward(fftconv_b200_ws* ws, const float* x, size_t S, size_t f, size_t
   c.gm = c2r_layout(m) == kGroupMajor;
   const int nc = c2r_run(ws, m, c, st);
   record(ws, 4, st);
-  ws->last_launches = nl + 1 + nc;
+  ws->last_launches = nl + ng + nc;
   ws->ctr[0] += S * f + fo * f;
   ws->ctr[1] += S * fo;
   ws->ctr[2] += (uint64_t)bins * fo * f * S;
@@ -714,17 +767,19 @@ void run_grad_input(fftconv_b200_ws* ws, const float* gy, size_t S, size_t fo, s
               (int)kp, (int)no, (int)(no | 1)};
   R2CParams b{w, ws->bufB, (long long)(k * k), (long long)(f * k * k), (int)f, (int)fo, (int)kp,
               (int)k, (int)(k | 1), /*conj=*/1};  // GX = GY . W = GY . conj(conj W)
-  const int nl = r2c_operands(ws, m, a, b, st);
+  const GemmRoute route = gemm_route(S, f, fo);
+  const int nl = r2c_operands(ws, m, a, b, st, route);
   record(ws, 1, st);  // both forward transforms
   record(ws, 2, st);
   C2RParams c{ws->bufD, gx, (long long)(n * n), (long long)(f * n * n), (int)f, (int)S, (int)n,
               0, 0, 1.0f / (float)(m * m), (int)round_up(S, 2)};
+  int ng;
   if (!gemm_swap(S, f)) {  // D[t][f][b]
-    launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, S, f, kp, 1.0f, c2r_layout(m), round_up(S, 2),
-                ws->di, st, a.amax, b.amax);
+    ng = launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, S, f, kp, 1.0f, c2r_layout(m), round_up(S, 2),
+                     ws->di, st, route, a.amax, b.amax, ws->gemm_path);
   } else {  // D^T[t][b][f]
-    launch_gemm(ws->bufB, ws->bufA, ws->bufD, bins, f, S, kp, -1.0f, c2r_layout(m), round_up(f, 2),
-                ws->di, st, b.amax, a.amax);
+    ng = launch_gemm(ws->bufB, ws->bufA, ws->bufD, bins, f, S, kp, -1.0f, c2r_layout(m), round_up(f, 2),
+                     ws->di, st, route, b.amax, a.amax, ws->gemm_path);
     c = C2RParams{ws->bufD, gx, (long long)(f * n * n), (long long)(n * n), (int)S, (int)f, (int)n,
                   0, 0, 1.0f / (float)(m * m), (int)round_up(f, 2)};
   }
@@ -732,7 +787,7 @@ void run_grad_input(fftconv_b200_ws* ws, const float* gy, size_t S, size_t fo, s
   c.gm = c2r_layout(m) == kGroupMajor;
   const int nc = c2r_run(ws, m, c, st);
   record(ws, 4, st);
-  ws->last_launches = nl + 1 + nc;
+  ws->last_launches = nl + ng + nc;
   ws->ctr[0] += S * fo + fo * f;
   ws->ctr[1] += S * f;
   ws->ctr[2] += (uint64_t)bins * fo * f * S;
@@ -760,11 +815,12 @@ void run_grad_weight(fftconv_b200_ws* ws, const float* gy, size_t Sg, size_t fo,
               (int)kp, (int)no, (int)(no | 1)};
   R2CParams b{x, ws->bufB, (long long)(n * n), (long long)(f * n * n), (int)f, (int)S, (int)kp,
               (int)n, (int)(n | 1)};
-  const int nl = r2c_operands(ws, m, a, b, st);
+  const GemmRoute route = gemm_route(fo, f, S);
+  const int nl = r2c_operands(ws, m, a, b, st, route);
   record(ws, 1, st);  // both forward transforms
   record(ws, 2, st);
-  launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, fo, f, kp, -1.0f, c2r_layout(m), round_up(fo, 2), ws->di, st,
-              a.amax, b.amax);
+  const int ng = launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, fo, f, kp, -1.0f, c2r_layout(m), round_up(fo, 2),
+                             ws->di, st, route, a.amax, b.amax, ws->gemm_path);
   record(ws, 3, st);
   C2RParams c{ws->bufD, gw, (long long)(k * k), (long long)(f * k * k), (int)f, (int)fo, (int)k,
               0, 0, 1.0f / (float)(m * m), (int)round_up(fo, 2)};
@@ -772,7 +828,7 @@ void run_grad_weight(fftconv_b200_ws* ws, const float* gy, size_t Sg, size_t fo,
   c.accum = accum;
   const int nc = c2r_run(ws, m, c, st);
   record(ws, 4, st);
-  ws->last_launches = nl + 1 + nc;
+  ws->last_launches = nl + ng + nc;
   ws->ctr[0] += S * f + S * fo;
   ws->ctr[1] += fo * f;
   ws->ctr[2] += (uint64_t)bins * fo * f * S;
@@ -807,8 +863,13 @@ int fftconv_b200_ws_create(const fftconv_b200_layer* configs, size_t count, int 
       DeviceGuard g(device);
       ws->di = dev_info(device);
       FCB_CUDA(cudaStreamCreateWithFlags(&ws->host_stream, cudaStreamNonBlocking));
-      FCB_CUDA(cudaMalloc(&ws->amax, 2 * sizeof(unsigned long long)));
-      FCB_CUDA(cudaMemset(ws->amax, 0, 2 * sizeof(unsigned long long)));
+      for (size_t i = 0; i < count; ++i)  // operand rows are maps or samples
+        ws->amax_rows = std::max({ws->amax_rows, (size_t)configs[i].batch, (size_t)configs[i].in_maps,
+                                  (size_t)configs[i].out_maps});
+      FCB_CUDA(cudaMalloc(&ws->amax, 2 * ws->amax_rows * sizeof(unsigned long long)));
+      FCB_CUDA(cudaMemset(ws->amax, 0, 2 * ws->amax_rows * sizeof(unsigned long long)));
+      FCB_CUDA(cudaMalloc(&ws->gemm_path, sizeof(int)));
+      FCB_CUDA(cudaMemset(ws->gemm_path, 0xff, sizeof(int)));
       FCB_CUDA(cudaStreamCreateWithFlags(&ws->h2d_stream, cudaStreamNonBlocking));
       FCB_CUDA(cudaStreamCreateWithFlags(&ws->d2h_stream, cudaStreamNonBlocking));
       for (auto& row : ws->pev)
@@ -844,6 +905,7 @@ void fftconv_b200_ws_destroy(fftconv_b200_ws* ws) {
     for (float* p : {ws->freq, ws->st_in0, ws->st_in1, ws->st_out})
       if (p) cudaFree(p);
     if (ws->amax) cudaFree(ws->amax);
+    if (ws->gemm_path) cudaFree(ws->gemm_path);
     if (ws->lscr) cudaFree(ws->lscr);
     if (ws->host_stream) cudaStreamDestroy(ws->host_stream);
     if (ws->h2d_stream) cudaStreamDestroy(ws->h2d_stream);
@@ -858,10 +920,20 @@ void fftconv_b200_ws_destroy(fftconv_b200_ws* ws) {
 }
 
 int fftconv_b200_set_gemm_kind(int kind) {
-  if (kind != FFTCONV_B200_GEMM_F16X3 && kind != FFTCONV_B200_GEMM_TF32X3) return -1;
+  if (kind != FFTCONV_B200_GEMM_F16X3 && kind != FFTCONV_B200_GEMM_TF32X3 && kind != FFTCONV_B200_GEMM_AUTO)
+    return -1;
   const int prev = g_gemm_kind;
   g_gemm_kind = kind;
   return prev;
+}
+
+int fftconv_b200_last_gemm_path(fftconv_b200_ws* ws) {
+  if (!ws) return -1;
+  int v = -1;
+  DeviceGuard g(ws->device);
+  if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+  if (cudaMemcpy(&v, ws->gemm_path, sizeof v, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  return v;
 }
 
 const char* fftconv_b200_last_error(const fftconv_b200_ws* ws) {
@@ -1204,12 +1276,17 @@ int fftconv_b200_debug_cgemm(const float* a, const float* b, float* out, size_t 
     if (mode == 1)  // A . B = A . conj(conj(B))
       conj_inplace_kernel<<<256, 256, 0, st>>>(reinterpret_cast<float2*>(B),
                                                (long long)(bins * N * kp));
+    // per-row maxima for the fp16 routes; under "auto" this hook always
+    // launches the fp16x3 / 3xTF32 pair, so the selection itself is tested
     unsigned long long* amax = nullptr;
-    FCB_CUDA(cudaMalloc(&amax, 2 * sizeof(unsigned long long)));
-    FCB_CUDA(cudaMemsetAsync(amax, 0, 2 * sizeof(unsigned long long), st));
-    absmax_kernel<<<256, 256, 0, st>>>(A, (long long)(bins * M * kp * 2), amax);
-    absmax_kernel<<<256, 256, 0, st>>>(B, (long long)(bins * N * kp * 2), amax + 1);
-    launch_gemm(A, B, out, bins, M, N, kp, mode == 2 ? -1.0f : 1.0f, kBinMajor, M, di, st, amax, amax + 1);
+    FCB_CUDA(cudaMalloc(&amax, (M + N) * sizeof(unsigned long long)));
+    FCB_CUDA(cudaMemsetAsync(amax, 0, (M + N) * sizeof(unsigned long long), st));
+    absmax_rows_kernel<<<(unsigned)M, 256, 0, st>>>(A, (long long)bins, (int)M, (int)(kp * 2), amax);
+    absmax_rows_kernel<<<(unsigned)N, 256, 0, st>>>(B, (long long)bins, (int)N, (int)(kp * 2), amax + M);
+    const GemmRoute route = g_gemm_kind == FFTCONV_B200_GEMM_TF32X3 ? kRouteTf32
+                            : g_gemm_kind == FFTCONV_B200_GEMM_F16X3 ? kRouteF16
+                                                                     : kRouteAuto;
+    launch_gemm(A, B, out, bins, M, N, kp, mode == 2 ? -1.0f : 1.0f, kBinMajor, M, di, st, route, amax, amax + M);
     FCB_CUDA(cudaStreamSynchronize(st));
     cudaFree(A);
     cudaFree(B);

@@ -130,6 +130,12 @@ class ConvWorkspace:
         raise_for_status(code, _native.last_error(self._h))
         return [float(v) for v in out]
 
+    def last_gemm_path(self) -> str | None:
+        """Which GEMM kernel ran in the last call: "f16x3", "tf32x3" or None
+        (synchronises the device; include/fftconv_b200.h)."""
+        v = int(_native.lib().fftconv_b200_last_gemm_path(self._h))
+        return {1: "f16x3", 0: "tf32x3"}.get(v)
+
     def last_launch_count(self) -> int:
         return int(_native.lib().fftconv_b200_last_launch_count(self._h))
 

@@ -38,12 +38,12 @@ def dev():
     return torch.device("cuda:0")
 
 
-@pytest.fixture(params=["f16x3", "tf32x3"])
+@pytest.fixture(params=["f16x3", "tf32x3", "auto"])
 def gemm_kind(request):
     """Runs the test under each K3 precision scheme (fftconv_b200_set_gemm_kind)."""
     from paper_1312_5851_b200 import _native
 
-    kind = {"f16x3": 0, "tf32x3": 1}[request.param]
+    kind = {"f16x3": 0, "tf32x3": 1, "auto": 2}[request.param]
     prev = _native.lib().fftconv_b200_set_gemm_kind(kind)
     yield request.param
     _native.lib().fftconv_b200_set_gemm_kind(prev)

@@ -70,3 +70,60 @@ def test_kinds_agree_at_paper_point(dev):
         lib.fftconv_b200_set_gemm_kind(prev)
     for u, v in zip(a, b):
         assert oracle.rel_l2_error(u, v.astype(np.float64)) <= 1e-5
+
+
+@pytest.mark.parametrize("kind", ["tf32x3", "auto"])
+def test_samples_of_very_different_magnitude(dev, kind):
+    """Samples 1e-12 and 1e12 in one minibatch each keep their own relative
+    accuracy under 3xTF32 and under auto (which falls back to 3xTF32 when
+    rows span more than 2^18)."""
+    from paper_1312_5851_b200 import _native
+
+    cfg = LayerConfig(3, 8, 128, 128, 128)  # tensor-bound GEMM shape: auto launches the pair
+    x, w, gy = _inputs(cfg, 93)
+    for arr in (x, gy):
+        arr[0] *= np.float32(1e12)
+        arr[2] *= np.float32(1e-12)
+    prev = _native.set_gemm_kind(kind)
+    try:
+        got = _run(cfg, x, w, gy, dev)
+    finally:
+        _native.set_gemm_kind(prev)
+    ref = _ref(x, w, gy)
+    for b in (0, 1, 2, 77):  # fprop / bprop outputs per sample
+        for g, r in zip(got[:2], ref[:2]):
+            assert oracle.rel_l2_error(g[b], r[b]) <= 1e-4
+    assert oracle.rel_l2_error(got[2], ref[2]) <= 1e-4
+
+
+def test_auto_route_selection(dev):
+    """auto: 3xTF32 where the GEMM is byte-bound (P's shape); on a
+    tensor-bound shape fp16x3 for well-scaled data and the 3xTF32 fallback
+    when an operand's rows span more than 2^18."""
+    import torch
+
+    from paper_1312_5851_b200 import _native
+
+    prev = _native.set_gemm_kind("auto")
+    try:
+        cfg = LayerConfig(3, 8, 128, 128, 128)  # MNK / (MK + NK + MN) = 42.7 > 42
+        x, w, gy = _inputs(cfg, 94)
+        ws = ConvWorkspace([cfg])
+        xd, wd = torch.from_numpy(x).to(dev), torch.from_numpy(w).to(dev)
+        y = ws.forward(xd, wd)
+        assert ws.last_gemm_path() == "f16x3"
+        assert oracle.rel_l2_error(y.cpu().numpy(), _ref(x, w, gy)[0]) <= 1e-4
+        x2 = x.copy()
+        x2[5] *= np.float32(2.0 ** -30)
+        y2 = ws.forward(torch.from_numpy(x2).to(dev), wd)
+        assert ws.last_gemm_path() == "tf32x3"
+        r2 = _ref(x2, w, gy)[0]
+        assert oracle.rel_l2_error(y2[5].cpu().numpy(), r2[5]) <= 1e-4
+        p = LayerConfig(7, 32, 96, 96, 16)  # P-like shape (34.9): byte-bound
+        xp, wp, _ = _inputs(p, 95)
+        ConvWorkspace([p]).forward(torch.from_numpy(xp).to(dev), torch.from_numpy(wp).to(dev))
+        wsp = ConvWorkspace([p])
+        wsp.forward(torch.from_numpy(xp).to(dev), torch.from_numpy(wp).to(dev))
+        assert wsp.last_gemm_path() == "tf32x3"
+    finally:
+        _native.set_gemm_kind(prev)
