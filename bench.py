@@ -297,18 +297,20 @@ def main():
     # ---- per-kernel device times (events between the launches of each op)
     ws.set_stage_timing(True)
     stage = {op: [] for op in OPS}
+    gemm_path = {}  # the GEMM kernel that actually ran per op (auto may pick either)
     for _ in range(5):
         for op, fn in (("forward", lambda: ws.forward(xd, wd)), ("grad_input", lambda: ws.grad_input(gyd, wd)),
                        ("grad_weight", lambda: ws.grad_weight(gyd, xd))):
             flush.fill_(2.0)
             fn()
             stage[op].append(ws.stage_ms())
+            gemm_path[op] = ws.last_gemm_path() or "tf32x3"
     ws.set_stage_timing(False)
     stage_ms = {op: [statistics.mean(v[i] for v in stage[op]) for i in range(4)] for op in OPS}
 
     hbm_gbs, bf16_tflops, peak_src = load_peaks()
     kind = gemm_kind()
-    gemm_tflops = cost_model.gemm_tensor_tflops(bf16_tflops, kind)
+    op_tflops = {op: cost_model.gemm_tensor_tflops(bf16_tflops, gemm_path[op]) for op in OPS}
     lc = lcfg
     bins = lc.bins()
     # algorithmic bytes per launch of each transform kernel, flops of the GEMM
@@ -337,16 +339,17 @@ def main():
                 continue
             if i == 2:  # bound by whichever floor is larger: tensor passes or operand/product bytes
                 gb = cost_model.gemm_bytes(lc)
+                gemm_tflops = op_tflops[op]
                 if alg[op][i] / (gemm_tflops * 1e12) >= gb / (hbm_gbs * 1e9):
                     ach = alg[op][i] / (t_ms * 1e-3) / 1e12
                     stages.append({"op": op, "kernel": kname[i], "ms": t_ms, "bound": "tensor", "achieved": ach,
                                    "peak": gemm_tflops, "unit": "TFLOP/s", "frac": ach / gemm_tflops,
-                                   "alg_flops": alg[op][i], "gemm_kind": kind})
+                                   "alg_flops": alg[op][i], "gemm_kind": gemm_path[op]})
                 else:
                     ach = gb / (t_ms * 1e-3) / 1e9
                     stages.append({"op": op, "kernel": kname[i], "ms": t_ms, "bound": "hbm", "achieved": ach,
                                    "peak": hbm_gbs, "unit": "GB/s", "frac": ach / hbm_gbs, "alg_bytes": gb,
-                                   "alg_flops": alg[op][i], "gemm_kind": kind})
+                                   "alg_flops": alg[op][i], "gemm_kind": gemm_path[op]})
             else:
                 ach = alg[op][i] / (t_ms * 1e-3) / 1e9
                 stages.append({"op": op, "kernel": kname[i], "ms": t_ms, "bound": "hbm", "achieved": ach,
@@ -366,9 +369,12 @@ def main():
     if dom == "cgemm_bins_tcgen05" and dom_st[0]["bound"] == "tensor":
         alg_per_launch = statistics.mean(s_["alg_flops"] for s_ in dom_st)
         achieved = alg_per_launch / (dom_ms * 1e-3) / 1e12
-        basis = "/ 3 (fp16x3 passes)" if kind == "f16x3" else "/ 2 (TF32 rate) / 3 (3xTF32 passes)"
-        roofline = {"bound": "tensor", "achieved": achieved, "peak": gemm_tflops, "unit": "TFLOP/s",
-                    "frac": achieved / gemm_tflops,
+        peak_t = statistics.mean(s_["peak"] for s_ in dom_st)
+        kinds = sorted({s_["gemm_kind"] for s_ in dom_st})
+        basis = " / ".join("/ 3 (fp16x3 passes)" if k_ == "f16x3" else "/ 2 (TF32 rate) / 3 (3xTF32 passes)"
+                           for k_ in kinds)
+        roofline = {"bound": "tensor", "achieved": achieved, "peak": peak_t, "unit": "TFLOP/s",
+                    "frac": achieved / peak_t,
                     "peak_basis": f"{peak_src} bf16 {bf16_tflops} TF/s {basis}"}
     else:
         alg_per_launch = statistics.mean(s_["alg_bytes"] for s_ in dom_st)
@@ -443,8 +449,9 @@ def main():
     stage_us = {op: {"r2c": 1e3 * (stage_ms[op][0] + (0.0 if stage_ms[op][1] < 0.005 else stage_ms[op][1])),
                      "gemm": 1e3 * stage_ms[op][2],
                      "c2r": 1e3 * stage_ms[op][3]} for op in OPS}
-    pass_roof = {op: {k: round(v, 4) for k, v in r.items()}
-                 for op, r in cost_model.roofline_report(lcfg, stage_us, hbm_gbs, gemm_tflops).items()}
+    pass_roof = {op: {k: round(v, 4) for k, v in
+                      cost_model.roofline_report(lcfg, {op: stage_us[op]}, hbm_gbs, op_tflops[op])[op].items()}
+                 for op in OPS}
 
     E = 2 * S * f * fo * no * no * k * k
     line = {
@@ -458,6 +465,7 @@ def main():
                    "l2": "flushed between timed steps (256 MiB write)"},
         "tflops_equiv": 3 * E / (ms * 1e-3) / 1e12,
         "gemm_kind": kind,
+        "gemm_path": gemm_path,
         "per_op_ms": {op: sum(stage_ms[op]) for op in OPS},
         "roofline": roofline,
         "pass_roofline": pass_roof,
