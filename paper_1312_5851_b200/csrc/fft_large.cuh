@@ -53,13 +53,18 @@ __device__ __forceinline__ void class_twiddle(float2 (&z)[32]) {
 }
 
 // ---------------------------------------------------------------- r2c K1a
+// Two real columns per complex FFT: the column pair (2p, 2p + 1) is
+// transformed as a + i b; K1b separates A[u] = (Z[u] + conj(Z[-u])) / 2 and
+// B[u] = (Z[u] - conj(Z[-u])) / 2i when it reads the scratch, so K1a keeps
+// all 128 rows u of the packed Z (half the column-pass work of a transform
+// per column).
 template <int C>
-__device__ __forceinline__ void r2c128_col_class(const float* col, float2* o, int src) {
+__device__ __forceinline__ void r2c128_colpair_class(const float2* col, int cs, float2* o, int src, int np) {
   // q-outer accumulation keeps one input live at a time (z + 1 load)
   float2 z[32];
   static_for<0, 32>([&](auto Y) {
     constexpr int y0 = decltype(Y)::value;
-    z[y0] = make_float2(y0 < src ? col[y0] : 0.f, 0.f);
+    z[y0] = y0 < src ? col[y0 * cs] : make_float2(0.f, 0.f);
   });
   static_for<1, 4>([&](auto Q) {
     constexpr int q = decltype(Q)::value;
@@ -67,49 +72,111 @@ __device__ __forceinline__ void r2c128_col_class(const float* col, float2* o, in
       static_for<0, 32>([&](auto Y) {
         constexpr int y0 = decltype(Y)::value;
         const int y = y0 + 32 * q;
-        if (y < src) z[y0] = cadd(z[y0], rot_i<false, (C * q) & 3>(make_float2(col[y0 + 32 * q], 0.f)));
+        if (y < src) z[y0] = cadd(z[y0], rot_i<false, (C * q) & 3>(col[(y0 + 32 * q) * cs]));
       });
   });
   class_twiddle<false, C>(z);
   fft_reg<32, false>(z);
-  static_for<0, 17>([&](auto K) {
+  static_for<0, 32>([&](auto K) {
     constexpr int u = 4 * decltype(K)::value + C;
-    if constexpr (u < kLRows) o[(long long)u * src] = z[decltype(K)::value];
+    o[(long long)u * np] = z[decltype(K)::value];
   });
 }
 
-constexpr int kLColPad = kL + 1;  // odd stride of a transposed (column-contiguous) staged plane
+constexpr int kLColPad = kL + 1;  // odd float2 stride of a staged column pair
 
-// grid = rows * J (one plane per CTA), block = 256 = (column x, class pair):
-// the plane is staged transposed in smem ([x][y], odd stride: conflict-free
-// both ways) with coalesced loads, so the column reads take immediate
-// offsets; thread (x, g) runs classes g and g + 2.
-// dynamic smem = src * 129 floats.
+// grid = rows * J (one plane per CTA), block = 256 = (column pair p, class
+// c): the plane is staged pair-interleaved in smem ([p][y] float2 = (x[y][2p],
+// x[y][2p + 1]), odd stride: conflict-free 4-B stores and 8-B reads) with
+// coalesced loads; thread (p, c) runs class c of pair p and writes rows
+// u = c mod 4 of the packed scratch Z[plane][u][p].
+// dynamic smem = ceil(src / 2) * 129 float2.
 __global__ void __launch_bounds__(256, 2) r2c128_cols_kernel(const R2CParams p, int r0, float2* scr) {
-  extern __shared__ float plane_s[];
+  extern __shared__ float2 pair_s[];
   pdl_wait();
   pdl_trigger();
   const int ql = blockIdx.x;
   const int r = r0 + ql / p.J, j = ql % p.J;
-  const int src = p.src;
+  const int src = p.src, np = (src + 1) >> 1;
   const float* in = p.in + (long long)r * p.in_sr + (long long)j * p.in_sj;
-  const int x = threadIdx.x & 127, g = threadIdx.x >> 7;
-  if (x < src) {  // row y of the plane: lanes = consecutive columns (coalesced)
+  {
+    const int x = threadIdx.x & 127, g = threadIdx.x >> 7;
+    float* ps = reinterpret_cast<float*>(pair_s) + (x >> 1) * (2 * kLColPad) + (x & 1);
+    if (x < 2 * np) {  // row y of the plane: lanes = consecutive columns (coalesced)
 #pragma unroll 8
-    for (int y = g; y < src; y += 2) plane_s[x * kLColPad + y] = __ldg(in + y * src + x);
+      for (int y = g; y < src; y += 2) ps[2 * y] = x < src ? __ldg(in + y * src + x) : 0.f;
+    }
   }
   __syncthreads();
-  if (x >= src) return;
-  float2* o = scr + (long long)ql * kLRows * src + x;
-  const float* col = plane_s + x * kLColPad;
-  if (g == 0) {
-    r2c128_col_class<0>(col, o, src);
-    __syncwarp();
-    r2c128_col_class<2>(col, o, src);
-  } else {
-    r2c128_col_class<1>(col, o, src);
-    __syncwarp();
-    r2c128_col_class<3>(col, o, src);
+  const int pp = threadIdx.x & 63, c = threadIdx.x >> 6;
+  if (pp >= np) return;
+  float2* o = scr + (long long)ql * kL * np + pp;
+  const float2* col = pair_s + pp * kLColPad;
+  switch (c) {
+    case 0: r2c128_colpair_class<0>(col, 1, o, src, np); break;
+    case 1: r2c128_colpair_class<1>(col, 1, o, src, np); break;
+    case 2: r2c128_colpair_class<2>(col, 1, o, src, np); break;
+    default: r2c128_colpair_class<3>(col, 1, o, src, np); break;
+  }
+}
+
+// K1a with the planes streamed by 1-D bulk copies (TMA) through a 2-stage
+// ring: a persistent CTA computes plane i from one stage while plane i + 1
+// lands in the other, so the loads no longer serialise with the FFTs.
+// Needs src even and 16-B aligned contiguous planes (host checks); the
+// stage holds the plane row-major ([y][x], 8-B column-pair reads,
+// conflict-free).  dynamic smem = 16 + 2 * round_up(src * src * 4, 16).
+__global__ void __launch_bounds__(256, 2) r2c128_cols_bulk_kernel(const R2CParams p, int r0, int nplanes,
+                                                                 float2* scr) {
+  extern __shared__ __align__(16) unsigned char lsm[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(lsm);
+  const int src = p.src, np = src >> 1;
+  const uint32_t pbytes = (uint32_t)(src * src * 4);
+  const uint32_t sbytes = (pbytes + 15u) & ~15u;
+  auto plane_in = [&](int ql) {
+    const int r = r0 + ql / p.J, j = ql % p.J;
+    return p.in + (long long)r * p.in_sr + (long long)j * p.in_sj;
+  };
+  const int G = gridDim.x;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  pdl_wait();
+  pdl_trigger();
+  const uint64_t pol = l2_policy_evict_first();
+  if (threadIdx.x == 0)
+    for (int s = 0; s < 2; ++s) {
+      const int ql = blockIdx.x + s * G;
+      if (ql < nplanes) {
+        mbar_arrive_expect_tx(bar + s, pbytes);
+        bulk_load(lsm + 16 + s * sbytes, plane_in(ql), pbytes, bar + s, pol);
+      }
+    }
+  const int pp = threadIdx.x & 63, c = threadIdx.x >> 6;
+  int it = 0;
+  for (int ql = blockIdx.x; ql < nplanes; ql += G, ++it) {
+    const int s = it & 1;
+    mbar_wait(bar + s, (it >> 1) & 1);
+    const float2* stage = reinterpret_cast<const float2*>(lsm + 16 + s * sbytes);
+    if (pp < np) {
+      float2* o = scr + (long long)ql * kL * np + pp;
+      const float2* col = stage + pp;
+      switch (c) {
+        case 0: r2c128_colpair_class<0>(col, np, o, src, np); break;
+        case 1: r2c128_colpair_class<1>(col, np, o, src, np); break;
+        case 2: r2c128_colpair_class<2>(col, np, o, src, np); break;
+        default: r2c128_colpair_class<3>(col, np, o, src, np); break;
+      }
+    }
+    __syncthreads();  // stage s read by every thread
+    if (threadIdx.x == 0 && ql + 2 * G < nplanes) {
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(bar + s, pbytes);
+      bulk_load(lsm + 16 + s * sbytes, plane_in(ql + 2 * G), pbytes, bar + s, pol);
+    }
   }
 }
 
@@ -150,19 +217,33 @@ __global__ void __launch_bounds__(128) r2c128_rows_kernel(const R2CParams p, int
   const int ul = threadIdx.x >> 6, u = blockIdx.z * kLUPerCta + ul;
   const int t = threadIdx.x & 63;
   float2* rows_s = buf + ul * kLRowBuf;
-  if (u < kLRows)
-    for (int jl = 0; jl < jv; ++jl) {
-      const float2* row = scr + ((long long)(rl * p.J + j0 + jl) * kLRows + u) * src;
+  const int np = (src + 1) >> 1;
+  if (u < kLRows && t < np) {  // separate the packed column pairs (K1a): A = (Z[u] + conj Z[-u]) / 2,
+    const float2* zp = scr + (long long)(rl * p.J + j0) * kL * np + t;  // B = (Z[u] - conj Z[-u]) / 2i
+    const long long ou = (long long)u * np, onu = (long long)((kL - u) & (kL - 1)) * np;
+    float2 za[16], zb[16];
 #pragma unroll
-      for (int x = t; x < kL; x += 64)
-        if (x < src) rows_s[jl * kLRowPad + x] = row[x];
-    }
+    for (int jl = 0; jl < 16; ++jl)  // all 32 loads in flight before the first use
+      if (jl < jv) {
+        za[jl] = zp[(long long)jl * kL * np + ou];
+        zb[jl] = zp[(long long)jl * kL * np + onu];
+      }
+#pragma unroll
+    for (int jl = 0; jl < 16; ++jl)
+      if (jl < jv) {
+        rows_s[jl * kLRowPad + 2 * t] = make_float2(0.5f * (za[jl].x + zb[jl].x), 0.5f * (za[jl].y - zb[jl].y));
+        if (2 * t + 1 < src)
+          rows_s[jl * kLRowPad + 2 * t + 1] = make_float2(0.5f * (za[jl].y + zb[jl].y), 0.5f * (zb[jl].x - za[jl].x));
+      }
+  }
   __syncthreads();
-  const int jl = t & 15, h = t >> 4;
+  // FFT phase: warp = class h (warp-uniform switch), lanes = (u row, plane)
+  const int h = threadIdx.x >> 5, cul = (threadIdx.x >> 4) & 1, jl = threadIdx.x & 15;
+  const int cu = blockIdx.z * kLUPerCta + cul;
   float2 z[32];
-  const bool act = u < kLRows && jl < jv;
+  const bool act = cu < kLRows && jl < jv;
   if (act) {
-    const float2* row = rows_s + jl * kLRowPad;
+    const float2* row = buf + cul * kLRowBuf + jl * kLRowPad;
     switch (h) {
       case 0: r2c128_row_class<0>(row, z, src); break;
       case 1: r2c128_row_class<1>(row, z, src); break;
@@ -171,10 +252,10 @@ __global__ void __launch_bounds__(128) r2c128_rows_kernel(const R2CParams p, int
     }
   }
   __syncthreads();  // rows read: reuse as the tile
-  float2* tile = rows_s;  // [v][16]
+  float2* tile = buf + cul * kLRowBuf;  // [v][16]
   const float csign = p.conj ? -1.f : 1.f;
   uint32_t amx = 0;
-  if (u < kLRows) {
+  if (cu < kLRows) {
 #pragma unroll
     for (int k = 0; k < 32; ++k) {
       const float2 v = act ? make_float2(z[k].x, csign * z[k].y) : make_float2(0.f, 0.f);
@@ -186,6 +267,7 @@ __global__ void __launch_bounds__(128) r2c128_rows_kernel(const R2CParams p, int
   // 128 bins x 16 planes per u row: one 128-B line per bin
   const long long bstride = (long long)p.R * p.kpad;  // float2 per bin
   if (u < kLRows) {
+    const float2* tile = rows_s;
     float2* out = reinterpret_cast<float2*>(p.out) + (long long)u * kL * bstride + (long long)r * p.kpad + j0;
 #pragma unroll 8
     for (int i = t; i < kL * 8; i += 64) {
@@ -256,24 +338,27 @@ __global__ void __launch_bounds__(128) c2r128_rows_kernel(const C2RParams p, int
     }
   }
   __syncthreads();
-  const int jl = t & 15, h = t >> 4;
-  const bool act = u < kLRows && jl < jv;
-  float2 z[32];
-  if (act) {
-    switch (h) {
-      case 0: c2r128_row_class<0>(tile, jl, z); break;
-      case 1: c2r128_row_class<1>(tile, jl, z); break;
-      case 2: c2r128_row_class<2>(tile, jl, z); break;
-      default: c2r128_row_class<3>(tile, jl, z); break;
+  {  // FFT phase: warp = class h (warp-uniform switch), lanes = (u row, plane)
+    const int h = threadIdx.x >> 5, cul = (threadIdx.x >> 4) & 1, jl = threadIdx.x & 15;
+    const bool act = blockIdx.z * kLUPerCta + cul < kLRows && jl < jv;
+    float2* ctile = buf + cul * kLTile;
+    float2 z[32];
+    if (act) {
+      switch (h) {
+        case 0: c2r128_row_class<0>(ctile, jl, z); break;
+        case 1: c2r128_row_class<1>(ctile, jl, z); break;
+        case 2: c2r128_row_class<2>(ctile, jl, z); break;
+        default: c2r128_row_class<3>(ctile, jl, z); break;
+      }
+    }
+    __syncthreads();  // tile read: reuse it for the output rows [plane][x']
+    if (act) {
+#pragma unroll
+      for (int k = 0; k < 32; ++k)
+        if (4 * k + h < crop) ctile[jl * kLRowPad + 4 * k + h] = z[k];
     }
   }
-  __syncthreads();  // tile read: reuse it for the output rows [plane][x']
   float2* outb = tile;
-  if (act) {
-#pragma unroll
-    for (int k = 0; k < 32; ++k)
-      if (4 * k + h < crop) outb[jl * kLRowPad + 4 * k + h] = z[k];
-  }
   __syncthreads();
   if (u < kLRows)
     for (int l = 0; l < jv; ++l) {

@@ -328,21 +328,53 @@ static size_t large_scratch_elems(size_t maxJ) {  // float2
   return std::max(large_scratch_budget() / sizeof(float2), maxJ * kLRows * kL);
 }
 
-static int large_rows_per_chunk(size_t J, size_t width, size_t scratch_elems) {
-  const size_t per_row = J * kLRows * width;
+// per_plane = scratch float2 per plane (r2c: 128 rows x column pairs; c2r:
+// 65 rows x crop)
+static int large_rows_per_chunk(size_t J, size_t per_plane, size_t scratch_elems) {
+  const size_t per_row = J * per_plane;
   const size_t cap = std::min(scratch_elems, large_scratch_budget() / sizeof(float2));
   return (int)std::max<size_t>(1, cap / std::max<size_t>(per_row, 1));
 }
 
+// Persistent grid: as many CTAs as fit on all SMs at once (capped by the work).
+template <typename K>
+static int resident_grid(K kern, int threads, int smem, int work) {
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  FCB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+  return std::max(1, std::min(work, std::max(1, per_sm) * sms));
+}
+
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+// K1a / K4b take the bulk-copy ring (fft_large.cuh) when the planes allow
+// 16-B bulk copies; FFTCONV_B200_LBULK=0 forces the staged kernels (tests).
+static bool large_bulk_enabled() {
+  const char* e = getenv("FFTCONV_B200_LBULK");
+  return !(e && atoi(e) == 0);
+}
+
 // Returns the number of launches.
 static int launch_r2c_large(const R2CParams& p, float2* scr, size_t scr_n, cudaStream_t st) {
-  const int rpc = large_rows_per_chunk(p.J, p.src, scr_n);
+  const int np = (p.src + 1) / 2;  // column pairs (K1a packs two real columns per FFT)
+  const int rpc = large_rows_per_chunk(p.J, (size_t)kL * np, scr_n);
   int nl = 0;
   for (int r0 = 0; r0 < p.R; r0 += rpc) {
     const int rows = std::min(rpc, p.R - r0);
-    const int smem = p.src * kLColPad * (int)sizeof(float);
-    smem_optin(r2c128_cols_kernel, smem);
-    launch_pdl(r2c128_cols_kernel, dim3(rows * p.J), dim3(256), smem, st, p, r0, scr);
+    const bool bulk = large_bulk_enabled() && p.src % 2 == 0 && (p.src * p.src) % 4 == 0 && aligned16(p.in) &&
+                      p.in_sr % 4 == 0 && p.in_sj % 4 == 0;
+    if (bulk) {
+      const int smem = 16 + 2 * ((p.src * p.src * 4 + 15) & ~15);
+      smem_optin(r2c128_cols_bulk_kernel, smem);
+      const int planes = rows * p.J;
+      launch_pdl(r2c128_cols_bulk_kernel, dim3(resident_grid(r2c128_cols_bulk_kernel, 256, smem, planes)), dim3(256),
+                 smem, st, p, r0, planes, scr);
+    } else {
+      const int smem = np * kLColPad * (int)sizeof(float2);
+      smem_optin(r2c128_cols_kernel, smem);
+      launch_pdl(r2c128_cols_kernel, dim3(rows * p.J), dim3(256), smem, st, p, r0, scr);
+    }
     launch_pdl(r2c128_rows_kernel, dim3(rows, p.kpad / 16, (kLRows + kLUPerCta - 1) / kLUPerCta), dim3(128), 0,
                st, p, r0, (const float2*)scr);
     nl += 2;
@@ -351,7 +383,7 @@ static int launch_r2c_large(const R2CParams& p, float2* scr, size_t scr_n, cudaS
 }
 
 static int launch_c2r_large(const C2RParams& p, float2* scr, size_t scr_n, cudaStream_t st) {
-  const int rpc = large_rows_per_chunk(p.J, p.crop, scr_n);
+  const int rpc = large_rows_per_chunk(p.J, (size_t)kLRows * p.crop, scr_n);
   int nl = 0;
   for (int r0 = 0; r0 < p.R; r0 += rpc) {
     const int rows = std::min(rpc, p.R - r0);
