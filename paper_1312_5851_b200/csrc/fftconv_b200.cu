@@ -317,15 +317,22 @@ static void launch_c2r(size_t m, const C2RParams& p, cudaStream_t st, const DevI
 
 // ---- m = 128: two passes per direction through an L2-sized scratch
 // (fft_large.cuh).  Operand rows are walked in chunks whose scratch fits.
-constexpr size_t kLScratchBudget = (size_t)48 << 20;  // bytes
+// The scratch holds a whole operator's intermediate planes when it fits
+// under this cap (measured at alex1: one launch pair per operand, 3.73 ms per
+// step, against 4.44 ms with 48 MB L2-sized chunks: the chunks' fill and
+// drain cost more than the L2 residency of the intermediate saves).
+constexpr size_t kLScratchBudget = (size_t)1 << 30;  // bytes
 
 static size_t large_scratch_budget() {  // FFTCONV_B200_LSCRATCH_MB overrides (tests: force chunking)
   const char* e = getenv("FFTCONV_B200_LSCRATCH_MB");
   return (e && atoi(e) > 0) ? ((size_t)atoi(e) << 20) : kLScratchBudget;
 }
 
-static size_t large_scratch_elems(size_t maxJ) {  // float2
-  return std::max(large_scratch_budget() / sizeof(float2), maxJ * kLRows * kL);
+// float2 elements: every plane of the largest role up to the budget, at
+// least one operand row (maxJ planes)
+static size_t large_scratch_elems(size_t maxJ, size_t planes) {
+  const size_t per_plane = (size_t)kLRows * kL;
+  return std::max(maxJ * per_plane, std::min(large_scratch_budget() / sizeof(float2), planes * per_plane));
 }
 
 // per_plane = scratch float2 per plane (r2c: 128 rows x column pairs; c2r:
@@ -671,7 +678,8 @@ void set_arena(fftconv_b200_ws* ws, size_t na, size_t nb, size_t nd) {
 
 void ensure_large_scratch(fftconv_b200_ws* ws, const fftconv_b200_layer& c, size_t m) {
   if (m != kL) return;
-  const size_t need = large_scratch_elems(std::max({c.batch, c.in_maps, c.out_maps}));
+  const size_t need = large_scratch_elems(std::max({c.batch, c.in_maps, c.out_maps}),
+                                         std::max({c.batch * c.in_maps, c.batch * c.out_maps, c.in_maps * c.out_maps}));
   if (need <= ws->lscr_n) return;
   if (ws->lscr) cudaFree(ws->lscr);
   ws->lscr = nullptr;
@@ -1244,8 +1252,8 @@ int fftconv_b200_debug_r2c(const float* in, size_t planes, size_t src, size_t m,
                 (int)(src | 1)};
     float2* scr = nullptr;
     if (m == kL) {
-      FCB_CUDA(cudaMalloc(&scr, large_scratch_elems(planes) * sizeof(float2)));
-      launch_r2c_large(p, scr, large_scratch_elems(planes), (cudaStream_t)stream);
+      FCB_CUDA(cudaMalloc(&scr, large_scratch_elems(planes, planes) * sizeof(float2)));
+      launch_r2c_large(p, scr, large_scratch_elems(planes, planes), (cudaStream_t)stream);
     } else {
       launch_r2c_one(m, p, (cudaStream_t)stream, dev_info(0));
     }
@@ -1276,8 +1284,8 @@ int fftconv_b200_debug_c2r(const float* in, size_t planes, size_t m, size_t crop
                 1.0f / (float)(m * m), (int)round_up(planes, 2)};
     float2* scr = nullptr;
     if (m == kL) {
-      FCB_CUDA(cudaMalloc(&scr, large_scratch_elems(planes) * sizeof(float2)));
-      launch_c2r_large(p, scr, large_scratch_elems(planes), (cudaStream_t)stream);
+      FCB_CUDA(cudaMalloc(&scr, large_scratch_elems(planes, planes) * sizeof(float2)));
+      launch_c2r_large(p, scr, large_scratch_elems(planes, planes), (cudaStream_t)stream);
     } else {
       launch_c2r(m, p, (cudaStream_t)stream, dev_info(0));
     }
