@@ -5,19 +5,22 @@
 //
 // A 128 x 65 half spectrum (66.5 KB per plane) does not fit the one-pass
 // shared-memory design of fft_tma.cuh with enough planes per CTA to write
-// whole lines, so each direction runs as two passes through an
-// L2-sized scratch (the host walks the planes in chunks of operand rows
-// whose scratch fits ~48 MB, so the intermediate never leaves L2):
+// whole lines, so each direction runs as two passes through an HBM scratch
+// sized for the whole operator (the host walks operand rows in chunks only
+// above a 1 GB cap):
 //
-//   r2c  K1a  column pass  (plane, u class c, column x):
-//             X[4k + c][x] = FFT32_k( w128^(c y') * sum_q x[y' + 32q][x] (-i)^(cq) )
-//             (radix-4 decimation in frequency: a 32-point register FFT per
-//             thread yields the rows u = c mod 4), rows u <= 64 -> scratch
-//             S[plane][u][x]
-//        K1b  row pass  (16 planes, one u): the 16 scratch rows staged in
-//             smem, per (plane, v class h) the same decimation over x, the
-//             [v][16 planes] tile written as full 128-B lines of the
-//             bin-major operand F[t][r][2*kpad] (K padding as zeros),
+//   r2c  K1a  column pass  (plane, column pair p = (2p, 2p + 1), u class c):
+//             Z[4k + c][p] = FFT32_k( w128^(c y') * sum_q z[y' + 32q] (-i)^(cq) ),
+//             z[y] = x[y][2p] + i x[y][2p + 1] (two real columns per complex
+//             FFT; radix-4 decimation in frequency: a 32-point register FFT
+//             per thread yields the rows u = c mod 4), all 128 rows u of the
+//             packed Z -> scratch S[plane][u][p]; planes streamed by bulk
+//             copies through a 2-stage smem ring (persistent CTAs)
+//        K1b  row pass  (16 planes, one u): the pairs separated on load,
+//             A[u] = (Z[u] + conj Z[-u]) / 2, B[u] = (Z[u] - conj Z[-u]) / 2i,
+//             staged in smem, per (plane, v class h) the same decimation
+//             over x, the [v][16 planes] tile written as full 128-B lines of
+//             the bin-major operand F[t][r][2*kpad] (K padding as zeros),
 //             optional conjugate, max-magnitude word for the fp16x3 GEMM
 //   c2r  K4a  row pass  (16 planes, one u): inverse over v of the product
 //             rows (group-major or bin-major, as the GEMM wrote them), only
@@ -283,14 +286,14 @@ __global__ void __launch_bounds__(128) r2c128_rows_kernel(const R2CParams p, int
 }
 
 // ---------------------------------------------------------------- c2r K4a
-template <int H>
+template <int H, int TS>  // TS = tile stride per bin (float2)
 __device__ __forceinline__ void c2r128_row_class(const float2* tile, int jl, float2 (&z)[32]) {
-  static_for<0, 32>([&](auto V) { z[decltype(V)::value] = tile[decltype(V)::value * 17 + jl]; });
+  static_for<0, 32>([&](auto V) { z[decltype(V)::value] = tile[decltype(V)::value * TS + jl]; });
   static_for<1, 4>([&](auto Q) {
     constexpr int q = decltype(Q)::value;
     static_for<0, 32>([&](auto V) {
       constexpr int v0 = decltype(V)::value;
-      z[v0] = cadd(z[v0], rot_i<true, (H * q) & 3>(tile[(v0 + 32 * q) * 17 + jl]));
+      z[v0] = cadd(z[v0], rot_i<true, (H * q) & 3>(tile[(v0 + 32 * q) * TS + jl]));
     });
   });
   class_twiddle<true, H>(z);
@@ -304,7 +307,16 @@ static_assert(kLTile >= kLRowBuf, "K4a reuses the input tile for the output rows
 // x' class h).  The input tile of a u row is overwritten by its cropped
 // output rows once every thread holds its FFT.
 __global__ void __launch_bounds__(128) c2r128_rows_kernel(const C2RParams p, int r0, float2* scr) {
-  __shared__ float2 buf[kLUPerCta * kLTile];
+  __shared__ __align__(128) float2 buf[kLUPerCta * kLTile];
+  __shared__ uint64_t bar;
+  // group-major product: each u row's 128 bins x 16 planes are one
+  // contiguous 16 KB block -> one bulk copy per row, tile stride 16
+  const bool bulk = p.gm && ((uintptr_t)p.in & 15u) == 0;
+  if (bulk && threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
   pdl_wait();
   pdl_trigger();
   const int rl = blockIdx.x, r = r0 + rl;
@@ -315,7 +327,18 @@ __global__ void __launch_bounds__(128) c2r128_rows_kernel(const C2RParams p, int
   const int t = threadIdx.x & 63;
   float2* tile = buf + ul * kLTile;
   const float2* in = reinterpret_cast<const float2*>(p.in);
-  if (u < kLRows) {
+  if (bulk) {
+    if (threadIdx.x == 0) {
+      const int ngj = (p.J + 15) >> 4, u0 = blockIdx.z * kLUPerCta;
+      const int nr = min(kLUPerCta, kLRows - u0);
+      const uint64_t pol = l2_policy_evict_first();
+      mbar_arrive_expect_tx(&bar, (uint32_t)nr * kL * 16 * 8);
+      for (int i = 0; i < nr; ++i)
+        bulk_load(buf + i * kLTile, in + (((long long)r * ngj + jg) * (kL * kLRows) + (long long)(u0 + i) * kL) * 16,
+                  kL * 16 * 8, &bar, pol);
+    }
+    mbar_wait(&bar, 0);
+  } else if (u < kLRows) {
     if (p.gm) {  // P[r][J/16][t][16]: the 128 bins x 16 planes of row u are contiguous
       const int ngj = (p.J + 15) >> 4;
       const float4* b = reinterpret_cast<const float4*>(
@@ -344,12 +367,18 @@ __global__ void __launch_bounds__(128) c2r128_rows_kernel(const C2RParams p, int
     float2* ctile = buf + cul * kLTile;
     float2 z[32];
     if (act) {
-      switch (h) {
-        case 0: c2r128_row_class<0>(ctile, jl, z); break;
-        case 1: c2r128_row_class<1>(ctile, jl, z); break;
-        case 2: c2r128_row_class<2>(ctile, jl, z); break;
-        default: c2r128_row_class<3>(ctile, jl, z); break;
-      }
+      if (bulk) switch (h) {
+          case 0: c2r128_row_class<0, 16>(ctile, jl, z); break;
+          case 1: c2r128_row_class<1, 16>(ctile, jl, z); break;
+          case 2: c2r128_row_class<2, 16>(ctile, jl, z); break;
+          default: c2r128_row_class<3, 16>(ctile, jl, z); break;
+        }
+      else switch (h) {
+          case 0: c2r128_row_class<0, 17>(ctile, jl, z); break;
+          case 1: c2r128_row_class<1, 17>(ctile, jl, z); break;
+          case 2: c2r128_row_class<2, 17>(ctile, jl, z); break;
+          default: c2r128_row_class<3, 17>(ctile, jl, z); break;
+        }
     }
     __syncthreads();  // tile read: reuse it for the output rows [plane][x']
     if (act) {
@@ -371,15 +400,15 @@ __global__ void __launch_bounds__(128) c2r128_rows_kernel(const C2RParams p, int
 
 // ---------------------------------------------------------------- c2r K4b
 template <int C>
-__device__ __forceinline__ void c2r128_col_class(const C2RParams& p, const float2* col, float* o, int crop) {
+__device__ __forceinline__ void c2r128_col_class(const C2RParams& p, const float2* col, int cs, float* o, int crop) {
   float2 z[32];
-  static_for<0, 32>([&](auto U) { z[decltype(U)::value] = col[decltype(U)::value]; });
+  static_for<0, 32>([&](auto U) { z[decltype(U)::value] = col[decltype(U)::value * cs]; });
   static_for<1, 4>([&](auto Q) {
     constexpr int q = decltype(Q)::value;
     static_for<0, 32>([&](auto U) {
       constexpr int u0 = decltype(U)::value;
       constexpr int u = u0 + 32 * q;
-      const float2 v = u < kLRows ? col[u] : cconj(col[kL - u]);
+      const float2 v = u < kLRows ? col[u * cs] : cconj(col[(kL - u) * cs]);
       z[u0] = cadd(z[u0], rot_i<true, (C * q) & 3>(v));
     });
   });
@@ -420,13 +449,53 @@ __global__ void __launch_bounds__(256, 2) c2r128_cols_kernel(const C2RParams p, 
   const float2* col = zs + x * kLRows;
   // __syncwarp between the classes keeps their register live ranges apart
   if (g == 0) {
-    c2r128_col_class<0>(p, col, o, crop);
+    c2r128_col_class<0>(p, col, 1, o, crop);
     __syncwarp();
-    c2r128_col_class<2>(p, col, o, crop);
+    c2r128_col_class<2>(p, col, 1, o, crop);
   } else {
-    c2r128_col_class<1>(p, col, o, crop);
+    c2r128_col_class<1>(p, col, 1, o, crop);
     __syncwarp();
-    c2r128_col_class<3>(p, col, o, crop);
+    c2r128_col_class<3>(p, col, 1, o, crop);
+  }
+}
+
+
+// K4b with the scratch plane fetched by one bulk copy (crop even: the
+// [65][crop] plane is a 16-B multiple) into a flat smem plane; column x'
+// reads stride crop (lanes = consecutive columns, conflict-free).  Same
+// FFT and stores as c2r128_cols_kernel.  dynamic smem = 16 + 65 * crop * 8.
+__global__ void __launch_bounds__(256, 2) c2r128_cols_flat_kernel(const C2RParams p, int r0, const float2* scr) {
+  extern __shared__ __align__(16) unsigned char lsm[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(lsm);
+  const float2* zs = reinterpret_cast<const float2*>(lsm + 16);
+  const int ql = blockIdx.x;
+  const int r = r0 + ql / p.J, j = ql % p.J;
+  const int crop = p.crop;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  pdl_wait();
+  pdl_trigger();
+  if (threadIdx.x == 0) {
+    const uint32_t bytes = (uint32_t)(kLRows * crop * 8);
+    mbar_arrive_expect_tx(bar, bytes);
+    bulk_load(lsm + 16, scr + (long long)ql * kLRows * crop, bytes, bar, l2_policy_evict_first());
+  }
+  const int x = threadIdx.x & 127, g = threadIdx.x >> 7;
+  mbar_wait(bar, 0);
+  if (x >= crop) return;
+  float* o = p.out + (long long)r * p.out_sr + (long long)j * p.out_sj + x;
+  const float2* col = zs + x;
+  if (g == 0) {
+    c2r128_col_class<0>(p, col, crop, o, crop);
+    __syncwarp();
+    c2r128_col_class<2>(p, col, crop, o, crop);
+  } else {
+    c2r128_col_class<1>(p, col, crop, o, crop);
+    __syncwarp();
+    c2r128_col_class<3>(p, col, crop, o, crop);
   }
 }
 

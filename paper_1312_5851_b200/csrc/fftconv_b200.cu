@@ -397,8 +397,13 @@ static int launch_c2r_large(const C2RParams& p, float2* scr, size_t scr_n, cudaS
     launch_pdl(c2r128_rows_kernel, dim3(rows, (p.J + 15) / 16, (kLRows + kLUPerCta - 1) / kLUPerCta),
                dim3(128), 0, st, p, r0, scr);
     const int smem = kLRows * p.crop * (int)sizeof(float2);
-    smem_optin(c2r128_cols_kernel, smem);
-    launch_pdl(c2r128_cols_kernel, dim3(rows * p.J), dim3(256), smem, st, p, r0, (const float2*)scr);
+    if (large_bulk_enabled() && p.crop % 2 == 0) {
+      smem_optin(c2r128_cols_flat_kernel, 16 + smem);
+      launch_pdl(c2r128_cols_flat_kernel, dim3(rows * p.J), dim3(256), 16 + smem, st, p, r0, (const float2*)scr);
+    } else {
+      smem_optin(c2r128_cols_kernel, smem);
+      launch_pdl(c2r128_cols_kernel, dim3(rows * p.J), dim3(256), smem, st, p, r0, (const float2*)scr);
+    }
     nl += 2;
   }
   return nl;

@@ -18,4 +18,6 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:'r2c
   -o $O/prof_paper python tools/profile_step.py --config paper > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'r2c|cgemm|c2r' -s 9 -c 9 \
   -o $O/prof_wide python tools/profile_step.py --config wide > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:'128' -c 4 \
+  -o $O/prof_alex1 python tools/profile_step.py --config alex1 --reps 1 --ops forward,grad_input > /dev/null 2>&1
 ls -la $O
