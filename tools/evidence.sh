@@ -20,4 +20,11 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:'r2c
   -o $O/prof_wide python tools/profile_step.py --config wide > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:'128' -c 4 \
   -o $O/prof_alex1 python tools/profile_step.py --config alex1 --reps 1 --ops forward,grad_input > /dev/null 2>&1
+# summarise on the box (the reports exceed gpurun's 64 MiB copy-back); keep
+# only the alex1 report
+for c in paper wide alex1; do
+  python tools/ncu_summarize.py $c $O/prof_$c.ncu-rep $O/ncu_full_${c}_$V > /dev/null 2>&1
+done
+cp profiles/ncu_summary.json $O/ncu_summary.json
+rm -f $O/prof_paper.ncu-rep $O/prof_wide.ncu-rep
 ls -la $O
