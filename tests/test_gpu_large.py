@@ -58,6 +58,46 @@ def test_c2r128_matches_numpy(dev, crop):
     assert _rel(got, ref) < 2e-6
 
 
+@pytest.mark.parametrize("src", [118, 128])
+def test_r2c128_staged_path_matches_dft(dev, monkeypatch, src):
+    """FFTCONV_B200_LBULK=0: even planes through the staged K1a / K4b instead
+    of the bulk-copy ones; same spectra and crops."""
+    import torch
+
+    from paper_1312_5851_b200 import kernels
+
+    monkeypatch.setenv("FFTCONV_B200_LBULK", "0")
+    P = 3
+    x = oracle.fill_uniform((P, src, src), 310 + src, 1)
+    got = kernels.r2c(torch.from_numpy(x).to(dev), 128).cpu().numpy()
+    pad = np.zeros((P, 128, 128))
+    pad[:, :src, :src] = x
+    assert _rel(got, np.fft.fft2(pad)[:, :65, :]) < 2e-6
+    rng = np.random.default_rng(src)
+    H = rng.standard_normal((P, 65, 128)) + 1j * rng.standard_normal((P, 65, 128))
+    back = kernels.c2r(torch.from_numpy(H.astype(np.complex64)).to(dev), src).cpu().numpy()
+    assert _rel(back, np.fft.irfft(np.fft.ifft(H, axis=2), n=128, axis=1)[:, :src, :src]) < 2e-6
+
+
+def test_r2c128_unaligned_planes_take_staged_path(dev):
+    """Planes 4 B off 16-B alignment cannot be bulk-copied: the host picks the
+    staged K1a for them (same result)."""
+    import torch
+
+    from paper_1312_5851_b200 import kernels
+
+    P, src = 3, 118
+    x = oracle.fill_uniform((P, src, src), 320, 1)
+    flat = torch.zeros(P * src * src + 4, dtype=torch.float32, device=dev)
+    view = flat[1:1 + P * src * src].view(P, src, src)
+    view.copy_(torch.from_numpy(x))
+    assert view.data_ptr() % 16 != 0 and view.is_contiguous()
+    got = kernels.r2c(view, 128).cpu().numpy()
+    pad = np.zeros((P, 128, 128))
+    pad[:, :src, :src] = x
+    assert _rel(got, np.fft.fft2(pad)[:, :65, :]) < 2e-6
+
+
 def test_r2c_c2r128_round_trip(dev):
     import torch
 
