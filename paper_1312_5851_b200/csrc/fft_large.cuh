@@ -186,24 +186,36 @@ __global__ void __launch_bounds__(256, 2) r2c128_cols_bulk_kernel(const R2CParam
 // ---------------------------------------------------------------- r2c K1b
 template <int H>
 __device__ __forceinline__ void r2c128_row_class(const float2* row, float2 (&z)[32], int src) {
-  static_for<0, 32>([&](auto X) {
-    constexpr int x0 = decltype(X)::value;
-    z[x0] = x0 < src ? row[x0] : make_float2(0.f, 0.f);
+  // 16-B pair reads: the staged row is zero-filled up to the even edge, so
+  // x0 < src (x0 even) makes the pair (x0, x0 + 1) safe to read whole
+  const float4* row4 = reinterpret_cast<const float4*>(row);
+  static_for<0, 16>([&](auto X2) {
+    constexpr int x0 = 2 * decltype(X2)::value;
+    const float4 v = x0 < src ? row4[x0 / 2] : make_float4(0.f, 0.f, 0.f, 0.f);
+    z[x0] = make_float2(v.x, v.y);
+    z[x0 + 1] = make_float2(v.z, v.w);
   });
   static_for<1, 4>([&](auto Q) {
     constexpr int q = decltype(Q)::value;
     if (32 * q < src)
-      static_for<0, 32>([&](auto X) {
-        constexpr int x0 = decltype(X)::value;
-        if (x0 + 32 * q < src) z[x0] = cadd(z[x0], rot_i<false, (H * q) & 3>(row[x0 + 32 * q]));
+      static_for<0, 16>([&](auto X2) {
+        constexpr int x0 = 2 * decltype(X2)::value;
+        if (x0 + 32 * q < src) {
+          const float4 v = row4[(x0 + 32 * q) / 2];
+          z[x0] = cadd(z[x0], rot_i<false, (H * q) & 3>(make_float2(v.x, v.y)));
+          z[x0 + 1] = cadd(z[x0 + 1], rot_i<false, (H * q) & 3>(make_float2(v.z, v.w)));
+        }
       });
   });
   class_twiddle<false, H>(z);
   fft_reg<32, false>(z);
 }
 
-constexpr int kLRowPad = kL + 1;                 // odd float2 stride of the staged rows
-constexpr int kLRowBuf = 16 * kLRowPad;          // float2 per staged u row (>= 128 x 16 tile)
+constexpr int kLRowPad = kL + 1;                 // odd float2 stride of K4a's output rows
+// K1b's staged rows: even float2 stride so column pairs are 16-B reads
+// (quarter-warp lanes jl at 4 jl banks: conflict-free)
+constexpr int kLRowPadF = kL + 2;
+constexpr int kLRowBuf = 16 * kLRowPadF;         // float2 per staged u row (>= 128 x 16 tile)
 constexpr int kLUPerCta = 2;                     // u rows per K1b / K4a CTA
 
 // grid = (rows, kpad / 16, ceil(65 / 2)), block = 128 = (u row, plane jl,
@@ -233,10 +245,11 @@ __global__ void __launch_bounds__(128) r2c128_rows_kernel(const R2CParams p, int
       }
 #pragma unroll
     for (int jl = 0; jl < 16; ++jl)
-      if (jl < jv) {
-        rows_s[jl * kLRowPad + 2 * t] = make_float2(0.5f * (za[jl].x + zb[jl].x), 0.5f * (za[jl].y - zb[jl].y));
-        if (2 * t + 1 < src)
-          rows_s[jl * kLRowPad + 2 * t + 1] = make_float2(0.5f * (za[jl].y + zb[jl].y), 0.5f * (zb[jl].x - za[jl].x));
+      if (jl < jv) {  // pair (2t, 2t + 1); a column at x = src (odd src) is zero
+        const bool two = 2 * t + 1 < src;
+        *reinterpret_cast<float4*>(rows_s + jl * kLRowPadF + 2 * t) =
+            make_float4(0.5f * (za[jl].x + zb[jl].x), 0.5f * (za[jl].y - zb[jl].y),
+                        two ? 0.5f * (za[jl].y + zb[jl].y) : 0.f, two ? 0.5f * (zb[jl].x - za[jl].x) : 0.f);
       }
   }
   __syncthreads();
@@ -246,7 +259,7 @@ __global__ void __launch_bounds__(128) r2c128_rows_kernel(const R2CParams p, int
   float2 z[32];
   const bool act = cu < kLRows && jl < jv;
   if (act) {
-    const float2* row = buf + cul * kLRowBuf + jl * kLRowPad;
+    const float2* row = buf + cul * kLRowBuf + jl * kLRowPadF;
     switch (h) {
       case 0: r2c128_row_class<0>(row, z, src); break;
       case 1: r2c128_row_class<1>(row, z, src); break;
@@ -301,7 +314,7 @@ __device__ __forceinline__ void c2r128_row_class(const float2* tile, int jl, flo
 }
 
 constexpr int kLTile = kL * 17;  // [v][16 planes] with an odd stride (>= kLRowBuf)
-static_assert(kLTile >= kLRowBuf, "K4a reuses the input tile for the output rows");
+static_assert(kLTile >= 16 * kLRowPad, "K4a reuses the input tile for the output rows");
 
 // grid = (rows, ceil(J / 16), ceil(65 / 2)), block = 128 = (u row, plane jl,
 // x' class h).  The input tile of a u row is overwritten by its cropped
