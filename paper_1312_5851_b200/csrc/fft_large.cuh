@@ -221,7 +221,7 @@ constexpr int kLUPerCta = 2;                     // u rows per K1b / K4a CTA
 // grid = (rows, kpad / 16, ceil(65 / 2)), block = 128 = (u row, plane jl,
 // v class h).  The 16 staged scratch rows of a u row are overwritten by
 // its [v][plane] output tile once every thread holds its FFT.
-__global__ void __launch_bounds__(128) r2c128_rows_kernel(const R2CParams p, int r0, const float2* scr) {
+__global__ void __launch_bounds__(128, 6) r2c128_rows_kernel(const R2CParams p, int r0, const float2* scr) {
   __shared__ __align__(16) float2 buf[kLUPerCta * kLRowBuf];
   pdl_wait();
   pdl_trigger();
@@ -319,7 +319,7 @@ static_assert(kLTile >= 16 * kLRowPad, "K4a reuses the input tile for the output
 // grid = (rows, ceil(J / 16), ceil(65 / 2)), block = 128 = (u row, plane jl,
 // x' class h).  The input tile of a u row is overwritten by its cropped
 // output rows once every thread holds its FFT.
-__global__ void __launch_bounds__(128) c2r128_rows_kernel(const C2RParams p, int r0, float2* scr) {
+__global__ void __launch_bounds__(128, 6) c2r128_rows_kernel(const C2RParams p, int r0, float2* scr) {
   __shared__ __align__(128) float2 buf[kLUPerCta * kLTile];
   __shared__ uint64_t bar;
   // group-major product: each u row's 128 bins x 16 planes are one
