@@ -18,7 +18,10 @@
  *
  * Threading: a workspace serves one invocation at a time (conv_fft.hpp:37-38);
  * calls on one workspace are not reentrant.  Device entry points enqueue on
- * the caller's stream and return without synchronising.
+ * the caller's stream and return without synchronising.  Consecutive calls
+ * on one workspace are ordered even across streams: a call on a stream other
+ * than the previous call's first waits for that call to finish on the device
+ * (the host entry points included; not inside a stream capture).
  */
 #ifndef FFTCONV_B200_H_
 #define FFTCONV_B200_H_
@@ -66,7 +69,9 @@ void fftconv_b200_ws_destroy(fftconv_b200_ws* ws);
  * workspace (when non-NULL). */
 const char* fftconv_b200_last_error(const fftconv_b200_ws* ws);
 
-/* Precision scheme of the per-bin complex GEMM (K3), process-wide.  All
+/* Precision scheme of the per-bin complex GEMM (K3): the process default
+ * (fftconv_b200_set_gemm_kind, atomic) and a per-workspace override
+ * (fftconv_b200_ws_set_gemm_kind).  All
  * keep fp32-level accuracy (rel. L2 ~1e-6 against the fp64 oracle):
  *   FFTCONV_B200_GEMM_TF32X3 x = tf32 hi + lo, D = hi.hi + hi.lo + lo.hi
  *       on kind::tf32 -- per-element exponents, the fp32 range;
@@ -87,6 +92,10 @@ const char* fftconv_b200_last_error(const fftconv_b200_ws* ws);
 #define FFTCONV_B200_GEMM_TF32X3 1
 #define FFTCONV_B200_GEMM_AUTO 2
 int fftconv_b200_set_gemm_kind(int kind);
+/* Per-workspace override of the above; kind -1 returns the workspace to the
+ * process default.  Returns the previous override (-1 = none), or -1 for an
+ * unknown kind / NULL workspace. */
+int fftconv_b200_ws_set_gemm_kind(fftconv_b200_ws* ws, int kind);
 /* Which GEMM kernel ran in the workspace's last operator call (synchronises
  * the device): 1 fp16x3, 0 3xTF32, -1 none yet / error. */
 int fftconv_b200_last_gemm_path(fftconv_b200_ws* ws);

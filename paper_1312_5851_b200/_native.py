@@ -41,6 +41,7 @@ SIGNATURES = [
     ("fftconv_b200_maxpool_backward", _i, [_p, _p, _sz, _sz, _sz, _p, _p]),
     ("fftconv_b200_fit_to", _i, [_p, _sz, _sz, _sz, _p, _sz, _p]),
     ("fftconv_b200_set_gemm_kind", _i, [_i]),
+    ("fftconv_b200_ws_set_gemm_kind", _i, [_p, _i]),
     ("fftconv_b200_last_gemm_path", _i, [_p]),
     ("fftconv_b200_debug_r2c", _i, [_p, _sz, _sz, _sz, _p, _p]),
     ("fftconv_b200_debug_c2r", _i, [_p, _sz, _sz, _sz, _p, _p]),

@@ -16,6 +16,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
+#include <map>
 #include <mutex>
 #include <unordered_map>
 #include <stdexcept>
@@ -160,17 +162,20 @@ static void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   FCB_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
 }
 
-// Per-kernel host-side caches, keyed by the kernel's address (several
-// kernels share a signature, so a function-local static would be shared).
+// Per-kernel host-side caches, keyed by (device, kernel address): the
+// shared-memory opt-in is a per-device attribute, and several kernels share a
+// signature, so a function-local static would be shared.
 static std::mutex g_kcache_mu;
-static std::unordered_map<const void*, int> g_smem_done;
+static std::map<std::pair<int, const void*>, int> g_smem_done;
 
-// Opt a kernel into > 48 KB dynamic shared memory (once per size).
+// Opt a kernel into > 48 KB dynamic shared memory (once per device and size).
 template <typename K>
 static void smem_optin(K kern, int bytes) {
   if (bytes <= 48 * 1024) return;
+  int dev = 0;
+  FCB_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lk(g_kcache_mu);
-  int& done = g_smem_done[reinterpret_cast<const void*>(kern)];
+  int& done = g_smem_done[{dev, reinterpret_cast<const void*>(kern)}];
   if (bytes > done) {
     FCB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     done = bytes;
@@ -441,21 +446,23 @@ static GemmGeom gemm_geom(size_t M, size_t N, const DevInfo& di, bool f16) {
 //           and a 3xTF32 fallback launched back to back: each reads K1's
 //           per-row maxima and exactly one of them runs -- fp16x3 when every
 //           operand row is within 2^18 of its operand's maximum.
-static int g_gemm_kind = [] {
+// The process default (atomic: set from any thread); a workspace may
+// override it (fftconv_b200_ws_set_gemm_kind).
+static std::atomic<int> g_gemm_kind{[] {
   const char* e = getenv("FFTCONV_B200_GEMM");
   if (e && std::string(e) == "tf32") return FFTCONV_B200_GEMM_TF32X3;
   if (e && std::string(e) == "f16x3") return FFTCONV_B200_GEMM_F16X3;
   return FFTCONV_B200_GEMM_AUTO;
-}();
+}()};
 
 enum GemmRoute { kRouteTf32 = 0, kRouteF16 = 1, kRouteAuto = 2 };
 
 // Which GEMM kernel(s) a product of M x N over K needs.  Tensor-bound iff
 // 8 bins M N K / P_tf32x3 > 8 bins (MK + NK + MN) / B_hbm, i.e.
 // MNK / (MK + NK + MN) > 274 TF/s / 6.55 TB/s ~= 42 (MEASURED_PEAKS.json).
-static GemmRoute gemm_route(size_t M, size_t N, size_t K) {
-  if (g_gemm_kind == FFTCONV_B200_GEMM_TF32X3) return kRouteTf32;
-  if (g_gemm_kind == FFTCONV_B200_GEMM_F16X3) return kRouteF16;
+static GemmRoute gemm_route(int kind, size_t M, size_t N, size_t K) {
+  if (kind == FFTCONV_B200_GEMM_TF32X3) return kRouteTf32;
+  if (kind == FFTCONV_B200_GEMM_F16X3) return kRouteF16;
   const double mnk = (double)M * N * K, bytes = (double)M * K + (double)N * K + (double)M * N;
   return mnk > 42.0 * bytes ? kRouteAuto : kRouteTf32;
 }
@@ -603,6 +610,14 @@ struct fftconv_b200_ws {
   float2* lscr = nullptr;              // m = 128 transform scratch (fft_large.cuh)
   size_t lscr_n = 0;
   unsigned epoch = 0;
+  int gemm_kind = -1;                   // -1: the process default (g_gemm_kind)
+  // Cross-stream ordering: the event recorded at the end of the last
+  // operator and the stream it ran on.  An operator on another stream (the
+  // host entry points' host_stream, or a different caller stream) waits on
+  // it first, since every operator reuses the same spectra buffers.
+  cudaEvent_t done_ev = nullptr;
+  cudaStream_t last_st = nullptr;
+  bool has_last = false;
   std::string last_error;
   bool timing = false;
   cudaEvent_t ev[5] = {};
@@ -640,6 +655,42 @@ struct DeviceGuard {
     if (prev >= 0 && cur != prev) cudaSetDevice(prev);
   }
 };
+
+int ws_gemm_kind(const fftconv_b200_ws* ws) { return ws->gemm_kind >= 0 ? ws->gemm_kind : g_gemm_kind.load(); }
+
+bool capturing(cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone;
+}
+
+// Orders an operator on `st` after the workspace's previous operator when that
+// one ran on another stream (device- and host-path calls share
+// bufA / bufB / bufD, amax and the scratch).  Not inside a stream capture: a
+// captured graph's own dependencies order it.
+void order_after_last(fftconv_b200_ws* ws, cudaStream_t st) {
+  if (ws->has_last && ws->last_st != st && !capturing(st)) FCB_CUDA(cudaStreamWaitEvent(st, ws->done_ev, 0));
+}
+
+void mark_done(fftconv_b200_ws* ws, cudaStream_t st) {
+  if (capturing(st)) return;
+  FCB_CUDA(cudaEventRecord(ws->done_ev, st));
+  ws->last_st = st;
+  ws->has_last = true;
+}
+
+// K1's per-row max-magnitude words hold max(rows of A, rows of B) per operand
+// region; a workspace reused for a layer with more operand rows than any
+// registered config (the capacity check bounds bins x rows x maps, not rows)
+// grows them.  cudaFree synchronises the device first.
+void ensure_amax(fftconv_b200_ws* ws, size_t rows) {
+  if (rows <= ws->amax_rows) return;
+  if (ws->amax) cudaFree(ws->amax);
+  ws->amax = nullptr;
+  ws->amax_rows = 0;
+  FCB_CUDA(cudaMalloc(&ws->amax, 2 * rows * sizeof(unsigned long long)));
+  FCB_CUDA(cudaMemset(ws->amax, 0, 2 * rows * sizeof(unsigned long long)));
+  ws->amax_rows = rows;
+}
 
 void grow(float*& p, size_t& have, size_t need) {
   if (need <= have) return;
@@ -732,6 +783,7 @@ static bool gemm_swap(size_t M, size_t N) {
 // otherwise (the GEMM then runs 3xTF32).
 int r2c_operands(fftconv_b200_ws* ws, size_t m, R2CParams& a, R2CParams& b, cudaStream_t st, GemmRoute route) {
   if (m >= 4 && route != kRouteTf32) {
+    ensure_amax(ws, (size_t)std::max(a.R, b.R));
     a.amax = ws->amax;
     b.amax = ws->amax + ws->amax_rows;
     a.epoch = b.epoch = ++ws->epoch;
@@ -766,7 +818,7 @@ void run_forward(fftconv_b200_ws* ws, const float* x, size_t S, size_t f, size_t
               (int)n, (int)(n | 1)};
   R2CParams b{w, ws->bufB, (long long)(f * k * k), (long long)(k * k), (int)fo, (int)f, (int)kp,
               (int)k, (int)(k | 1)};
-  const GemmRoute route = gemm_route(S, fo, f);
+  const GemmRoute route = gemm_route(ws_gemm_kind(ws), S, fo, f);
   const int nl = r2c_operands(ws, m, a, b, st, route);
   record(ws, 1, st);  // both forward transforms
   record(ws, 2, st);
@@ -812,7 +864,7 @@ void run_grad_input(fftconv_b200_ws* ws, const float* gy, size_t S, size_t fo, s
               (int)kp, (int)no, (int)(no | 1)};
   R2CParams b{w, ws->bufB, (long long)(k * k), (long long)(f * k * k), (int)f, (int)fo, (int)kp,
               (int)k, (int)(k | 1), /*conj=*/1};  // GX = GY . W = GY . conj(conj W)
-  const GemmRoute route = gemm_route(S, f, fo);
+  const GemmRoute route = gemm_route(ws_gemm_kind(ws), S, f, fo);
   const int nl = r2c_operands(ws, m, a, b, st, route);
   record(ws, 1, st);  // both forward transforms
   record(ws, 2, st);
@@ -860,7 +912,7 @@ void run_grad_weight(fftconv_b200_ws* ws, const float* gy, size_t Sg, size_t fo,
               (int)kp, (int)no, (int)(no | 1)};
   R2CParams b{x, ws->bufB, (long long)(n * n), (long long)(f * n * n), (int)f, (int)S, (int)kp,
               (int)n, (int)(n | 1)};
-  const GemmRoute route = gemm_route(fo, f, S);
+  const GemmRoute route = gemm_route(ws_gemm_kind(ws), fo, f, S);
   const int nl = r2c_operands(ws, m, a, b, st, route);
   record(ws, 1, st);  // both forward transforms
   record(ws, 2, st);
@@ -920,6 +972,7 @@ int fftconv_b200_ws_create(const fftconv_b200_layer* configs, size_t count, int 
       for (auto& row : ws->pev)
         for (auto& e : row) FCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       ws->pev_ready = true;
+      FCB_CUDA(cudaEventCreateWithFlags(&ws->done_ev, cudaEventDisableTiming));
       // Size the frequency buffers for every registered layer and pass up
       // front, so timed calls never allocate.
       size_t na = 0, nb = 0, nd = 0;
@@ -960,6 +1013,7 @@ void fftconv_b200_ws_destroy(fftconv_b200_ws* ws) {
         for (auto& e : row) cudaEventDestroy(e);
     if (ws->ev_ready)
       for (auto& e : ws->ev) cudaEventDestroy(e);
+    if (ws->done_ev) cudaEventDestroy(ws->done_ev);
   }
   delete ws;
 }
@@ -967,8 +1021,16 @@ void fftconv_b200_ws_destroy(fftconv_b200_ws* ws) {
 int fftconv_b200_set_gemm_kind(int kind) {
   if (kind != FFTCONV_B200_GEMM_F16X3 && kind != FFTCONV_B200_GEMM_TF32X3 && kind != FFTCONV_B200_GEMM_AUTO)
     return -1;
-  const int prev = g_gemm_kind;
-  g_gemm_kind = kind;
+  return g_gemm_kind.exchange(kind);
+}
+
+int fftconv_b200_ws_set_gemm_kind(fftconv_b200_ws* ws, int kind) {
+  if (!ws) return -1;
+  if (kind != -1 && kind != FFTCONV_B200_GEMM_F16X3 && kind != FFTCONV_B200_GEMM_TF32X3 &&
+      kind != FFTCONV_B200_GEMM_AUTO)
+    return -1;
+  const int prev = ws->gemm_kind < 0 ? -1 : ws->gemm_kind;
+  ws->gemm_kind = kind;
   return prev;
 }
 
@@ -1014,7 +1076,9 @@ int fftconv_b200_forward(fftconv_b200_ws* ws, const float* x, size_t S, size_t f
   if (!ws) return FFTCONV_B200_INVALID_ARGUMENT;
   return guarded(ws, [&] {
     DeviceGuard g(ws->device);
+    order_after_last(ws, (cudaStream_t)stream);
     run_forward(ws, x, S, f, x_rows, x_cols, w, w_out, w_in, k, y, (cudaStream_t)stream);
+    mark_done(ws, (cudaStream_t)stream);
   });
 }
 
@@ -1024,7 +1088,9 @@ int fftconv_b200_grad_input(fftconv_b200_ws* ws, const float* gy, size_t S, size
   if (!ws) return FFTCONV_B200_INVALID_ARGUMENT;
   return guarded(ws, [&] {
     DeviceGuard g(ws->device);
+    order_after_last(ws, (cudaStream_t)stream);
     run_grad_input(ws, gy, S, fo, gy_rows, gy_cols, w, w_out, w_in, k, gx, (cudaStream_t)stream);
+    mark_done(ws, (cudaStream_t)stream);
   });
 }
 
@@ -1034,8 +1100,10 @@ int fftconv_b200_grad_weight(fftconv_b200_ws* ws, const float* gy, size_t S_gy, 
   if (!ws) return FFTCONV_B200_INVALID_ARGUMENT;
   return guarded(ws, [&] {
     DeviceGuard g(ws->device);
+    order_after_last(ws, (cudaStream_t)stream);
     run_grad_weight(ws, gy, S_gy, fo, gy_rows, gy_cols, x, S_x, f, x_rows, x_cols, gw,
                     (cudaStream_t)stream);
+    mark_done(ws, (cudaStream_t)stream);
   });
 }
 
@@ -1101,6 +1169,7 @@ int fftconv_b200_forward_host(fftconv_b200_ws* ws, const float* x, size_t S, siz
     grow(ws->st_in1, ws->n_in1, nw);
     grow(ws->st_out, ws->n_out, S * py);
     const int C = host_chunks(S, S * px * sizeof(float), m, 12);
+    order_after_last(ws, ws->host_stream);
     uint64_t saved[3];
     std::memcpy(saved, ws->ctr, sizeof saved);
     h2d(ws, ws->st_in1, w, nw);
@@ -1120,6 +1189,7 @@ int fftconv_b200_forward_host(fftconv_b200_ws* ws, const float* x, size_t S, siz
                                cudaMemcpyDeviceToHost, ws->d2h_stream));
     }
     FCB_CUDA(cudaStreamSynchronize(ws->d2h_stream));
+    ws->has_last = false;  // everything this call enqueued has completed
     const uint64_t bins = m * (m / 2 + 1);  // one call = one reference forward
     ws->ctr[0] = saved[0] + S * f + fo * f;
     ws->ctr[1] = saved[1] + S * fo;
@@ -1148,6 +1218,7 @@ int fftconv_b200_grad_input_host(fftconv_b200_ws* ws, const float* gy, size_t S,
     grow(ws->st_in1, ws->n_in1, nw);
     grow(ws->st_out, ws->n_out, S * pgx);
     const int C = host_chunks(S, S * pgy * sizeof(float), m, 6);
+    order_after_last(ws, ws->host_stream);
     uint64_t saved[3];
     std::memcpy(saved, ws->ctr, sizeof saved);
     h2d(ws, ws->st_in1, w, nw);
@@ -1168,6 +1239,7 @@ int fftconv_b200_grad_input_host(fftconv_b200_ws* ws, const float* gy, size_t S,
                                ws->d2h_stream));
     }
     FCB_CUDA(cudaStreamSynchronize(ws->d2h_stream));
+    ws->has_last = false;  // everything this call enqueued has completed
     const uint64_t bins = m * (m / 2 + 1);
     ws->ctr[0] = saved[0] + S * fo + fo * f;
     ws->ctr[1] = saved[1] + S * f;
@@ -1197,6 +1269,7 @@ int fftconv_b200_grad_weight_host(fftconv_b200_ws* ws, const float* gy, size_t S
     grow(ws->st_in1, ws->n_in1, S * px);
     grow(ws->st_out, ws->n_out, ngw);
     const int C = host_chunks(S, S * (pgy + px) * sizeof(float), m, 32);
+    order_after_last(ws, ws->host_stream);
     uint64_t saved[3];
     std::memcpy(saved, ws->ctr, sizeof saved);
     for (int c = 0; c < C; ++c) {
@@ -1215,6 +1288,7 @@ int fftconv_b200_grad_weight_host(fftconv_b200_ws* ws, const float* gy, size_t S
     FCB_CUDA(cudaMemcpyAsync(gw, ws->st_out, ngw * sizeof(float), cudaMemcpyDeviceToHost,
                              ws->host_stream));
     FCB_CUDA(cudaStreamSynchronize(ws->host_stream));
+    ws->has_last = false;
     const uint64_t bins = m * (m / 2 + 1);
     ws->ctr[0] = saved[0] + S * f + S * fo;
     ws->ctr[1] = saved[1] + fo * f;
@@ -1328,9 +1402,10 @@ int fftconv_b200_debug_cgemm(const float* a, const float* b, float* out, size_t 
     FCB_CUDA(cudaMemsetAsync(amax, 0, (M + N) * sizeof(unsigned long long), st));
     absmax_rows_kernel<<<(unsigned)M, 256, 0, st>>>(A, (long long)bins, (int)M, (int)(kp * 2), amax);
     absmax_rows_kernel<<<(unsigned)N, 256, 0, st>>>(B, (long long)bins, (int)N, (int)(kp * 2), amax + M);
-    const GemmRoute route = g_gemm_kind == FFTCONV_B200_GEMM_TF32X3 ? kRouteTf32
-                            : g_gemm_kind == FFTCONV_B200_GEMM_F16X3 ? kRouteF16
-                                                                     : kRouteAuto;
+    const int kind = g_gemm_kind.load();
+    const GemmRoute route = kind == FFTCONV_B200_GEMM_TF32X3 ? kRouteTf32
+                            : kind == FFTCONV_B200_GEMM_F16X3 ? kRouteF16
+                                                              : kRouteAuto;
     launch_gemm(A, B, out, bins, M, N, kp, mode == 2 ? -1.0f : 1.0f, kBinMajor, M, di, st, route, amax, amax + M);
     FCB_CUDA(cudaStreamSynchronize(st));
     cudaFree(A);

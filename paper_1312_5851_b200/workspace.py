@@ -136,6 +136,13 @@ class ConvWorkspace:
         v = int(_native.lib().fftconv_b200_last_gemm_path(self._h))
         return {1: "f16x3", 0: "tf32x3"}.get(v)
 
+    def set_gemm_kind(self, kind: str | None) -> str | None:
+        """This workspace's K3 precision scheme ("tf32x3", "f16x3", "auto"), or
+        None for the process default; returns the previous override."""
+        code = -1 if kind is None else _native.GEMM_KINDS[kind]
+        prev = int(_native.lib().fftconv_b200_ws_set_gemm_kind(self._h, code))
+        return {v: k for k, v in _native.GEMM_KINDS.items()}.get(prev)
+
     def last_launch_count(self) -> int:
         return int(_native.lib().fftconv_b200_last_launch_count(self._h))
 

@@ -88,3 +88,52 @@ def test_sharded_ops_world2_gloo():
     assert oracle.max_rel_error(gx, gx_full) < 1e-13
     for r in res:  # every rank holds the all-reduced gradient
         assert oracle.max_rel_error(r[5], gw_full) < 1e-12
+
+
+class OracleWorkspace32(OracleWorkspace):
+    """fp32 results like the B200 workspace (an empty shard contributes fp32 zeros)."""
+
+    def grad_weight(self, gy, x):
+        return oracle.grad_weight_fft(gy, x).astype(np.float32)
+
+
+def _worker_empty(rank, world, port, q):
+    """S = 1 over two ranks: rank 1's shard is empty."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        x, w, gy = _inputs()
+        x, gy = x[:1], gy[:1]
+        b0, b1 = shard_range(1, world, rank)
+        sc = ShardedConv(OracleWorkspace32())
+        y = sc.forward(x[b0:b1], w)
+        gx = sc.grad_input(gy[b0:b1], w)
+        gw = sc.grad_weight(gy[b0:b1], x[b0:b1])
+        q.put((rank, b0, b1, y.shape, gx.shape, gw.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(180)
+def test_sharded_empty_shard_world2_gloo():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_empty, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=150) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    x, w, gy = _inputs()
+    gw_full = oracle.grad_weight_fft(gy[:1], x[:1])
+    k, n, f, fo, S = CFG
+    no = n - k + 1
+    assert [r[1:3] for r in res] == [(0, 1), (1, 1)]
+    assert res[0][3] == (1, fo, no, no) and res[1][3] == (0, fo, no, no)
+    assert res[1][4] == (0, f, n, n)
+    for r in res:
+        assert oracle.max_rel_error(r[5], gw_full) < 1e-6
