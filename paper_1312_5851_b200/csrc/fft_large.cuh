@@ -431,11 +431,19 @@ __device__ __forceinline__ void c2r128_col_class(const C2RParams& p, const float
   const bool accum = p.accum;
   const long long step = 4LL * crop;
   float* d = o + (long long)C * crop;  // walks rows y = 4k + C
-  static_for<0, 32>([&](auto K) {
-    constexpr int k = decltype(K)::value;
-    if (4 * k + C < crop) *d = accum ? *d + scale * z[k].x : scale * z[k].x;
-    d += step;
-  });
+  if (accum) {  // branch outside the stores: no speculative loads of *d
+    static_for<0, 32>([&](auto K) {
+      constexpr int k = decltype(K)::value;
+      if (4 * k + C < crop) *d += scale * z[k].x;
+      d += step;
+    });
+  } else {
+    static_for<0, 32>([&](auto K) {
+      constexpr int k = decltype(K)::value;
+      if (4 * k + C < crop) *d = scale * z[k].x;
+      d += step;
+    });
+  }
 }
 
 // grid = rows * J (one plane per CTA), block = 256 = (column x', class

@@ -447,6 +447,34 @@ __global__ void __launch_bounds__(TR2C<M>::THREADS, 1)
 //                  and refills the stage once the stores have read it.
 //                  Planes that are not 16-B aligned (odd crops) are stored
 //                  directly from registers instead (EMPTY[s] after the reads).
+// K4 output-tile plane stride in floats: >= crop^2, a multiple of 4 (16-B
+// aligned bulk-store sources) with an odd quotient.
+__host__ __device__ constexpr int tile_plane_stride(int crop) {
+  return ((crop * crop + 3) / 4 % 2 == 0) ? ((crop * crop + 3) / 4 + 1) * 4 : (crop * crop + 3) / 4 * 4;
+}
+
+// Stores jv staged planes (tile plane stride pst floats, pe floats each)
+// to out + jl * out_sj with consecutive threads on consecutive floats of a
+// plane; accum adds into the output.
+__device__ __forceinline__ void c2r_store_tile(const float* tile, int pst, int jv, int pe, float* out,
+                                               long long out_sj, int accum, int t, int nthreads) {
+  // separate loops: with `v + (accum ? *d : 0)` the compiler may hoist the
+  // load of *d (the store proves it valid), putting an HBM round trip in
+  // front of every store (measured: accGrad's K4 pass 2 took 4-6k cycles)
+  if (accum) {
+    for (int e = t; e < jv * pe; e += nthreads) {
+      const int jl = e / pe, rem = e - jl * pe;
+      float* d = out + jl * out_sj + rem;
+      *d += tile[jl * pst + rem];
+    }
+  } else {
+    for (int e = t; e < jv * pe; e += nthreads) {
+      const int jl = e / pe, rem = e - jl * pe;
+      out[jl * out_sj + rem] = tile[jl * pst + rem];
+    }
+  }
+}
+
 template <int M>
 struct TC2R {
   static constexpr bool BIG = (M == 64);
@@ -473,7 +501,7 @@ struct TC2R {
   // FFT per column (pair) that would leave most pass-2 threads idle
   static constexpr int DFT_MAX_ITEMS = 4;  // per pass-2 thread
   static constexpr uint32_t BOX_BYTES = 2 * G * 4 * M;  // one u row
-  static_assert(G * M * M * 4 <= STAGE, "a staged output tile must fit a stage");
+  static_assert(G * tile_plane_stride(M) * 4 <= STAGE, "a staged output tile must fit a stage");
 };
 
 // tm: 3-D fp32 map over the product spectrum P[t][r][2*ld] with box
@@ -493,6 +521,10 @@ __global__ void __launch_bounds__(TC2R<M>::THREADS, 1)
   const int ngroups = p.R * ngj;
   const int crop = p.crop;
   const bool dft2 = crop <= M / 4 && G * crop * crop <= T::DFT_MAX_ITEMS * T::P2W;
+  // output-tile plane stride (floats): 16-B aligned for the bulk stores and
+  // an odd number of 16-B units, so the plane-fastest pass-2 lanes spread
+  // over the banks (a 32 x 32 crop at stride 1024 put 16 planes on one bank)
+  const int pst = tile_plane_stride(crop);
   if (threadIdx.x == 32)
     static_for<0, M>([&](auto K) { twt[decltype(K)::value] = tw128c<true, decltype(K)::value * (128 / M)>(); });
   if (threadIdx.x == 0) {
@@ -514,6 +546,7 @@ __global__ void __launch_bounds__(TC2R<M>::THREADS, 1)
     if (threadIdx.x == 0) {
       const uint64_t pol = l2_policy_evict_first();
       const uint32_t plane_bytes = (uint32_t)(crop * crop) * 4u;
+      const uint32_t tile_stride = (uint32_t)pst * 4u;
       auto issue_load = [&](int i) {
         const int g = blockIdx.x + i * gridDim.x;
         if (g >= ngroups) return;
@@ -544,7 +577,7 @@ __global__ void __launch_bounds__(TC2R<M>::THREADS, 1)
           if (FCB_XFORM_EXP != 2)
             for (int jl = 0; jl < jv; ++jl)
               bulk_store(p.out + (long long)r * p.out_sr + (long long)(j0 + jl) * p.out_sj,
-                         tile + jl * plane_bytes, plane_bytes);
+                         tile + jl * tile_stride, plane_bytes);
           bulk_commit_group();
           constexpr int D = stores_inflight(S);
           if (i >= D) {  // group i-D's stores have read their tile: refill its stage
@@ -631,17 +664,20 @@ __global__ void __launch_bounds__(TC2R<M>::THREADS, 1)
       mbar_wait(&mid[s], (i / S) & 1);
       if (dft2) {
         // x[y] = Re Z[0] + (-1)^y Re Z[M/2] + 2 sum_{0<u<M/2} Re(Z[u] e^(2 pi i u y / M))
-        // (the imaginary parts of Z[0] and Z[M/2] are dropped, as c2r does);
-        // items y-major so a warp shares few y (twiddle-table broadcasts)
-        const int per_y = jv * crop, items = per_y * crop;
+        // (the imaginary parts of Z[0] and Z[M/2] are dropped, as c2r does).
+        // Items (plane, y, c) with the plane fastest: a half-warp reads one
+        // (y, c) of G planes -- distinct banks (odd plane stride PS) -- and
+        // shares y (twiddle-table broadcasts).  Measured: the column-fastest
+        // order hit 3-4-way bank conflicts and bounded accGrad's K4.
+        const int items = G * crop * crop;
         float res[T::DFT_MAX_ITEMS];
 #pragma unroll
         for (int q = 0; q < T::DFT_MAX_ITEMS; ++q) {
           const int it = t + q * T::P2W;
           res[q] = 0.f;
-          if (it < items) {
-            const int y = it / per_y, rem = it - y * per_y;
-            const int jl = rem / crop, c = rem - jl * crop;
+          const int jl = it % G, rest = it / G;
+          if (it < items && jl < jv) {
+            const int y = rest / crop, c = rest - y * crop;
             const float2* col = inter + jl * PS + c;
             float acc = 0.f;
             static_for<1, M / 2>([&](auto U) {
@@ -654,40 +690,35 @@ __global__ void __launch_bounds__(TC2R<M>::THREADS, 1)
             res[q] = (e + 2.f * acc) * scale;
           }
         }
-        if (p.bulk) {
-          named_bar_sync(1 + T::NPIPE + pipe, T::P2W);  // stage read: reuse it as the output tile
-          float* tile = reinterpret_cast<float*>(smem + s * T::STAGE);
+        named_bar_sync(1 + T::NPIPE + pipe, T::P2W);  // stage read: reuse it as the output tile
+        float* tile = reinterpret_cast<float*>(smem + s * T::STAGE);
 #pragma unroll
-          for (int q = 0; q < T::DFT_MAX_ITEMS; ++q) {
-            const int it = t + q * T::P2W;
-            if (it < items) {
-              const int y = it / per_y, rem = it - y * per_y;
-              const int jl = rem / crop, c = rem - jl * crop;
-              tile[jl * crop * crop + y * crop + c] = res[q];
-            }
-          }
+        for (int q = 0; q < T::DFT_MAX_ITEMS; ++q) {
+          const int it = t + q * T::P2W;
+          const int jl = it % G, rest = it / G;
+          if (it < items && jl < jv) tile[jl * pst + rest] = res[q];
+        }
+        if (p.bulk) {
           fence_proxy_async_smem();
           mbar_arrive(&outb[s]);
         } else {
+          // coalesced stores of the jv cropped planes (each crop*crop floats
+          // contiguous in HBM), accumulating when asked
+          named_bar_sync(1 + T::NPIPE + pipe, T::P2W);
+          c2r_store_tile(tile, pst, jv, crop * crop, p.out + (long long)r * p.out_sr + (long long)j0 * p.out_sj,
+                         p.out_sj, p.accum, t, T::P2W);
+          named_bar_sync(1 + T::NPIPE + pipe, T::P2W);  // every tile read: the stage may be refilled
           mbar_arrive(&empty[s]);
-#pragma unroll
-          for (int q = 0; q < T::DFT_MAX_ITEMS; ++q) {
-            const int it = t + q * T::P2W;
-            if (it < items) {
-              const int y = it / per_y, rem = it - y * per_y;
-              const int jl = rem / crop, c = rem - jl * crop;
-              float* d = p.out + (long long)r * p.out_sr + (long long)(j0 + jl) * p.out_sj + y * crop + c;
-              *d = res[q] + (p.accum ? *d : 0.f);
-            }
-          }
         }
         if (t == 0) XTRACE(4, i);
       } else if constexpr (!T::BIG) {
-        // (plane, column-pair) items packed densely over the valid planes;
-        // columns (c, c + H) form one complex inverse FFT
+        // (plane, column-pair) items, columns (c, c + H) forming one complex
+        // inverse FFT, with the plane fastest: a half-warp reads one column
+        // of G planes (odd plane stride PS: distinct banks; the column-fastest
+        // order had 2-3-way conflicts)
         const int H = (crop + 1) >> 1;
-        const bool act = t < jv * H;
-        const int jl = act ? t / H : 0, c = t - jl * H;
+        const int jl = t % G, c = t / G;
+        const bool act = jl < jv && c < H;
         const bool hb = c + H < crop;
         float2 zz[M];
         {
@@ -704,37 +735,31 @@ __global__ void __launch_bounds__(TC2R<M>::THREADS, 1)
             if constexpr (uu != 0 && 2 * uu != M) zz[M - uu] = make_float2(a.x + b.y, b.x - a.y);
           });
         }
-        if (p.bulk) {
-          named_bar_sync(1 + T::NPIPE + pipe, T::P2W);  // stage read: reuse it as the output tile
-          if (act) {
-            if (FCB_XFORM_EXP != 1) fft_reg<M, true>(zz);
-            float* tile = reinterpret_cast<float*>(smem + s * T::STAGE) + jl * crop * crop + c;
+        named_bar_sync(1 + T::NPIPE + pipe, T::P2W);  // stage read: reuse it as the output tile
+        if (t == 0) XTRACE(3, i);
+        if (act) {
+          if (FCB_XFORM_EXP != 1) fft_reg<M, true>(zz);
+          float* tile = reinterpret_cast<float*>(smem + s * T::STAGE) + jl * pst + c;
 #pragma unroll
-            for (int row = 0; row < M; ++row) {
-              if (row < crop) {
-                tile[0] = zz[row].x * scale;
-                if (hb) tile[H] = zz[row].y * scale;
-              }
-              tile += crop;
+          for (int row = 0; row < M; ++row) {
+            if (row < crop) {
+              tile[0] = zz[row].x * scale;
+              if (hb) tile[H] = zz[row].y * scale;
             }
+            tile += crop;
           }
+        }
+        if (p.bulk) {
           fence_proxy_async_smem();  // the tile is read by the bulk store (async proxy)
           mbar_arrive(&outb[s]);
-        } else {
-          mbar_arrive(&empty[s]);  // operands in registers: the stage may be refilled
-          if (t == 0) XTRACE(3, i);
-          if (act) {
-            if (FCB_XFORM_EXP != 1) fft_reg<M, true>(zz);
-            float* dst = p.out + (long long)r * p.out_sr + (long long)(j0 + jl) * p.out_sj + c;
-#pragma unroll
-            for (int row = 0; row < M; ++row) {
-              if (row < crop && FCB_XFORM_EXP != 2) {
-                dst[0] = zz[row].x * scale + (p.accum ? dst[0] : 0.f);
-                if (hb) dst[H] = zz[row].y * scale + (p.accum ? dst[H] : 0.f);
-              }
-              dst += crop;
-            }
-          }
+        } else {  // unaligned planes / accumulate: coalesced stores from the tile
+          named_bar_sync(1 + T::NPIPE + pipe, T::P2W);
+          if (FCB_XFORM_EXP != 2)
+            c2r_store_tile(reinterpret_cast<const float*>(smem + s * T::STAGE), pst, jv, crop * crop,
+                           p.out + (long long)r * p.out_sr + (long long)j0 * p.out_sj, p.out_sj, p.accum, t,
+                           T::P2W);
+          named_bar_sync(1 + T::NPIPE + pipe, T::P2W);  // every tile read: the stage may be refilled
+          mbar_arrive(&empty[s]);
         }
         if (t == 0) XTRACE(4, i);
       } else {
@@ -765,7 +790,7 @@ __global__ void __launch_bounds__(TC2R<M>::THREADS, 1)
           named_bar_sync(1 + T::NPIPE + pipe, T::P2W);
           if (act) {
             if (FCB_XFORM_EXP != 1) fft_reg<H, true>(z);
-            float* tile = reinterpret_cast<float*>(smem + s * T::STAGE) + jl * crop * crop + c;
+            float* tile = reinterpret_cast<float*>(smem + s * T::STAGE) + jl * pst + c;
 #pragma unroll
             for (int i2 = 0; i2 < H; ++i2) {
               if (2 * i2 < crop) tile[(2 * i2) * crop] = z[i2].x * scale;
@@ -783,8 +808,13 @@ __global__ void __launch_bounds__(TC2R<M>::THREADS, 1)
             for (int i2 = 0; i2 < H; ++i2) {
               float* d0 = dst + (2 * i2) * crop;
               float* d1 = d0 + crop;
-              if (2 * i2 < crop) *d0 = z[i2].x * scale + (p.accum ? *d0 : 0.f);
-              if (2 * i2 + 1 < crop) *d1 = z[i2].y * scale + (p.accum ? *d1 : 0.f);
+              if (p.accum) {
+                if (2 * i2 < crop) *d0 += z[i2].x * scale;
+                if (2 * i2 + 1 < crop) *d1 += z[i2].y * scale;
+              } else {
+                if (2 * i2 < crop) *d0 = z[i2].x * scale;
+                if (2 * i2 + 1 < crop) *d1 = z[i2].y * scale;
+              }
             }
           }
         }

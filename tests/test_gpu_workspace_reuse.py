@@ -29,13 +29,13 @@ def _fft64(x, w, gy):
 @pytest.mark.parametrize("kind", ["f16x3", "auto", "tf32x3"])
 def test_more_operand_rows_than_registered(dev, kind):
     """Registered: n=64, f=f'=32, S=16 (32 operand rows).  Called: n=16,
-    S=200, f=f'=40 -- inside every capacity, but 200 rows of K1 per-row
+    S=150, f=f'=40 -- inside every capacity, but 150 rows of K1 per-row
     maxima: the words grow instead of overrunning."""
     import torch
 
     ws = ConvWorkspace([LayerConfig(5, 64, 32, 32, 16)])
     ws.set_gemm_kind(kind)
-    cfg = LayerConfig(5, 16, 40, 40, 200)
+    cfg = LayerConfig(5, 16, 40, 40, 150)
     x, w, gy = _inputs(cfg, 41)
     x[7] *= 1e3  # one sample far larger than the rest: row maxima matter
     xd, wd, gyd = (torch.from_numpy(a).to(dev) for a in (x, w, gy))
