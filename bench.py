@@ -153,8 +153,8 @@ def run_reference_arm(args, cfg, label):
         "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference fill_uniform, seed 1234)",
-        "config": {"workload": label, "k": k, "n": n, "f": f, "f_prime": fo, "S": S,
-                   "parallelism": "reference CPU (std::thread parallel_for)"},
+        "config": {"workload": label, "k": k, "n": n, "f": f, "f_prime": fo, "S": S},
+        "run": {"parallelism": f"reference CPU (std::thread parallel_for, {threads} threads)"},
         "impl": "reference",
         "tflops_equiv": 3 * E / (ms * 1e-3) / 1e12,
         "cpu_baseline": {"value": ms, "unit": "ms", "cores": threads, "kind": "reference",
@@ -181,7 +181,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--strong", action="store_true",
-                    help="N>1: split the S-sample minibatch across ranks (default: weak scaling, S per rank)")
+                    help="N>1: split the S-sample minibatch across ranks (the default; kept for compatibility)")
+    ap.add_argument("--weak", action="store_true",
+                    help="N>1: weak scaling instead -- every rank holds a full S-sample shard of an N*S minibatch")
+    ap.add_argument("--chunks", type=int, default=4,
+                    help="N>1: f'-chunks of accGrad's c2r, each all-reduced while the next transforms")
     ap.add_argument("--dist-backend", default="nccl",
                     help="nccl (one GPU per rank); gloo lets ranks share a GPU for testing")
     args = ap.parse_args()
@@ -209,16 +213,21 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         if args.dist_backend == "nccl":
+            # NCCL init lines in the log (nranks / NVLink / NVLS) for the driver
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(args.dist_backend)
 
     k, n, f, fo, S = cfg
     no = n - k + 1
-    # Weak scaling (default): every rank holds a full S-sample shard of an
-    # N*S-sample minibatch (per-GPU work fixed; gw all-reduced).  --strong:
-    # the S-sample minibatch itself is split across the ranks.
-    S_glob = S if (args.strong or world == 1) else S * world
+    # Strong scaling (default, BASELINE configs[3] / the north star: "the
+    # minibatch S is sharded across the GPUs"): the S-sample minibatch is
+    # split across the ranks.  --weak: every rank holds a full S-sample shard
+    # of an N*S-sample minibatch (per-GPU work fixed).
+    weak = args.weak and world > 1
+    S_glob = S * world if weak else S
     b0, b1 = shard_range(S_glob, world, rank)
     Sl = b1 - b0
     lcfg = LayerConfig(k, n, f, fo, Sl)
@@ -232,13 +241,19 @@ def main():
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
+    sc = None
+    if world > 1:
+        from paper_1312_5851_b200.sharded import NcclComm, ShardedConv
+
+        # accGrad's gw all-reduce through the library (NCCL, chunked behind
+        # the c2r); gloo (ranks sharing a GPU in tests) reduces via torch
+        comm = NcclComm(local) if args.dist_backend == "nccl" else None
+        sc = ShardedConv(ws, comm=comm, chunks=args.chunks)
+
     def step(reduce=True):
-        y = ws.forward(xd, wd)
-        gx = ws.grad_input(gyd, wd)
-        gw = ws.grad_weight(gyd, xd)
-        if world > 1 and reduce:
-            dist.all_reduce(gw)
-        return y, gx, gw
+        if sc is not None and reduce:
+            return sc.forward(xd, wd), sc.grad_input(gyd, wd), sc.grad_weight(gyd, xd)
+        return ws.forward(xd, wd), ws.grad_input(gyd, wd), ws.grad_weight(gyd, xd)
 
     # warm-up (also brings clocks up)
     for _ in range(args.warmup):
@@ -305,6 +320,37 @@ def main():
             fn()
             stage[op].append(ws.stage_ms())
             gemm_path[op] = ws.last_gemm_path() or "tf32x3"
+    comm_stats = None
+    if sc is not None:
+        # the sharded accGrad: collective span, the part not hidden behind the
+        # chunked c2r, and the whole sharded op (all ranks run the same count)
+        spans, exposed, op_ms = [], [], []
+        for _ in range(5):
+            flush.fill_(2.0)
+            dist.barrier()
+            torch.cuda.synchronize()
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record(stream)
+            sc.grad_weight(gyd, xd)
+            b_.record(stream)
+            torch.cuda.synchronize()
+            op_ms.append(a_.elapsed_time(b_))
+            if sc.comm is not None:
+                sp, ex = sc.comm_ms()
+                spans.append(sp)
+                exposed.append(ex)
+        t = torch.tensor([statistics.mean(op_ms), statistics.mean(spans) if spans else 0.0,
+                          statistics.mean(exposed) if exposed else 0.0], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sharded_ms, ar_ms, ar_exposed = (float(v) for v in t.tolist())
+        comm_stats = {"grad_weight_sharded_ms": sharded_ms, "allreduce_ms": ar_ms if sc.comm else None,
+                      "allreduce_exposed_ms": ar_exposed if sc.comm else None,
+                      "allreduce_hidden_frac": (1.0 - ar_exposed / ar_ms) if (sc.comm and ar_ms > 0) else None,
+                      "allreduce_bytes": 4 * fo * f * k * k, "chunks": args.chunks,
+                      "path": ("fftconv_b200_grad_weight_sharded: c2r in f'-chunks, each chunk's gw rows "
+                               "ncclAllReduce'd on a side stream (library-owned communicator)")
+                      if sc.comm else "torch.distributed all_reduce of gw (gloo)",
+                      "max_over_ranks": True}
     ws.set_stage_timing(False)
     stage_ms = {op: [statistics.mean(v[i] for v in stage[op]) for i in range(4)] for op in OPS}
 
@@ -457,12 +503,13 @@ def main():
     line = {
         "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": False,
-        "scaling": "strong" if (args.strong or world == 1) else "weak", "vs_baseline": None, "dtype": "f32",
+        "scaling": "weak" if weak else "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (reference fill_uniform, seed 1234)",
-        "config": {"workload": label, "k": k, "n": n, "f": f, "f_prime": fo, "S": S, "global_batch": S_glob,
-                   "S_per_gpu": Sl,
-                   "parallelism": f"dp{world} (minibatch-sharded, NCCL all-reduce of gw)" if world > 1 else "dp1",
-                   "l2": "flushed between timed steps (256 MiB write)"},
+        # the workload only (identical in both arms); how it ran is in "run"
+        "config": {"workload": label, "k": k, "n": n, "f": f, "f_prime": fo, "S": S_glob},
+        "run": {"global_batch": S_glob, "S_per_gpu": Sl,
+                "parallelism": f"dp{world} (minibatch-sharded, NCCL all-reduce of gw)" if world > 1 else "dp1",
+                "l2": "flushed between timed steps (256 MiB write)"},
         "tflops_equiv": 3 * E / (ms * 1e-3) / 1e12,
         "gemm_kind": kind,
         "gemm_path": gemm_path,
@@ -471,6 +518,7 @@ def main():
         "pass_roofline": pass_roof,
         "stages": stages,
         "gpu_launches": launches_per_step * args.steps,
+        "multi_gpu": comm_stats,
         "clocks": clocks,
         "e2e": e2e,
         "cpu_baseline": cpu,

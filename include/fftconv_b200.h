@@ -42,7 +42,7 @@ enum fftconv_b200_status {
   FFTCONV_B200_CAPACITY_ERROR = 4, /* fftconv::capacity_error */
   FFTCONV_B200_PLAN_ERROR = 5,     /* fftconv::plan_error     */
   FFTCONV_B200_CUDA_ERROR = 6,     /* CUDA runtime/driver failure */
-  FFTCONV_B200_NCCL_ERROR = 7,     /* reserved: collective failure */
+  FFTCONV_B200_NCCL_ERROR = 7,     /* NCCL missing or a collective failed */
   FFTCONV_B200_INVALID_ARGUMENT = 8
 };
 
@@ -131,6 +131,35 @@ int fftconv_b200_grad_input(fftconv_b200_ws* ws, const float* gy, size_t S, size
 int fftconv_b200_grad_weight(fftconv_b200_ws* ws, const float* gy, size_t S_gy, size_t fo,
                              size_t gy_rows, size_t gy_cols, const float* x, size_t S_x,
                              size_t f, size_t x_rows, size_t x_cols, float* gw, void* stream);
+
+/* ---- Minibatch-sharded accGrad (BASELINE configs[3] / [4]) ----------------
+ * fprop and bprop of a minibatch shard are the plain device entry points on
+ * the shard (no communication; batch decomposability, conv_direct_test.cpp:
+ * 186-212).  accGrad's weight gradient is the sum over shards:
+ * fftconv_b200_grad_weight_sharded runs the local grad_weight (conv_fft.hpp:
+ * 154-206) with its final c2r/crop stage in `chunks` f'-row chunks and
+ * all-reduces (sum) each chunk's rows of gw over `comm` (an ncclComm_t) on
+ * an internal stream as soon as that chunk's launch finishes, so the
+ * collective overlaps the remaining chunks.  `stream` waits for the last
+ * all-reduce: on return-and-sync every rank holds the full-batch gradient.
+ * A rank whose shard is empty (S_gy == S_x == 0, world > S) contributes
+ * zeros.  NCCL is loaded at run time (libnccl.so.2); FFTCONV_B200_NCCL_ERROR
+ * if it is missing or a collective fails.
+ * The three helpers create the communicator without linking NCCL: rank 0
+ * gets a 128-byte unique id, the caller distributes it (MPI, torch.distributed
+ * ...), every rank creates its communicator on its device. */
+int fftconv_b200_nccl_get_unique_id(void* id /* 128 bytes */);
+int fftconv_b200_nccl_comm_create(const void* id, int nranks, int rank, int device, void** comm);
+int fftconv_b200_nccl_comm_destroy(void* comm);
+int fftconv_b200_grad_weight_sharded(fftconv_b200_ws* ws, const float* gy, size_t S_gy, size_t fo,
+                                     size_t gy_rows, size_t gy_cols, const float* x, size_t S_x, size_t f,
+                                     size_t x_rows, size_t x_cols, float* gw, void* comm, int chunks,
+                                     void* stream);
+/* With stage timing enabled, the last sharded call's all-reduce timing (ms):
+ * out[0] = first all-reduce start -> last all-reduce end (collective span),
+ * out[1] = end of the local transforms -> last all-reduce end (the part not
+ * hidden behind the chunked c2r). */
+int fftconv_b200_comm_ms(fftconv_b200_ws* ws, float out[2]);
 
 /* ---- Host-pointer operators (the drop-in: Tensor4/Weights4 storage) ------
  * Same contracts; inputs are copied host->device, the result device->host,

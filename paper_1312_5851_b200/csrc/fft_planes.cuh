@@ -435,6 +435,12 @@ struct C2RParams {
   int bulk;     // 1: output planes 16-B aligned -> staged + bulk-stored (K4 TMA kernel)
   int gm;       // 1: P is group-major P[r][J/16][t][16] (K4 TMA kernel, m <= 32)
   int accum;    // 1: add into the output (direct-store mode; chunked accGrad)
+  // column window (K4 TMA kernel): columns [jbase, jbase + J) of a product
+  // whose rows hold J_all columns; out points at column jbase's planes.
+  // Lets accGrad's K4 run in f'-chunks (each chunk's gw rows all-reduced
+  // while the next chunk transforms).  jbase is a multiple of the group size.
+  int jbase = 0;
+  int J_all = 0;  // 0: J
 };
 
 // grid = (ceil(J/G), R, ceil(crop/cc)), block = PlaneTraits<M>::THREADS.

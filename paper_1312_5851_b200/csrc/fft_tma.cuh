@@ -556,10 +556,12 @@ __global__ void __launch_bounds__(TC2R<M>::THREADS, 1)
         mbar_arrive_expect_tx(&full[s], PC * T::BOX_BYTES);
         uint8_t* st = smem + s * T::STAGE;
         if (p.gm) {  // group-major product: the group is one contiguous block
-          const float* src = p.in + (long long)(r * ngj + j0 / G) * (PC * T::BOX_BYTES / 4);
+          const int ngj_all = p.J_all ? (p.J_all + G - 1) / G : ngj;
+          const float* src = p.in + (long long)(r * ngj_all + (p.jbase + j0) / G) * (PC * T::BOX_BYTES / 4);
           bulk_load(st, src, PC * T::BOX_BYTES, &full[s], pol);
         } else {
-          for (int u = 0; u < PC; ++u) tma_load_3d_hint(st + u * RS * 8, &tm, &full[s], 2 * j0, r, u * M, pol);
+          for (int u = 0; u < PC; ++u)
+            tma_load_3d_hint(st + u * RS * 8, &tm, &full[s], 2 * (p.jbase + j0), r, u * M, pol);
         }
       };
 #pragma unroll 1

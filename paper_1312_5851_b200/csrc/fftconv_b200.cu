@@ -10,6 +10,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: libnccl is loaded at run time (nccl_api)
 
 #include <algorithm>
 #include <cstdint>
@@ -17,6 +19,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <atomic>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <unordered_map>
@@ -578,6 +581,51 @@ __global__ void conj_inplace_kernel(float2* v, long long n) {
 
 using namespace fcb;
 
+// ------------------------------------------------------------ NCCL (run-time loaded)
+// The product does not link NCCL: the sharded entry points dlopen
+// libnccl.so.2 on first use (inside a torch process that is torch's own
+// NCCL, already loaded under that soname), so single-GPU users never need it.
+namespace fcb {
+struct NcclApi {
+  decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+  decltype(&ncclCommInitRank) comm_init_rank = nullptr;
+  decltype(&ncclCommDestroy) comm_destroy = nullptr;
+  decltype(&ncclAllReduce) all_reduce = nullptr;
+  decltype(&ncclGetErrorString) error_string = nullptr;
+  std::string why;
+};
+
+static const NcclApi& nccl_api() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      const char* e = dlerror();
+      api.why = e ? e : "dlopen failed";
+      return;
+    }
+    api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+    api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(dlsym(h, "ncclAllReduce"));
+    api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
+    if (!api.get_unique_id || !api.comm_init_rank || !api.comm_destroy || !api.all_reduce || !api.error_string)
+      api.why = "libnccl.so.2 lacks an expected symbol";
+  });
+  if (!api.why.empty()) throw Error(FFTCONV_B200_NCCL_ERROR, "NCCL unavailable: " + api.why);
+  return api;
+}
+
+#define FCB_NCCL(call)                                                                      \
+  do {                                                                                      \
+    ncclResult_t r_ = (call);                                                               \
+    if (r_ != ncclSuccess)                                                                  \
+      throw Error(FFTCONV_B200_NCCL_ERROR, std::string(#call) + ": " + nccl_api().error_string(r_)); \
+  } while (0)
+}  // namespace fcb
+
 // ------------------------------------------------------------ workspace
 constexpr int kMaxChunks = 16;
 
@@ -618,6 +666,14 @@ struct fftconv_b200_ws {
   cudaEvent_t done_ev = nullptr;
   cudaStream_t last_st = nullptr;
   bool has_last = false;
+  // sharded accGrad: the all-reduces run on comm_stream, each after the K4
+  // chunk that wrote its rows (chunk_ev); comm_ev[0..2] time them (K4 end on
+  // the compute stream, first all-reduce start, last all-reduce end)
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t chunk_ev[kMaxChunks + 1] = {};
+  cudaEvent_t comm_ev[3] = {};
+  bool comm_ready = false;
+  bool comm_timed = false;
   std::string last_error;
   bool timing = false;
   cudaEvent_t ev[5] = {};
@@ -890,9 +946,17 @@ void run_grad_input(fftconv_b200_ws* ws, const float* gy, size_t S, size_t fo, s
   ws->ctr[2] += (uint64_t)bins * fo * f * S;
 }
 
+// accGrad's K4 in f'-chunks: `done(o0, o1, st)` runs after the launch that
+// wrote gw rows [o0, o1) (the sharded entry point all-reduces them there,
+// overlapping the next chunk's transforms).
+struct ChunkHook {
+  int chunks = 1;
+  std::function<void(size_t, size_t, cudaStream_t)> done;
+};
+
 void run_grad_weight(fftconv_b200_ws* ws, const float* gy, size_t Sg, size_t fo, size_t gr,
                      size_t gc, const float* x, size_t Sx, size_t f, size_t xr, size_t xc,
-                     float* gw, cudaStream_t st, bool accum = false) {
+                     float* gw, cudaStream_t st, bool accum = false, const ChunkHook* hook = nullptr) {
   require_nonzero(Sg, fo, gr, gc, "Tensor4");
   require_nonzero(Sx, f, xr, xc, "Tensor4");
   if (gr != gc) throw Error(FFTCONV_B200_SIZE_ERROR, "grad_weight_fft: planes must be square");
@@ -923,7 +987,27 @@ void run_grad_weight(fftconv_b200_ws* ws, const float* gy, size_t Sg, size_t fo,
               0, 0, 1.0f / (float)(m * m), (int)round_up(fo, 2)};
   c.gm = c2r_layout(m) == kGroupMajor;
   c.accum = accum;
-  const int nc = c2r_run(ws, m, c, st);
+  int nc = 0;
+  // chunked only where the TMA K4 runs (m in 4..64); chunk edges on 16-plane
+  // group boundaries (the K4 group size at every such m divides 16)
+  const int nchunk = (hook && m >= 4 && m <= 64) ? (int)std::max<size_t>(1, std::min<size_t>(hook->chunks, (fo + 15) / 16)) : 1;
+  if (nchunk == 1) {
+    nc = c2r_run(ws, m, c, st);
+    if (hook && hook->done) hook->done(0, fo, st);
+  } else {
+    const size_t groups = (fo + 15) / 16;
+    for (int ci = 0; ci < nchunk; ++ci) {
+      const size_t o0 = std::min(fo, 16 * (groups * ci / nchunk)), o1 = std::min(fo, 16 * (groups * (ci + 1) / nchunk));
+      if (o1 <= o0) continue;
+      C2RParams cc = c;
+      cc.jbase = (int)o0;
+      cc.J = (int)(o1 - o0);
+      cc.J_all = (int)fo;
+      cc.out = gw + o0 * f * k * k;
+      nc += c2r_run(ws, m, cc, st);
+      if (hook->done) hook->done(o0, o1, st);
+    }
+  }
   record(ws, 4, st);
   ws->last_launches = nl + ng + nc;
   ws->ctr[0] += S * f + S * fo;
@@ -1014,6 +1098,11 @@ void fftconv_b200_ws_destroy(fftconv_b200_ws* ws) {
     if (ws->ev_ready)
       for (auto& e : ws->ev) cudaEventDestroy(e);
     if (ws->done_ev) cudaEventDestroy(ws->done_ev);
+    if (ws->comm_ready) {
+      cudaStreamDestroy(ws->comm_stream);
+      for (auto& e : ws->chunk_ev) cudaEventDestroy(e);
+      for (auto& e : ws->comm_ev) cudaEventDestroy(e);
+    }
   }
   delete ws;
 }
@@ -1104,6 +1193,107 @@ int fftconv_b200_grad_weight(fftconv_b200_ws* ws, const float* gy, size_t S_gy, 
     run_grad_weight(ws, gy, S_gy, fo, gy_rows, gy_cols, x, S_x, f, x_rows, x_cols, gw,
                     (cudaStream_t)stream);
     mark_done(ws, (cudaStream_t)stream);
+  });
+}
+
+// ---- minibatch-sharded accGrad (NCCL over NVLink) ----------------------
+
+int fftconv_b200_nccl_get_unique_id(void* id) {
+  return guarded(nullptr, [&] {
+    if (!id) throw Error(FFTCONV_B200_INVALID_ARGUMENT, "id is NULL");
+    ncclUniqueId u;
+    FCB_NCCL(nccl_api().get_unique_id(&u));
+    std::memcpy(id, &u, sizeof u);
+  });
+}
+
+int fftconv_b200_nccl_comm_create(const void* id, int nranks, int rank, int device, void** comm) {
+  return guarded(nullptr, [&] {
+    if (!id || !comm) throw Error(FFTCONV_B200_INVALID_ARGUMENT, "id / comm is NULL");
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw Error(FFTCONV_B200_INVALID_ARGUMENT, "bad nranks / rank");
+    *comm = nullptr;
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof u);
+    DeviceGuard g(device);
+    FCB_CUDA(cudaSetDevice(device));
+    ncclComm_t c = nullptr;
+    FCB_NCCL(nccl_api().comm_init_rank(&c, nranks, u, rank));
+    *comm = c;
+  });
+}
+
+int fftconv_b200_nccl_comm_destroy(void* comm) {
+  return guarded(nullptr, [&] {
+    if (comm) FCB_NCCL(nccl_api().comm_destroy(reinterpret_cast<ncclComm_t>(comm)));
+  });
+}
+
+int fftconv_b200_grad_weight_sharded(fftconv_b200_ws* ws, const float* gy, size_t S_gy, size_t fo,
+                                     size_t gy_rows, size_t gy_cols, const float* x, size_t S_x, size_t f,
+                                     size_t x_rows, size_t x_cols, float* gw, void* comm, int chunks,
+                                     void* stream) {
+  if (!ws) return FFTCONV_B200_INVALID_ARGUMENT;
+  return guarded(ws, [&] {
+    DeviceGuard g(ws->device);
+    const cudaStream_t st = (cudaStream_t)stream;
+    if (!comm) throw Error(FFTCONV_B200_INVALID_ARGUMENT, "grad_weight_sharded: comm is NULL");
+    const NcclApi& api = nccl_api();
+    if (!ws->comm_ready) {
+      FCB_CUDA(cudaStreamCreateWithFlags(&ws->comm_stream, cudaStreamNonBlocking));
+      for (auto& e : ws->chunk_ev) FCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      for (auto& e : ws->comm_ev) FCB_CUDA(cudaEventCreate(&e));
+      ws->comm_ready = true;
+    }
+    order_after_last(ws, st);
+    int ci = 0;
+    bool first = true;
+    auto reduce_rows = [&](size_t o0, size_t o1, size_t per_row, cudaStream_t s_) {
+      // the all-reduce of rows [o0, o1) waits for the launch that wrote them
+      FCB_CUDA(cudaEventRecord(ws->chunk_ev[ci], s_));
+      FCB_CUDA(cudaStreamWaitEvent(ws->comm_stream, ws->chunk_ev[ci], 0));
+      if (first && ws->timing) FCB_CUDA(cudaEventRecord(ws->comm_ev[1], ws->comm_stream));
+      first = false;
+      FCB_NCCL(api.all_reduce(gw + o0 * per_row, gw + o0 * per_row, (o1 - o0) * per_row, ncclFloat32, ncclSum,
+                              reinterpret_cast<ncclComm_t>(comm), ws->comm_stream));
+      ci = std::min(ci + 1, kMaxChunks);
+    };
+    if (S_gy == 0 && S_x == 0) {
+      // empty shard (world > S): contribute zeros so the peers' all-reduce completes
+      require_nonzero(fo, gy_rows, gy_cols, 1, "Tensor4");
+      require_nonzero(f, x_rows, x_cols, 1, "Tensor4");
+      if (gy_rows > x_rows) throw Error(FFTCONV_B200_SIZE_ERROR, "grad_weight_fft: gradient larger than input");
+      const size_t k = x_rows - gy_rows + 1;
+      FCB_CUDA(cudaMemsetAsync(gw, 0, fo * f * k * k * sizeof(float), st));
+      if (ws->timing) FCB_CUDA(cudaEventRecord(ws->comm_ev[0], st));
+      reduce_rows(0, fo, f * k * k, st);
+    } else {
+      const size_t k = (gy_rows <= x_rows) ? x_rows - gy_rows + 1 : 1;
+      ChunkHook hook;
+      hook.chunks = std::max(1, std::min(chunks, kMaxChunks));
+      hook.done = [&](size_t o0, size_t o1, cudaStream_t s_) { reduce_rows(o0, o1, f * k * k, s_); };
+      run_grad_weight(ws, gy, S_gy, fo, gy_rows, gy_cols, x, S_x, f, x_rows, x_cols, gw, st, false, &hook);
+      if (ws->timing) FCB_CUDA(cudaEventRecord(ws->comm_ev[0], st));  // K4 end
+    }
+    if (ws->timing) FCB_CUDA(cudaEventRecord(ws->comm_ev[2], ws->comm_stream));
+    // the caller's stream resumes once every row is reduced
+    FCB_CUDA(cudaEventRecord(ws->chunk_ev[kMaxChunks], ws->comm_stream));
+    FCB_CUDA(cudaStreamWaitEvent(st, ws->chunk_ev[kMaxChunks], 0));
+    ws->comm_timed = ws->timing;
+    mark_done(ws, st);
+  });
+}
+
+int fftconv_b200_comm_ms(fftconv_b200_ws* ws, float out[2]) {
+  if (!ws || !out) return FFTCONV_B200_INVALID_ARGUMENT;
+  return guarded(ws, [&] {
+    if (!ws->comm_timed) throw Error(FFTCONV_B200_INVALID_ARGUMENT, "no timed sharded call yet (enable stage timing)");
+    DeviceGuard g(ws->device);
+    FCB_CUDA(cudaEventSynchronize(ws->comm_ev[2]));
+    float span = 0.f, exposed = 0.f;
+    FCB_CUDA(cudaEventElapsedTime(&span, ws->comm_ev[1], ws->comm_ev[2]));
+    FCB_CUDA(cudaEventElapsedTime(&exposed, ws->comm_ev[0], ws->comm_ev[2]));
+    out[0] = span;
+    out[1] = std::max(0.f, exposed);
   });
 }
 

@@ -8,10 +8,22 @@ all-reduce of the *spatial* f'*f*k*k gradient (1.8 MB at the paper point,
 31.7 MB for the wide layer) -- reducing after the local c2r+crop moves 22-35x
 fewer bytes than reducing spectra.
 
-Works with any torch.distributed backend: NCCL over NVLink on the GPU box,
-gloo for the CPU tests.
+Two collective paths:
+
+* ``NcclComm`` + the C ABI (``fftconv_b200_grad_weight_sharded``, the
+  product path on GPUs): accGrad's final c2r runs in f'-row chunks and each
+  chunk's gw rows are all-reduced over NCCL / NVLink on a side stream while
+  the next chunk transforms.  The communicator is created by the library
+  from a unique id that rank 0 broadcasts over the torch.distributed group.
+* torch.distributed ``all_reduce`` of the finished gw (any backend; gloo for
+  the CPU tests and numpy operands).
 """
 from __future__ import annotations
+
+import ctypes as C
+
+from . import _native
+from .errors import raise_for_status
 
 
 def shard_range(S: int, world: int, rank: int):
@@ -33,17 +45,70 @@ def _empty_like_slice(t, shape):
     return np.empty(shape, dtype=np.float32)
 
 
+class NcclComm:
+    """An NCCL communicator owned by libfftconv_b200 (include/fftconv_b200.h,
+    fftconv_b200_nccl_comm_create): rank 0 draws the unique id, the
+    torch.distributed group broadcasts it, every rank joins on `device`."""
+
+    def __init__(self, device: int, group=None):
+        import torch.distributed as dist
+
+        L = _native.lib()
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        uid = (C.c_uint8 * 128)()
+        if self.rank == 0:
+            raise_for_status(L.fftconv_b200_nccl_get_unique_id(uid), _native.last_error(None))
+        box = [bytes(uid)]
+        dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                   group=group)
+        uid = (C.c_uint8 * 128).from_buffer_copy(box[0])
+        h = C.c_void_p()
+        raise_for_status(L.fftconv_b200_nccl_comm_create(uid, self.world, self.rank, int(device), C.byref(h)),
+                         _native.last_error(None))
+        self.handle = h
+
+    @classmethod
+    def single(cls, device: int):
+        """A one-rank communicator (no process group): the sharded entry point
+        on one GPU, as the tests use it."""
+        self = cls.__new__(cls)
+        L = _native.lib()
+        uid = (C.c_uint8 * 128)()
+        raise_for_status(L.fftconv_b200_nccl_get_unique_id(uid), _native.last_error(None))
+        h = C.c_void_p()
+        raise_for_status(L.fftconv_b200_nccl_comm_create(uid, 1, 0, int(device), C.byref(h)),
+                         _native.last_error(None))
+        self.handle, self.rank, self.world = h, 0, 1
+        return self
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _native.lib().fftconv_b200_nccl_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class ShardedConv:
     """fprop / bprop / accGrad of one layer with this rank's minibatch slice.
 
     `ws` is any object with the ConvWorkspace operator interface (the B200
     workspace on GPUs); `group` a torch.distributed process group (None =
-    default).
+    default).  With `comm` (an NcclComm) and CUDA operands, accGrad goes
+    through the library's chunked, overlapped all-reduce; otherwise through
+    torch.distributed.
     """
 
-    def __init__(self, ws, group=None):
+    def __init__(self, ws, group=None, comm: NcclComm | None = None, chunks: int = 4):
         self.ws = ws
         self.group = group
+        self.comm = comm
+        self.chunks = int(chunks)
 
     def forward(self, x_local, w):
         if int(x_local.shape[0]) == 0:  # empty shard: an empty slice of y
@@ -63,6 +128,8 @@ class ShardedConv:
         import torch
         import torch.distributed as dist
 
+        if self.comm is not None and isinstance(gy_local, torch.Tensor) and gy_local.is_cuda:
+            return self._grad_weight_nccl(gy_local, x_local)
         multi = dist.is_initialized() and dist.get_world_size(self.group) > 1
         if int(gy_local.shape[0]) == 0 and int(x_local.shape[0]) == 0:
             # empty shard (world > S): contribute zeros so the other ranks'
@@ -83,3 +150,27 @@ class ShardedConv:
                 gw = gw.to(torch.device("cuda", torch.cuda.current_device()))
             dist.all_reduce(gw, op=dist.ReduceOp.SUM, group=self.group)
         return gw
+
+    def _grad_weight_nccl(self, gy, x):
+        """conv_fft.hpp:154-206 over the whole sharded minibatch, via
+        fftconv_b200_grad_weight_sharded (include/fftconv_b200.h)."""
+        import torch
+
+        ws = self.ws
+        Sg, fo, gr, gc = (int(v) for v in gy.shape)
+        Sx, f, xr, xc = (int(v) for v in x.shape)
+        k = xr - gr + 1 if gr <= xr else 1
+        gw = torch.empty((fo, f, k, k), dtype=torch.float32, device=gy.device)
+        code = _native.lib().fftconv_b200_grad_weight_sharded(
+            ws._h, ws._dev_ptr(gy), Sg, fo, gr, gc, ws._dev_ptr(x), Sx, f, xr, xc,
+            ws._dev_ptr(gw), self.comm.handle, self.chunks,
+            C.c_void_p(torch.cuda.current_stream(gy.device).cuda_stream))
+        raise_for_status(code, _native.last_error(ws._h))
+        return gw
+
+    def comm_ms(self):
+        """(collective span, exposed) ms of the last timed sharded accGrad."""
+        out = (C.c_float * 2)()
+        code = _native.lib().fftconv_b200_comm_ms(self.ws._h, out)
+        raise_for_status(code, _native.last_error(self.ws._h))
+        return float(out[0]), float(out[1])

@@ -30,14 +30,17 @@ def test_bench_two_ranks_gloo():
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1  # rank 0 only
     line = json.loads(lines[0])
-    # weak scaling by default: each rank a full S=8 shard of a 16-sample minibatch
-    assert line["n_gpus"] == 2 and line["scaling"] == "weak" and line["value"] > 0
-    assert line["config"]["S_per_gpu"] == 8 and line["config"]["global_batch"] == 16
-    r = subprocess.run(cmd[:6] + [f"--master-port={_port()}"] + cmd[7:] + ["--strong"], capture_output=True,
+    # strong scaling by default (BASELINE configs[3]): the S=8 minibatch split 4 + 4
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong" and line["value"] > 0
+    assert line["run"]["S_per_gpu"] == 4 and line["run"]["global_batch"] == 8
+    assert line["config"]["S"] == 8
+    mg = line["multi_gpu"]
+    assert mg["grad_weight_sharded_ms"] > 0 and mg["max_over_ranks"]
+    r = subprocess.run(cmd[:6] + [f"--master-port={_port()}"] + cmd[7:] + ["--weak"], capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][0])
-    assert line["scaling"] == "strong" and line["config"]["S_per_gpu"] == 4
+    assert line["scaling"] == "weak" and line["run"]["S_per_gpu"] == 8 and line["run"]["global_batch"] == 16
 
 
 def test_sharded_grad_weight_matches_full_batch(dev):
