@@ -549,6 +549,8 @@ def run_stack(args):
                 else ("fc %d" % s.fc_outputs if s.kind == 3 else s.kind.name) for s in spec.stages),
                 "S": S, "parallelism": "dp1"}}
     if args.impl == "reference":
+        if int(os.environ.get("RANK", "0")) != 0:
+            return
         th = cpu_threads()
         t = []
         for _ in range(max(1, args.steps)):
@@ -562,36 +564,71 @@ def run_stack(args):
         print(json.dumps(line), flush=True)
         return
     import torch
+    import torch.distributed as dist
 
-    dev = torch.device("cuda", 0)
+    from paper_1312_5851_b200.sharded import NcclComm, shard_range
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    comm = None
+    if world > 1:
+        # data-parallel step (BASELINE configs[4] on N GPUs): the S-sample
+        # minibatch split over the ranks, every gradient summed
+        if args.dist_backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            dist.init_process_group("nccl", device_id=dev)
+            comm = NcclComm(local)
+        else:
+            dist.init_process_group(args.dist_backend)
+    b0, b1 = shard_range(S, world, rank)
     params = layers.init_params(spec, seed)
-    batch = torch.from_numpy(layers.make_batch(spec, S, seed)).to(dev)
-    ws = __import__("paper_1312_5851_b200").ConvWorkspace(spec.conv_configs(S), device=0)
+    batch = torch.from_numpy(np.ascontiguousarray(layers.make_batch(spec, S, seed)[b0:b1])).to(dev)
+    ws = __import__("paper_1312_5851_b200").ConvWorkspace(spec.conv_configs(b1 - b0), device=local)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     for _ in range(args.warmup):
-        layers.run_iteration(spec, params, batch, ws=ws)
+        layers.run_iteration(spec, params, batch, ws=ws, device=local, comm=comm)
     cats = {"update_output_ms": [], "update_grad_input_ms": [], "acc_grad_ms": []}
     wall, launches = [], []
-    sampler = ClockSampler(0)
+    sampler = ClockSampler(local)
     sampler.start()
     for i in range(args.steps):
         flush.fill_(float(i))
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
-        r = layers.run_iteration(spec, params, batch, ws=ws)
+        r = layers.run_iteration(spec, params, batch, ws=ws, device=local, comm=comm)
         wall.append((time.perf_counter() - t0) * 1e3)
         launches.append(r.gpu_launches)
         for k in cats:
             cats[k].append(getattr(r.times, k))
     clocks = sampler.stop()
     per = {k: statistics.mean(v) for k, v in cats.items()}
+    if world > 1:  # device times, max over ranks
+        t = torch.tensor([per[k] for k in cats], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        per = dict(zip(cats, (float(v) for v in t.tolist())))
+        base["n_gpus"] = world
+        base["config"]["parallelism"] = (f"dp{world} (minibatch-sharded; conv gw all-reduced by "
+                                         f"fftconv_b200_grad_weight_sharded behind the backward pass)")
+        base["run"] = {"S_per_gpu": b1 - b0, "global_batch": S}
     ms = sum(per.values())
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
     line = dict(base, value=ms, ms_per_step=ms, per_category_ms=per,
                 wall_ms_incl_param_upload=statistics.mean(wall), loss=r.loss, grad_checksum=r.grad_checksum,
                 clocks=clocks, gpu_launches=sum(launches),
                 note="value = device time of the three reference categories (CUDA events); conv stages on the "
                      "B200 kernels, relu/pool/fit_to on the layer-stack kernels, fc on fp32 cuBLAS")
     print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def ncu_traffic(kernel, config):

@@ -142,6 +142,12 @@ int fftconv_b200_grad_weight(fftconv_b200_ws* ws, const float* gy, size_t S_gy, 
  * an internal stream as soon as that chunk's launch finishes, so the
  * collective overlaps the remaining chunks.  `stream` waits for the last
  * all-reduce: on return-and-sync every rank holds the full-batch gradient.
+ * With flags & FFTCONV_B200_SHARDED_ASYNC the stream does not wait: the
+ * collective keeps running behind whatever the caller enqueues next (a
+ * training step's remaining backward layers; gw must not be read, and the
+ * next sharded call on this workspace orders itself after it) until
+ * fftconv_b200_comm_wait(ws, stream) makes `stream` wait for every
+ * all-reduce issued so far.
  * A rank whose shard is empty (S_gy == S_x == 0, world > S) contributes
  * zeros.  NCCL is loaded at run time (libnccl.so.2); FFTCONV_B200_NCCL_ERROR
  * if it is missing or a collective fails.
@@ -154,7 +160,9 @@ int fftconv_b200_nccl_comm_destroy(void* comm);
 int fftconv_b200_grad_weight_sharded(fftconv_b200_ws* ws, const float* gy, size_t S_gy, size_t fo,
                                      size_t gy_rows, size_t gy_cols, const float* x, size_t S_x, size_t f,
                                      size_t x_rows, size_t x_cols, float* gw, void* comm, int chunks,
-                                     void* stream);
+                                     unsigned flags, void* stream);
+#define FFTCONV_B200_SHARDED_ASYNC 1u
+int fftconv_b200_comm_wait(fftconv_b200_ws* ws, void* stream);
 /* With stage timing enabled, the last sharded call's all-reduce timing (ms):
  * out[0] = first all-reduce start -> last all-reduce end (collective span),
  * out[1] = end of the local transforms -> last all-reduce end (the part not

@@ -1231,7 +1231,7 @@ int fftconv_b200_nccl_comm_destroy(void* comm) {
 int fftconv_b200_grad_weight_sharded(fftconv_b200_ws* ws, const float* gy, size_t S_gy, size_t fo,
                                      size_t gy_rows, size_t gy_cols, const float* x, size_t S_x, size_t f,
                                      size_t x_rows, size_t x_cols, float* gw, void* comm, int chunks,
-                                     void* stream) {
+                                     unsigned flags, void* stream) {
   if (!ws) return FFTCONV_B200_INVALID_ARGUMENT;
   return guarded(ws, [&] {
     DeviceGuard g(ws->device);
@@ -1275,11 +1275,21 @@ int fftconv_b200_grad_weight_sharded(fftconv_b200_ws* ws, const float* gy, size_
       if (ws->timing) FCB_CUDA(cudaEventRecord(ws->comm_ev[0], st));  // K4 end
     }
     if (ws->timing) FCB_CUDA(cudaEventRecord(ws->comm_ev[2], ws->comm_stream));
-    // the caller's stream resumes once every row is reduced
+    // the caller's stream resumes once every row is reduced -- now, or (ASYNC)
+    // at fftconv_b200_comm_wait, so a training step's later layers overlap it
     FCB_CUDA(cudaEventRecord(ws->chunk_ev[kMaxChunks], ws->comm_stream));
-    FCB_CUDA(cudaStreamWaitEvent(st, ws->chunk_ev[kMaxChunks], 0));
+    if (!(flags & FFTCONV_B200_SHARDED_ASYNC)) FCB_CUDA(cudaStreamWaitEvent(st, ws->chunk_ev[kMaxChunks], 0));
     ws->comm_timed = ws->timing;
     mark_done(ws, st);
+  });
+}
+
+int fftconv_b200_comm_wait(fftconv_b200_ws* ws, void* stream) {
+  if (!ws) return FFTCONV_B200_INVALID_ARGUMENT;
+  return guarded(ws, [&] {
+    if (!ws->comm_ready) return;
+    DeviceGuard g(ws->device);
+    FCB_CUDA(cudaStreamWaitEvent((cudaStream_t)stream, ws->chunk_ev[kMaxChunks], 0));
   });
 }
 

@@ -335,11 +335,21 @@ def maxpool_backward(gy, rec):
 
 
 def run_iteration(spec: NetworkSpec, params: NetworkParams, batch, ws: ConvWorkspace | None = None,
-                  device: int = 0) -> IterationResult:
+                  device: int = 0, group=None, comm=None, chunks: int = 4) -> IterationResult:
     """One training iteration (layers.hpp:441-609) on the GPU.  `batch` is a
     host array or a CUDA tensor [S][maps][n][n]; parameters are host arrays
-    (copied to the device once per call, outside the timed categories)."""
+    (copied to the device once per call, outside the timed categories).
+
+    Data-parallel (BASELINE configs[4] on N GPUs): with torch.distributed
+    initialised and more than one rank in `group`, `batch` is this rank's
+    minibatch shard; the loss (a sum over samples) and every gradient are
+    summed over the ranks.  Each conv layer's weight gradient goes through
+    fftconv_b200_grad_weight_sharded when `comm` (a sharded.NcclComm) is
+    given -- chunked c2r, all-reduces on a side stream that overlap the rest
+    of the backward pass, one wait at the end -- otherwise through
+    torch.distributed all_reduce; the fc gradients through torch."""
     import torch
+    import torch.distributed as dist
 
     sh = spec.shape()
     if len(params.conv) != sh.conv_count:
@@ -352,6 +362,13 @@ def run_iteration(spec: NetworkSpec, params: NetworkParams, batch, ws: ConvWorks
     S = x.shape[0]
     if ws is None:
         ws = ConvWorkspace(spec.conv_configs(S), device=device)
+    multi = dist.is_available() and dist.is_initialized() and (dist.get_world_size(group) > 1 or comm is not None)
+    sharded = None
+    if multi and comm is not None:
+        from .sharded import ShardedConv
+
+        sharded = ShardedConv(ws, group=group, comm=comm, chunks=chunks)
+    raw_ws = ws
     ws = _CountingWorkspace(ws)
     _LAUNCHES[0] = 0
     w_dev = [torch.from_numpy(np.ascontiguousarray(w)).to(dev) for w in params.conv]
@@ -421,7 +438,14 @@ def run_iteration(spec: NetworkSpec, params: NetworkParams, batch, ws: ConvWorks
                 ci -= 1
                 fin, pre = conv_rec[ci]
                 g = grad
-                conv_grads[ci] = timed("acc_grad_ms", lambda g=g, fin=fin: ws.grad_weight(g, fin))
+                if sharded is not None:  # all-reduce overlaps the remaining backward layers
+                    def acc(g=g, fin=fin):
+                        r = sharded.grad_weight_async(g, fin)
+                        _launched(raw_ws.last_launch_count())
+                        return r
+                    conv_grads[ci] = timed("acc_grad_ms", acc)
+                else:
+                    conv_grads[ci] = timed("acc_grad_ms", lambda g=g, fin=fin: ws.grad_weight(g, fin))
                 if ci > 0:
                     grad = timed("update_grad_input_ms",
                                  lambda g=g, c=ci, pre=pre: fit_to(ws.grad_input(g, w_dev[c]), pre))
@@ -435,6 +459,20 @@ def run_iteration(spec: NetworkSpec, params: NetworkParams, batch, ws: ConvWorks
                 pi -= 1
                 grad = timed("update_grad_input_ms", lambda g=grad, r=pool_rec[pi]: maxpool_backward(g, r))
 
+        if multi:
+            def reduce_all():
+                if sharded is not None:
+                    sharded.wait()
+                else:
+                    for g in conv_grads:
+                        dist.all_reduce(g, group=group)
+                if sh.has_fc:
+                    dist.all_reduce(fc_gw, group=group)
+                    dist.all_reduce(fc_gb, group=group)
+                lt = loss_t.reshape(1).clone()
+                dist.all_reduce(lt, group=group)
+                return lt
+            loss_t = timed("acc_grad_ms", reduce_all)
         torch.cuda.synchronize(dev)
         times = StageTimes(**{k: sum(a.elapsed_time(b) for a, b in v) for k, v in events.items()})
         checksum = sum(float(g.double().sum()) for g in conv_grads)

@@ -151,7 +151,19 @@ class ShardedConv:
             dist.all_reduce(gw, op=dist.ReduceOp.SUM, group=self.group)
         return gw
 
-    def _grad_weight_nccl(self, gy, x):
+    def grad_weight_async(self, gy_local, x_local):
+        """accGrad whose all-reduce keeps running behind the caller's next
+        work (FFTCONV_B200_SHARDED_ASYNC); call wait() before reading gw."""
+        return self._grad_weight_nccl(gy_local, x_local, flags=1)
+
+    def wait(self):
+        """The current stream waits for every all-reduce issued so far."""
+        import torch
+
+        code = _native.lib().fftconv_b200_comm_wait(self.ws._h, C.c_void_p(torch.cuda.current_stream().cuda_stream))
+        raise_for_status(code, _native.last_error(self.ws._h))
+
+    def _grad_weight_nccl(self, gy, x, flags=0):
         """conv_fft.hpp:154-206 over the whole sharded minibatch, via
         fftconv_b200_grad_weight_sharded (include/fftconv_b200.h)."""
         import torch
@@ -163,7 +175,7 @@ class ShardedConv:
         gw = torch.empty((fo, f, k, k), dtype=torch.float32, device=gy.device)
         code = _native.lib().fftconv_b200_grad_weight_sharded(
             ws._h, ws._dev_ptr(gy), Sg, fo, gr, gc, ws._dev_ptr(x), Sx, f, xr, xc,
-            ws._dev_ptr(gw), self.comm.handle, self.chunks,
+            ws._dev_ptr(gw), self.comm.handle, self.chunks, int(flags),
             C.c_void_p(torch.cuda.current_stream(gy.device).cuda_stream))
         raise_for_status(code, _native.last_error(ws._h))
         return gw

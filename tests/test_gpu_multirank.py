@@ -65,3 +65,24 @@ def test_sharded_grad_weight_matches_full_batch(dev):
     tot = sum(parts).cpu().numpy()
     assert oracle.max_rel_error(tot, full.cpu().numpy()) < 1e-5
     del np
+
+
+def test_stack_two_ranks_gloo_matches_one_rank():
+    """The data-parallel training step (BASELINE configs[4] on N GPUs): two
+    ranks each run half the minibatch of the reference-net-small stack; the
+    summed loss and gradient checksum match the one-rank iteration."""
+    base = [os.path.join(ROOT, "bench.py"), "--steps", "2", "--warmup", "3", "--config",
+            "stack:reference-net-small"]
+    r1 = subprocess.run([sys.executable] + base, capture_output=True, text=True, timeout=600)
+    assert r1.returncode == 0, r1.stderr[-3000:]
+    one = json.loads([l for l in r1.stdout.splitlines() if l.startswith("{")][0])
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}"] + base + ["--gpus", "2", "--dist-backend", "gloo"]
+    r2 = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r2.returncode == 0, r2.stderr[-3000:]
+    lines = [l for l in r2.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    two = json.loads(lines[0])
+    assert two["n_gpus"] == 2 and two["run"]["S_per_gpu"] == 4 and two["value"] > 0
+    assert abs(two["loss"] - one["loss"]) <= 1e-5 * abs(one["loss"])
+    assert abs(two["grad_checksum"] - one["grad_checksum"]) <= 1e-4 * abs(one["grad_checksum"])

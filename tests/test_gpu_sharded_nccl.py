@@ -77,3 +77,36 @@ def test_sharded_comm_timing(dev, comm):
     ws.set_stage_timing(False)
     assert span > 0 and 0 <= exposed
     assert ws.last_launch_count() >= 2 + 4  # K1, K3 and four K4 chunks
+
+
+def test_run_iteration_through_sharded_accgrad(dev, comm):
+    """The data-parallel training step's conv gradients via the async sharded
+    entry point (all-reduces behind the backward pass, one wait at the end)
+    on a one-rank group equal the plain iteration's."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1312_5851_b200 import layers
+
+    spec = layers.preset_network("reference-net-small")
+    params = layers.init_params(spec, 5)
+    batch = layers.make_batch(spec, spec.default_batch, 5)
+    plain = layers.run_iteration(spec, params, batch)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        dp = layers.run_iteration(spec, params, batch, comm=comm)
+    finally:
+        dist.destroy_process_group()
+    torch.cuda.synchronize()
+    assert dp.loss == plain.loss
+    for a, b in zip(dp.conv_weight_grads, plain.conv_weight_grads):
+        assert torch.equal(a, b)
+    assert torch.equal(dp.fc_weight_grad, plain.fc_weight_grad)
