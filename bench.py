@@ -122,6 +122,18 @@ def cpu_reference_step_ms(cfg, iters, warmup, threads, seed=1234):
     return out
 
 
+def cpu_model():
+    """The host CPU's model name (lscpu's, from /proc/cpuinfo)."""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_threads():
     import oracle
 
@@ -157,7 +169,7 @@ def run_reference_arm(args, cfg, label):
         "run": {"parallelism": f"reference CPU (std::thread parallel_for, {threads} threads)"},
         "impl": "reference",
         "tflops_equiv": 3 * E / (ms * 1e-3) / 1e12,
-        "cpu_baseline": {"value": ms, "unit": "ms", "cores": threads, "kind": "reference",
+        "cpu_baseline": {"value": ms, "unit": "ms", "cores": threads, "kind": "reference", "cpu_model": cpu_model(),
                          "sample": f"reference run_op_bench<float> (FFT method) fprop+bprop+accGrad on the "
                                    f"full layer, {args.steps} steps (1 warm-up + 1 timed call per operator "
                                    f"each) after {args.warmup} warm-up steps"},
@@ -472,20 +484,61 @@ def main():
                        "fftconv_b200_*_host C ABI; each call pipelined over minibatch chunks "
                        "(H2D / compute / D2H on three streams), synchronous per call"}
 
-    # ---- CPU reference beside it (rank 0, N=1 only)
+    # ---- CPU reference beside it (rank 0, N=1 only), and the reference's
+    # own bench protocol (bench.hpp:80-145) for both implementations
     cpu = None
+    protocol = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             import oracle
+            from paper_1312_5851_b200 import harness
 
             if oracle.ref_available():
                 threads = cpu_threads()
                 iters = 1 if args.config == "wide" else 2
-                per_op = cpu_reference_step_ms(cfg, iters, 1, threads)
+                lcfg_full = LayerConfig(k, n, f, fo, S)
+                ref_rows = []
+                per_op = {}
+                for op_i, op in enumerate(OPS):
+                    st = oracle.ref_run_op_bench(k, n, f, fo, S, op_i, 1, iters, 1, threads, 1234)
+                    per_op[op] = st["mean_ms"]
+                    ref_rows.append(("fft", op_i, iters, st))
                 cpu = {"value": sum(per_op.values()), "unit": "ms", "cores": threads, "kind": "reference",
-                       "per_op_ms": per_op,
+                       "cpu_model": cpu_model(), "per_op_ms": per_op,
                        "sample": f"reference run_op_bench<float> (FFT method) on the full layer, {iters} iters "
                                  f"after 1 warm-up per op"}
+                if args.config in ("small", "paper"):
+                    # Method::direct beside it; one timed call per op (P: ~3 x 5 s)
+                    dper = {}
+                    for op_i, op in enumerate(OPS):
+                        st = oracle.ref_run_op_bench(k, n, f, fo, S, op_i, 0, 1, 0, threads, 1234)
+                        dper[op] = st["mean_ms"]
+                        ref_rows.append(("direct", op_i, 1, st))
+                    cpu["direct"] = {"value": sum(dper.values()), "unit": "ms", "per_op_ms": dper,
+                                     "sample": "reference run_op_bench<float> (direct method), 1 timed call per op"}
+                # our operators under the same protocol (device-resident, CUDA events per call)
+                ours = [harness.run_op_bench(lcfg_full, harness.BenchOp(i), iters=10, warmup=3, seed=1234,
+                                             resident=True, device=local) for i in range(3)]
+                rows = list(ours)
+                for method, op_i, it, st in ref_rows:
+                    r_ = harness.BenchResult(harness.BenchOp(op_i), method, lcfg_full, it, 1 if method == "fft" else 0,
+                                             threads, 1234, harness.BenchStats(st["mean_ms"], st["std_ms"],
+                                                                               st["min_ms"], st["median_ms"]),
+                                             st["checksum"])
+                    rows.append(r_)
+                ref_ck = {r_.op: r_.checksum for r_ in rows if r_.method == "fft"}
+                protocol = {
+                    "b200": {OPS[int(r_.op)]: {"mean_ms": r_.stats.mean_ms, "std_ms": r_.stats.std_ms,
+                                               "min_ms": r_.stats.min_ms, "median_ms": r_.stats.median_ms,
+                                               "checksum": r_.checksum,
+                                               "checksum_rel_diff_vs_reference":
+                                                   abs(r_.checksum - ref_ck[r_.op]) / max(abs(ref_ck[r_.op]), 1e-30)}
+                             for r_ in ours},
+                    "csv": harness.bench_table(rows, "csv"),
+                    "note": "rows in the reference CLI schema (fftconv_cli.cpp:144-149): method b200 = this "
+                            "implementation (device-resident, per-call CUDA events), fft / direct = the "
+                            "reference's run_op_bench<float> on the host cores",
+                }
         except Exception as exc:  # reported, never fatal
             cpu = {"value": None, "unit": "ms", "cores": None, "kind": "reference", "sample": f"failed: {exc}"}
 
@@ -522,6 +575,7 @@ def main():
         "clocks": clocks,
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "protocol": protocol,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -184,6 +184,24 @@ int fftconv_b200_grad_weight_host(fftconv_b200_ws* ws, const float* gy, size_t S
                                   size_t f, size_t x_rows, size_t x_cols, float* gw,
                                   unsigned threads);
 
+/* ---- Packed-spectrum API (fft.hpp:105-152, :209-243) --------------------
+ * fft_2d_real_batch: `planes` real m x m planes (already padded to the plan
+ * size, fp32, device) -> their packed half spectra in the reference's
+ * HalfSpectrum layout, spec[p][u][v] for u < m, v <= m/2 (complex
+ * interleaved fp32), unnormalised.  ifft_2d_real_batch: the inverse, full
+ * m x m planes scaled by 1/m^2 (as the reference's two 1/m passes); like the
+ * reference's c2r it reads only the packed columns and drops the imaginary
+ * parts c2r discards.  Both run on the K1 / K4 kernels, enqueued on
+ * `stream`; `scratch` is a device buffer of at least
+ * fftconv_b200_spectrum_scratch_bytes(planes, m) bytes (0 for an invalid m).
+ * m must be a power of two (FFTCONV_B200_PLAN_ERROR, FftPlan) of at most
+ * 128 (FFTCONV_B200_SIZE_ERROR). */
+size_t fftconv_b200_spectrum_scratch_bytes(size_t planes, size_t m);
+int fftconv_b200_fft_2d_real_batch(const float* planes, size_t planes_count, size_t m, float* spec,
+                                   void* scratch, size_t scratch_bytes, void* stream);
+int fftconv_b200_ifft_2d_real_batch(const float* spec, size_t planes_count, size_t m, float* planes,
+                                    void* scratch, size_t scratch_bytes, void* stream);
+
 /* ---- Instrumentation ----------------------------------------------------
  * When enabled, each operator records CUDA events between its stages on
  * the launching stream; fftconv_b200_stage_ms returns the last call's

@@ -39,6 +39,9 @@ SIGNATURES = [
     ("fftconv_b200_forward_host", _i, [_p, _p, _sz, _sz, _sz, _sz, _p, _sz, _sz, _sz, _p, C.c_uint]),
     ("fftconv_b200_grad_input_host", _i, [_p, _p, _sz, _sz, _sz, _sz, _p, _sz, _sz, _sz, _p, C.c_uint]),
     ("fftconv_b200_grad_weight_host", _i, [_p, _p, _sz, _sz, _sz, _sz, _p, _sz, _sz, _sz, _sz, _p, C.c_uint]),
+    ("fftconv_b200_spectrum_scratch_bytes", _sz, [_sz, _sz]),
+    ("fftconv_b200_fft_2d_real_batch", _i, [_p, _sz, _sz, _p, _p, _sz, _p]),
+    ("fftconv_b200_ifft_2d_real_batch", _i, [_p, _sz, _sz, _p, _p, _sz, _p]),
     ("fftconv_b200_set_stage_timing", _i, [_p, _i]),
     ("fftconv_b200_stage_ms", _i, [_p, _p]),
     ("fftconv_b200_last_launch_count", _i, [_p]),

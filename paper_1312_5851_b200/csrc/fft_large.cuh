@@ -280,16 +280,26 @@ __global__ void __launch_bounds__(128, 6) r2c128_rows_kernel(const R2CParams p, 
     }
   }
   __syncthreads();
-  // 128 bins x 16 planes per u row: one 128-B line per bin
+  // 128 bins x 16 planes per u row: one 128-B line per bin (a narrow kpad
+  // of 4 / 8 -- first-layer f = 3 -- writes only its 32 / 64 B)
   const long long bstride = (long long)p.R * p.kpad;  // float2 per bin
   if (u < kLRows) {
     const float2* tile = rows_s;
     float2* out = reinterpret_cast<float2*>(p.out) + (long long)u * kL * bstride + (long long)r * p.kpad + j0;
+    if (p.kpad - j0 >= 16) {
 #pragma unroll 8
-    for (int i = t; i < kL * 8; i += 64) {
-      const int v = i >> 3, part = i & 7;
-      *reinterpret_cast<float4*>(out + v * bstride + 2 * part) =
-          *reinterpret_cast<const float4*>(tile + v * 16 + 2 * part);
+      for (int i = t; i < kL * 8; i += 64) {
+        const int v = i >> 3, part = i & 7;
+        *reinterpret_cast<float4*>(out + v * bstride + 2 * part) =
+            *reinterpret_cast<const float4*>(tile + v * 16 + 2 * part);
+      }
+    } else {
+      const int hp = (p.kpad - j0) >> 1;  // float4 parts per bin (kpad is 4 or 8 here)
+      for (int i = t; i < kL * hp; i += 64) {
+        const int v = i / hp, part = i - v * hp;
+        *reinterpret_cast<float4*>(out + v * bstride + 2 * part) =
+            *reinterpret_cast<const float4*>(tile + v * 16 + 2 * part);
+      }
     }
   }
   if (p.amax) {  // row r's maximum

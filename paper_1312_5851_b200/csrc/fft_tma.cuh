@@ -145,7 +145,7 @@ template <int G>
 __device__ __forceinline__ GroupRef r2c_group(const R2CPair& P, int ngA, int g) {
   const int which = g >= ngA;
   const R2CParams& p = P.op[which];
-  const int gl = g - which * ngA, ngj = p.kpad / G;
+  const int gl = g - which * ngA, ngj = (p.kpad + G - 1) / G;
   const int r = gl / ngj;
   return {&p, which, r, (gl - r * ngj) * G};
 }
@@ -180,8 +180,8 @@ __global__ void __launch_bounds__(TR2C<M>::THREADS, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * T::STAGE);  // loads landed
   uint64_t* mid = full + S;                                           // intermediate written
   uint64_t* outb = mid + S;                                           // output tile written
-  const int ngA = P.op[0].R * (P.op[0].kpad / G);
-  const int ngroups = ngA + (P.n > 1 ? P.op[1].R * (P.op[1].kpad / G) : 0);
+  const int ngA = P.op[0].R * ((P.op[0].kpad + G - 1) / G);
+  const int ngroups = ngA + (P.n > 1 ? P.op[1].R * ((P.op[1].kpad + G - 1) / G) : 0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);

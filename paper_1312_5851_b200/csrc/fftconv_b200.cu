@@ -71,6 +71,17 @@ static void validate_cfg(const fftconv_b200_layer& c) {
 
 enum Pass { kFprop = 0, kBprop = 1, kAccGrad = 2 };
 
+// Padded K (complex per operand row of a spectrum F[t][row][2 kpad]): the
+// GEMM consumes K in chunks of 16 (one 128-B SW128 row), but a K below 16
+// (a first layer's f = 3 input maps) is padded only to 4 or 8 -- the GEMM's
+// TMA box reads past the row end and the copy engine zero-fills it, so the
+// spectra carry 1.3x instead of 5.3x their bytes at f = 3.  The one-pass
+// m <= 2 kernels write whole 16-plane lines and keep 16.
+static size_t kpad_for(size_t K, size_t m) {
+  if (m <= 2) return round_up(K, 16);
+  return K <= 4 ? 4 : K <= 8 ? 8 : round_up(K, 16);
+}
+
 // Device bytes (floats) each pass needs in the three frequency buffers.
 struct PassNeed {
   size_t a, b, d;
@@ -79,13 +90,13 @@ static PassNeed pass_need(Pass pass, size_t S, size_t f, size_t fo, size_t m) {
   const size_t bins = m * (m / 2 + 1);
   switch (pass) {
     case kFprop:  // D is [fo][S] or, swapped, [S][fo]
-      return {bins * S * 2 * round_up(f, 16), bins * fo * 2 * round_up(f, 16),
+      return {bins * S * 2 * kpad_for(f, m), bins * fo * 2 * kpad_for(f, m),
               bins * 2 * std::max(fo * round_up(S, 16), S * round_up(fo, 16))};
     case kBprop:
-      return {bins * S * 2 * round_up(fo, 16), bins * f * 2 * round_up(fo, 16),
+      return {bins * S * 2 * kpad_for(fo, m), bins * f * 2 * kpad_for(fo, m),
               bins * 2 * std::max(f * round_up(S, 16), S * round_up(f, 16))};
     default:
-      return {bins * fo * 2 * round_up(S, 16), bins * f * 2 * round_up(S, 16),
+      return {bins * fo * 2 * kpad_for(S, m), bins * f * 2 * kpad_for(S, m),
               bins * f * 2 * round_up(fo, 16)};
   }
 }
@@ -242,7 +253,7 @@ static void launch_r2c_tma(const R2CPair& P, const DevInfo& di, cudaStream_t st)
   auto kern = r2c_tma_kernel<M>;
   smem_optin(kern, T::SMEM);
   int groups = 0;
-  for (int i = 0; i < P.n; ++i) groups += P.op[i].R * (P.op[i].kpad / T::G);
+  for (int i = 0; i < P.n; ++i) groups += P.op[i].R * ((P.op[i].kpad + T::G - 1) / T::G);
   const int grid = std::max(1, std::min(groups, di.sms));
   const size_t bins = (size_t)T::BINS;
   CUtensorMap tm[2];
@@ -390,7 +401,7 @@ static int launch_r2c_large(const R2CParams& p, float2* scr, size_t scr_n, cudaS
       smem_optin(r2c128_cols_kernel, smem);
       launch_pdl(r2c128_cols_kernel, dim3(rows * p.J), dim3(256), smem, st, p, r0, scr);
     }
-    launch_pdl(r2c128_rows_kernel, dim3(rows, p.kpad / 16, (kLRows + kLUPerCta - 1) / kLUPerCta), dim3(128), 0,
+    launch_pdl(r2c128_rows_kernel, dim3(rows, (p.kpad + 15) / 16, (kLRows + kLUPerCta - 1) / kLUPerCta), dim3(128), 0,
                st, p, r0, (const float2*)scr);
     nl += 2;
   }
@@ -506,7 +517,7 @@ static void launch_gemm_kernel(const float* A, const float* B, float* out, size_
   p.bins = (int)bins;
   p.m_valid = (int)M;
   p.n_valid = (int)N;
-  p.k_chunks = (int)(kpad / 16);
+  p.k_chunks = (int)((kpad + 15) / 16);  // a K below 16: TMA zero-fills the chunk past the row
   p.m_tiles = g.m_tiles;
   p.n_tiles = g.n_tiles;
   p.nc = g.nc;
@@ -575,6 +586,49 @@ __global__ void conj_inplace_kernel(float2* v, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     v[i].y = -v[i].y;
+}
+
+// ---- packed-spectrum API (fft.hpp:105-152, :209-243) --------------------
+// The kernels' half spectrum keeps rows u <= m/2 and every column v, planes
+// as the K index: F[t][j] (t = u*m + v, row stride ld complex).  The
+// reference packing keeps every row u and columns v <= m/2 per plane:
+// spec[j][u][v].  Hermitian identity F[u][v] = conj(F[(m-u)%m][(m-v)%m]).
+
+// F -> reference packing; one thread per output element, v fastest.
+__global__ void spectrum_pack_ref_kernel(const float2* F, long long ld, int m, long long planes, float2* out) {
+  const int pc = m / 2 + 1;
+  const long long n = planes * m * pc;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long j = i / (m * pc);
+    const int rem = (int)(i - j * m * pc), u = rem / pc, v = rem - u * pc;
+    if (u <= m / 2) {
+      out[i] = F[(long long)(u * m + v) * ld + j];
+    } else {
+      const float2 z = F[(long long)(((m - u) % m) * m + (m - v) % m) * ld + j];
+      out[i] = make_float2(z.x, -z.y);
+    }
+  }
+}
+
+// reference packing -> F (ld complex per bin, planes >= J zero); one thread
+// per F element, plane fastest.
+__global__ void spectrum_unpack_ref_kernel(const float2* spec, int m, long long planes, long long ld, float2* F) {
+  const int pc = m / 2 + 1;
+  const long long n = (long long)pc * m * ld;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long t = i / ld, j = i - t * ld;
+    const int u = (int)(t / m), v = (int)(t - (long long)u * m);
+    float2 z = make_float2(0.f, 0.f);
+    if (j < planes) {
+      if (v <= m / 2) {
+        z = spec[(j * m + u) * pc + v];
+      } else {
+        z = spec[(j * m + (m - u) % m) * pc + (m - v)];
+        z.y = -z.y;
+      }
+    }
+    F[i] = z;
+  }
 }
 
 }  // namespace fcb
@@ -867,7 +921,7 @@ void run_forward(fftconv_b200_ws* ws, const float* x, size_t S, size_t f, size_t
   const size_t m = prepare(ws, cfg);
   const size_t bins = m * (m / 2 + 1);
   ensure_freq(ws, kFprop, cfg, m);
-  const size_t kp = round_up(f, 16);
+  const size_t kp = kpad_for(f, m);
 
   record(ws, 0, st);
   R2CParams a{x, ws->bufA, (long long)(f * n * n), (long long)(n * n), (int)S, (int)f, (int)kp,
@@ -913,7 +967,7 @@ void run_grad_input(fftconv_b200_ws* ws, const float* gy, size_t S, size_t fo, s
   const size_t m = prepare(ws, cfg);
   const size_t bins = m * (m / 2 + 1);
   ensure_freq(ws, kBprop, cfg, m);
-  const size_t kp = round_up(fo, 16);
+  const size_t kp = kpad_for(fo, m);
 
   record(ws, 0, st);
   R2CParams a{gy, ws->bufA, (long long)(fo * no * no), (long long)(no * no), (int)S, (int)fo,
@@ -969,7 +1023,7 @@ void run_grad_weight(fftconv_b200_ws* ws, const float* gy, size_t Sg, size_t fo,
   const size_t m = prepare(ws, cfg);
   const size_t bins = m * (m / 2 + 1);
   ensure_freq(ws, kAccGrad, cfg, m);
-  const size_t kp = round_up(S, 16);
+  const size_t kp = kpad_for(S, m);
 
   record(ws, 0, st);
   R2CParams a{gy, ws->bufA, (long long)(no * no), (long long)(fo * no * no), (int)fo, (int)S,
@@ -1514,6 +1568,83 @@ int fftconv_b200_stage_ms(fftconv_b200_ws* ws, float out[4]) {
 
 int fftconv_b200_last_launch_count(const fftconv_b200_ws* ws) {
   return ws ? ws->last_launches : -1;
+}
+
+// ---- packed-spectrum API ---------------------------------------------
+
+namespace {
+struct SpecScratch {
+  size_t f_bytes, l_elems, total;
+};
+SpecScratch spectrum_scratch(size_t planes, size_t m) {
+  const size_t bins = m * (m / 2 + 1), kp = round_up(std::max<size_t>(planes, 1), 16);
+  SpecScratch s;
+  s.f_bytes = round_up(bins * kp * sizeof(float2), 256);
+  s.l_elems = (m == kL) ? large_scratch_elems(planes, planes) : 0;
+  s.total = s.f_bytes + s.l_elems * sizeof(float2);
+  return s;
+}
+void spectrum_checks(size_t planes, size_t m, const void* scratch, size_t scratch_bytes) {
+  if (m == 0 || (m & (m - 1)))  // FftPlan (fft.hpp:23-26)
+    throw Error(FFTCONV_B200_PLAN_ERROR, "fft plan: size " + std::to_string(m) + " is not a power of 2");
+  if (m > kL) size_unsupported(m);
+  if (planes == 0) throw Error(FFTCONV_B200_SIZE_ERROR, "HalfSpectrum: all dimensions must be >= 1");
+  if (!scratch || scratch_bytes < spectrum_scratch(planes, m).total)
+    throw Error(FFTCONV_B200_INVALID_ARGUMENT, "spectrum: scratch smaller than fftconv_b200_spectrum_scratch_bytes");
+}
+int ew_blocks(long long n) { return (int)std::max<long long>(1, std::min<long long>((n + 255) / 256, 148LL * 16)); }
+}  // namespace
+
+size_t fftconv_b200_spectrum_scratch_bytes(size_t planes, size_t m) {
+  if (m == 0 || (m & (m - 1)) || m > kL) return 0;
+  return spectrum_scratch(planes, m).total;
+}
+
+int fftconv_b200_fft_2d_real_batch(const float* planes, size_t P, size_t m, float* spec, void* scratch,
+                                   size_t scratch_bytes, void* stream) {
+  return guarded(nullptr, [&] {
+    spectrum_checks(P, m, scratch, scratch_bytes);
+    const SpecScratch ss = spectrum_scratch(P, m);
+    const cudaStream_t st = (cudaStream_t)stream;
+    int dev = 0;
+    FCB_CUDA(cudaGetDevice(&dev));
+    float* F = static_cast<float*>(scratch);
+    const size_t kp = round_up(P, 16);
+    // planes as the K index of one operand row: F[t][0][2 kp] (pad planes zero)
+    R2CParams p{planes, F, 0, (long long)(m * m), 1, (int)P, (int)kp, (int)m, (int)(m | 1)};
+    if (m == kL)
+      launch_r2c_large(p, reinterpret_cast<float2*>(static_cast<char*>(scratch) + ss.f_bytes), ss.l_elems, st);
+    else
+      launch_r2c_one(m, p, st, dev_info(dev));
+    const long long n = (long long)P * m * (m / 2 + 1);
+    spectrum_pack_ref_kernel<<<ew_blocks(n), 256, 0, st>>>(reinterpret_cast<const float2*>(F), (long long)kp,
+                                                           (int)m, (long long)P, reinterpret_cast<float2*>(spec));
+    FCB_CUDA(cudaGetLastError());
+  });
+}
+
+int fftconv_b200_ifft_2d_real_batch(const float* spec, size_t P, size_t m, float* planes, void* scratch,
+                                    size_t scratch_bytes, void* stream) {
+  return guarded(nullptr, [&] {
+    spectrum_checks(P, m, scratch, scratch_bytes);
+    const SpecScratch ss = spectrum_scratch(P, m);
+    const cudaStream_t st = (cudaStream_t)stream;
+    int dev = 0;
+    FCB_CUDA(cudaGetDevice(&dev));
+    float* F = static_cast<float*>(scratch);
+    const size_t ld = round_up(P, 16);  // complex per bin (even, 16-B aligned rows for the TMA maps)
+    const long long n = (long long)(m / 2 + 1) * m * ld;
+    spectrum_unpack_ref_kernel<<<ew_blocks(n), 256, 0, st>>>(reinterpret_cast<const float2*>(spec), (int)m,
+                                                             (long long)P, (long long)ld,
+                                                             reinterpret_cast<float2*>(F));
+    FCB_CUDA(cudaGetLastError());
+    // bin-major product P[t][0][ld]: planes (0, j) -> planes + j m^2, full m x m, 1/m^2
+    C2RParams c{F, planes, 0, (long long)(m * m), 1, (int)P, (int)m, 0, 0, 1.0f / (float)(m * m), (int)ld};
+    if (m == kL)
+      launch_c2r_large(c, reinterpret_cast<float2*>(static_cast<char*>(scratch) + ss.f_bytes), ss.l_elems, st);
+    else
+      launch_c2r(m, c, st, dev_info(dev));
+  });
 }
 
 // ---- unit-level test hooks -------------------------------------------

@@ -7,15 +7,15 @@ operators themselves, but the reference's unit-level surface for K1/K4
 Packing is the reference's: per plane m rows x (m/2 + 1) packed columns,
 ``full[u][v] = conj(full[(m-u)%m][(m-v)%m])`` for the unstored columns.  The
 kernels' internal half spectrum keeps the other half (rows u <= m/2, all
-columns v), so these wrappers repack at the boundary through the same
-Hermitian identity; they are convenience / parity entry points, not a hot
-path.
+columns v); the C-ABI entry points (include/fftconv_b200.h,
+fftconv_b200_fft_2d_real_batch / _ifft_) repack at the boundary with one
+device kernel through the same Hermitian identity.
 """
 from __future__ import annotations
 
 from dataclasses import dataclass
 
-from .errors import SizeError
+from .errors import PlanError, SizeError
 from .layer_config import is_pow2
 
 
@@ -64,62 +64,61 @@ class HalfSpectrum:
         return self.packed_bin(b, f, (m - u) % m, m - v).conjugate()
 
 
+def _call(fn, src, P, m, dst):
+    import ctypes as C
+
+    from . import _native
+    from .errors import raise_for_status
+
+    torch = _torch()
+    L = _native.lib()
+    nbytes = int(L.fftconv_b200_spectrum_scratch_bytes(P, m))
+    scratch = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=src.device)
+    code = fn(C.c_void_p(src.data_ptr()), P, m, C.c_void_p(dst.data_ptr()), C.c_void_p(scratch.data_ptr()), nbytes,
+              C.c_void_p(torch.cuda.current_stream(src.device).cuda_stream))
+    raise_for_status(code, _native.last_error(None))
+
+
 def fft_2d_real_batch(t, m: int | None = None) -> HalfSpectrum:
     """fft.hpp:209-225: packed forward transform of every (batch, map) plane
-    of t [batch][maps][m][m] (fp32; CUDA tensor or host array).  Planes must
-    already be padded to the plan size m (``size_error`` otherwise)."""
-    torch = _torch()
-    from . import kernels
+    of t [batch][maps][m][m] (fp32; CUDA tensor or host array), through
+    fftconv_b200_fft_2d_real_batch (K1 + a repack into the reference
+    packing).  Planes must already be padded to the plan size m
+    (``size_error`` otherwise)."""
+    from . import _native
 
+    torch = _torch()
     t = torch.as_tensor(t, dtype=torch.float32)
     if t.device.type != "cuda":
         t = t.cuda()
+    t = t.contiguous()
     B, F, R, Cc = t.shape
     m = R if m is None else m
     if m == 0 or not is_pow2(m):
-        raise SizeError("fft_2d_real_batch: plan size must be a power of two")
+        raise PlanError(f"fft plan: size {m} is not a power of 2")
     if R != m or Cc != m:
         raise SizeError("fft_2d_real_batch: planes must be padded to the plan size")
-    ours = kernels.r2c(t.reshape(B * F, m, m), m)  # [P][m/2+1][m]: half over rows
-    return HalfSpectrum(_rows_to_cols(ours, m).reshape(B, F, m, m // 2 + 1))
+    if B == 0 or F == 0:
+        raise SizeError("HalfSpectrum: all dimensions must be >= 1")
+    out = torch.empty((B, F, m, m // 2 + 1), dtype=torch.complex64, device=t.device)
+    _call(_native.lib().fftconv_b200_fft_2d_real_batch, t, B * F, m, out)
+    return HalfSpectrum(out)
 
 
 def ifft_2d_real_batch(s: HalfSpectrum, m: int | None = None):
     """fft.hpp:227-243: inverse of fft_2d_real_batch, full real m x m planes
-    (scaled by 1/m^2 like the reference's two 1/m passes)."""
-    from . import kernels
+    (scaled by 1/m^2 like the reference's two 1/m passes), through
+    fftconv_b200_ifft_2d_real_batch."""
+    from . import _native
 
+    torch = _torch()
     B, F, R, pc = s.data.shape
     m = R if m is None else m
+    if m == 0 or not is_pow2(m):
+        raise PlanError(f"fft plan: size {m} is not a power of 2")
     if R != m:
         raise SizeError("ifft_2d_real_batch: spectrum rows do not match plan size")
-    ours = _cols_to_rows(s.data.reshape(B * F, m, pc), m)  # [P][m/2+1][m]
-    return kernels.c2r(ours, m).reshape(B, F, m, m)
-
-
-def _rows_to_cols(h, m: int):
-    """[P][m/2+1][m] (u <= m/2, all v) -> [P][m][m/2+1] (all u, v <= m/2):
-    F[u][v] = conj(F[m-u][(m-v) % m]) for u > m/2."""
-    torch = _torch()
-    pc = m // 2 + 1
-    u = torch.arange(m, device=h.device).view(m, 1)
-    v = torch.arange(pc, device=h.device).view(1, pc)
-    low = u <= m // 2
-    ru = torch.where(low, u, m - u).expand(m, pc)
-    rv = torch.where(low, v, (m - v) % m).expand(m, pc)
-    out = h[:, ru, rv]
-    return torch.where(low.expand(m, pc), out, out.conj())
-
-
-def _cols_to_rows(c, m: int):
-    """[P][m][m/2+1] (all u, v <= m/2) -> [P][m/2+1][m] (u <= m/2, all v):
-    F[u][v] = conj(F[(m-u) % m][m-v]) for v > m/2."""
-    torch = _torch()
-    pc = m // 2 + 1
-    u = torch.arange(pc, device=c.device).view(pc, 1)
-    v = torch.arange(m, device=c.device).view(1, m)
-    low = v <= m // 2
-    ru = torch.where(low, u, (m - u) % m).expand(pc, m)
-    rv = torch.where(low, v, m - v).expand(pc, m)
-    out = c[:, ru, rv]
-    return torch.where(low.expand(pc, m), out, out.conj()).contiguous()
+    spec = s.data.contiguous()
+    out = torch.empty((B, F, m, m), dtype=torch.float32, device=spec.device)
+    _call(_native.lib().fftconv_b200_ifft_2d_real_batch, spec, B * F, m, out)
+    return out

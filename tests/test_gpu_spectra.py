@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 
 import oracle
-from paper_1312_5851_b200 import SizeError
+from paper_1312_5851_b200 import PlanError, SizeError
 from paper_1312_5851_b200.spectra import HalfSpectrum, fft_2d_real_batch, ifft_2d_real_batch
 
 pytestmark = pytest.mark.gpu
@@ -55,8 +55,8 @@ def test_round_trip(dev, m):
 def test_size_errors(dev):
     with pytest.raises(SizeError):
         fft_2d_real_batch(np.zeros((1, 1, 8, 8), np.float32), m=16)  # not padded to the plan
-    with pytest.raises(SizeError):
-        fft_2d_real_batch(np.zeros((1, 1, 6, 6), np.float32))  # plan size not a power of two
+    with pytest.raises(PlanError):  # FftPlan(6): plan_error (fft.hpp:23-26)
+        fft_2d_real_batch(np.zeros((1, 1, 6, 6), np.float32))
     with pytest.raises(SizeError):
         ifft_2d_real_batch(HalfSpectrum.zeros(1, 1, 8), m=16)
     with pytest.raises(SizeError):
@@ -88,3 +88,15 @@ def test_linearity(dev):
     lhs = fft_2d_real_batch(a * x + b * y).data.cpu().numpy()
     rhs = a * fft_2d_real_batch(x).data.cpu().numpy() + b * fft_2d_real_batch(y).data.cpu().numpy()
     assert np.linalg.norm(lhs - rhs) <= 1e-5 * np.linalg.norm(rhs)
+
+
+@pytest.mark.parametrize("shape", [(3, 7, 32, 32), (1, 37, 8, 8), (2, 9, 64, 64), (1, 19, 128, 128), (4, 5, 2, 2)])
+def test_many_planes_round_trip(dev, shape):
+    """Plane counts off the 16-plane grouping, every FFT-size family, through
+    the C-ABI batch entry points (fftconv_b200_fft_2d_real_batch / _ifft_)."""
+    t = oracle.fill_uniform(shape, 31 + shape[1], 1)
+    s = fft_2d_real_batch(t)
+    ref = np.fft.rfft2(t.astype(np.float64))
+    assert np.linalg.norm(s.data.cpu().numpy() - ref) <= 2e-6 * np.linalg.norm(ref)
+    back = ifft_2d_real_batch(s).cpu().numpy()
+    assert np.linalg.norm(back - t) <= 2e-6 * np.linalg.norm(t)
