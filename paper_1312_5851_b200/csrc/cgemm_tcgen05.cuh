@@ -270,6 +270,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint32_t ph = 0;
       int gi = 0;
       (void)gi;
+      // operand spectra are read by the tiles of one bin at about the same
+      // time, then never again: evict them first, so the product the c2r
+      // reads next stays in L2 (FCB_GEMM_EVF=0: default policy)
+#ifndef FCB_GEMM_EVF
+#define FCB_GEMM_EVF 1
+#endif
+      const uint64_t pol = FCB_GEMM_EVF ? l2_policy_evict_first() : l2_policy_evict_normal();
       for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
         const int t = tile / tiles_per_bin;
         const int rem = tile - t * tiles_per_bin;
@@ -281,16 +288,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           uint8_t* st = smem + s * rawBytes;
           if constexpr (!F16) {
             mbar_arrive_expect_tx(&rfull[s], kChunkBytesA + rowsB);
-            tma_load_3d(st, &tmA, &rfull[s], kc * 32, mt * kTileM, t);
-            tma_load_3d(st + offB, &tmB, &rfull[s], kc * 32, nt * nc, t);
+            tma_load_3d_hint(st, &tmA, &rfull[s], kc * 32, mt * kTileM, t, pol);
+            tma_load_3d_hint(st + offB, &tmB, &rfull[s], kc * 32, nt * nc, t, pol);
           } else {  // chunks 2kc, 2kc+1 (the second absent at odd k_chunks: converters zero it)
             const bool two = 2 * kc + 1 < p.k_chunks;
             mbar_arrive_expect_tx(&rfull[s], (two ? 2 : 1) * (kChunkBytesA + rowsB));
-            tma_load_3d(st, &tmA, &rfull[s], kc * 64, mt * kTileM, t);
-            tma_load_3d(st + offB, &tmB, &rfull[s], kc * 64, nt * nc, t);
+            tma_load_3d_hint(st, &tmA, &rfull[s], kc * 64, mt * kTileM, t, pol);
+            tma_load_3d_hint(st + offB, &tmB, &rfull[s], kc * 64, nt * nc, t, pol);
             if (two) {
-              tma_load_3d(st + kChunkBytesA, &tmA, &rfull[s], kc * 64 + 32, mt * kTileM, t);
-              tma_load_3d(st + offB + rowsB, &tmB, &rfull[s], kc * 64 + 32, nt * nc, t);
+              tma_load_3d_hint(st + kChunkBytesA, &tmA, &rfull[s], kc * 64 + 32, mt * kTileM, t, pol);
+              tma_load_3d_hint(st + offB + rowsB, &tmB, &rfull[s], kc * 64 + 32, nt * nc, t, pol);
             }
           }
           if (++s == RS) { s = 0; ph ^= 1; }
@@ -507,6 +514,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       tc_fence_after();
       const int m = mt * kTileM + row;
       const bool mok = m < p.m_valid;
+#if FCB_GEMM_EVL
+      const uint64_t pol_out = l2_policy_evict_last();
+#endif
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + a * (2 * nc);
       float2* out = reinterpret_cast<float2*>(p.out) + (long long)t * p.s_t + (m >> p.gm_log2) * p.s_mg +
                     (m & ((1 << p.gm_log2) - 1));
@@ -519,9 +529,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int n = n0 + i;
-          if (mok && n < p.n_valid)
-            out[(long long)n * p.s_n] = F16 ? make_float2(re[i] * oscale, im_sign * oscale * im[i])
-                                            : make_float2(re[i], im_sign * im[i]);
+          if (mok && n < p.n_valid) {
+            const float2 v = F16 ? make_float2(re[i] * oscale, im_sign * oscale * im[i])
+                                 : make_float2(re[i], im_sign * im[i]);
+#if FCB_GEMM_EVL
+            st_global_hint(out + (long long)n * p.s_n, v, pol_out);
+#else
+            out[(long long)n * p.s_n] = v;
+#endif
+          }
         }
       }
       tc_fence_before();
