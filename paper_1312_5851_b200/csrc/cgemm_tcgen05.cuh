@@ -276,7 +276,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #ifndef FCB_GEMM_EVF
 #define FCB_GEMM_EVF 1
 #endif
-      const uint64_t pol = FCB_GEMM_EVF ? l2_policy_evict_first() : l2_policy_evict_normal();
+      // (only an operand no other tile re-reads: A when one N tile covers the
+      // bin, B when one M tile does -- W re-reads A three times)
+      const uint64_t pol_first = l2_policy_evict_first(), pol_norm = l2_policy_evict_normal();
+      const uint64_t pol_a = (FCB_GEMM_EVF && p.n_tiles == 1) ? pol_first : pol_norm;
+      const uint64_t pol_b = (FCB_GEMM_EVF && p.m_tiles == 1) ? pol_first : pol_norm;
       for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
         const int t = tile / tiles_per_bin;
         const int rem = tile - t * tiles_per_bin;
@@ -288,16 +292,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           uint8_t* st = smem + s * rawBytes;
           if constexpr (!F16) {
             mbar_arrive_expect_tx(&rfull[s], kChunkBytesA + rowsB);
-            tma_load_3d_hint(st, &tmA, &rfull[s], kc * 32, mt * kTileM, t, pol);
-            tma_load_3d_hint(st + offB, &tmB, &rfull[s], kc * 32, nt * nc, t, pol);
+            tma_load_3d_hint(st, &tmA, &rfull[s], kc * 32, mt * kTileM, t, pol_a);
+            tma_load_3d_hint(st + offB, &tmB, &rfull[s], kc * 32, nt * nc, t, pol_b);
           } else {  // chunks 2kc, 2kc+1 (the second absent at odd k_chunks: converters zero it)
             const bool two = 2 * kc + 1 < p.k_chunks;
             mbar_arrive_expect_tx(&rfull[s], (two ? 2 : 1) * (kChunkBytesA + rowsB));
-            tma_load_3d_hint(st, &tmA, &rfull[s], kc * 64, mt * kTileM, t, pol);
-            tma_load_3d_hint(st + offB, &tmB, &rfull[s], kc * 64, nt * nc, t, pol);
+            tma_load_3d_hint(st, &tmA, &rfull[s], kc * 64, mt * kTileM, t, pol_a);
+            tma_load_3d_hint(st + offB, &tmB, &rfull[s], kc * 64, nt * nc, t, pol_b);
             if (two) {
-              tma_load_3d_hint(st + kChunkBytesA, &tmA, &rfull[s], kc * 64 + 32, mt * kTileM, t, pol);
-              tma_load_3d_hint(st + offB + rowsB, &tmB, &rfull[s], kc * 64 + 32, nt * nc, t, pol);
+              tma_load_3d_hint(st + kChunkBytesA, &tmA, &rfull[s], kc * 64 + 32, mt * kTileM, t, pol_a);
+              tma_load_3d_hint(st + offB + rowsB, &tmB, &rfull[s], kc * 64 + 32, nt * nc, t, pol_b);
             }
           }
           if (++s == RS) { s = 0; ph ^= 1; }

@@ -432,10 +432,14 @@ struct GemmGeom {
   int nc, n_tiles, m_tiles, stages;
   size_t smem;
 };
+#ifndef FCB_F16_MAXNC
+#define FCB_F16_MAXNC kMaxNc
+#endif
 static GemmGeom gemm_geom(size_t M, size_t N, const DevInfo& di, bool f16) {
   GemmGeom g;
   const size_t n16 = round_up(N, 16);
-  g.n_tiles = (int)((n16 + kMaxNc - 1) / kMaxNc);
+  const size_t max_nc = f16 ? FCB_F16_MAXNC : kMaxNc;
+  g.n_tiles = (int)((n16 + max_nc - 1) / max_nc);
   g.nc = (int)round_up((n16 + g.n_tiles - 1) / g.n_tiles, 16);
   g.m_tiles = (int)((M + kTileM - 1) / kTileM);
   // raw TMA stages (A + B chunks) fill what the two converted-B buffers leave
