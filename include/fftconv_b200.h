@@ -163,6 +163,13 @@ int fftconv_b200_grad_weight_sharded(fftconv_b200_ws* ws, const float* gy, size_
                                      unsigned flags, void* stream);
 #define FFTCONV_B200_SHARDED_ASYNC 1u
 int fftconv_b200_comm_wait(fftconv_b200_ws* ws, void* stream);
+/* Host-buffer form of the above (the drop-in's Tensor4 storage): this rank's
+ * shard is copied in (chunked H2D pipeline), its gw computed, all-reduced
+ * over `comm` and copied back; returns with the full-batch gradient in `gw`. */
+int fftconv_b200_grad_weight_sharded_host(fftconv_b200_ws* ws, const float* gy, size_t S_gy, size_t fo,
+                                          size_t gy_rows, size_t gy_cols, const float* x, size_t S_x,
+                                          size_t f, size_t x_rows, size_t x_cols, float* gw, void* comm,
+                                          unsigned threads);
 /* With stage timing enabled, the last sharded call's all-reduce timing (ms):
  * out[0] = first all-reduce start -> last all-reduce end (collective span),
  * out[1] = end of the local transforms -> last all-reduce end (the part not

@@ -123,6 +123,22 @@ class ConvWorkspace {
     return gw;
   }
 
+  // Minibatch-sharded accGrad (BASELINE configs[3] / [4] on N GPUs): `gy`
+  // and `x` are this rank's shard of the minibatch; returns the full-batch
+  // weight gradient, summed over the ranks of `nccl_comm` (an ncclComm_t,
+  // e.g. from nccl_comm_create).  A Tensor4 cannot be empty, so a rank whose
+  // shard is empty (world > S) calls fftconv_b200_grad_weight_sharded_host
+  // with S_gy = S_x = 0 instead; it contributes zeros to the sum.
+  Weights4<float> grad_weight_sharded(const Tensor4<float>& gy, const Tensor4<float>& x, void* nccl_comm,
+                                      unsigned threads = 1) {
+    const std::size_t k = x.rows() >= gy.rows() ? x.rows() - gy.rows() + 1 : 1;
+    Weights4<float> gw(gy.maps(), x.maps(), k);
+    call(fftconv_b200_grad_weight_sharded_host(ws_, gy.data().data(), gy.batch(), gy.maps(), gy.rows(),
+                                               gy.cols(), x.data().data(), x.batch(), x.maps(), x.rows(),
+                                               x.cols(), gw.data().data(), nccl_comm, threads));
+    return gw;
+  }
+
   fftconv_b200_ws* native_handle() const { return ws_; }
 
  private:
@@ -136,6 +152,23 @@ class ConvWorkspace {
   fftconv_b200_ws* ws_ = nullptr;
   mutable OpCounters counters_{};
 };
+
+// NCCL communicator for grad_weight_sharded without linking NCCL: rank 0
+// calls nccl_unique_id, the caller distributes the 128 bytes, every rank
+// calls nccl_comm_create.  Throws fftconv::error on failure.
+inline std::vector<unsigned char> nccl_unique_id() {
+  std::vector<unsigned char> id(128);
+  const int code = fftconv_b200_nccl_get_unique_id(id.data());
+  detail::throw_status(code, fftconv_b200_last_error(nullptr));
+  return id;
+}
+inline void* nccl_comm_create(const std::vector<unsigned char>& id, int nranks, int rank, int device = 0) {
+  void* comm = nullptr;
+  const int code = fftconv_b200_nccl_comm_create(id.data(), nranks, rank, device, &comm);
+  detail::throw_status(code, fftconv_b200_last_error(nullptr));
+  return comm;
+}
+inline void nccl_comm_destroy(void* comm) { fftconv_b200_nccl_comm_destroy(comm); }
 
 // conv_fft.hpp:314-335
 inline ConvWorkspace workspace_for(const std::vector<LayerConfig>& configs, int device = 0) {

@@ -35,6 +35,8 @@ SIGNATURES = [
     ("fftconv_b200_grad_weight_sharded", _i,
      [_p, _p, _sz, _sz, _sz, _sz, _p, _sz, _sz, _sz, _sz, _p, _p, _i, C.c_uint, _p]),
     ("fftconv_b200_comm_wait", _i, [_p, _p]),
+    ("fftconv_b200_grad_weight_sharded_host", _i,
+     [_p, _p, _sz, _sz, _sz, _sz, _p, _sz, _sz, _sz, _sz, _p, _p, C.c_uint]),
     ("fftconv_b200_comm_ms", _i, [_p, _p]),
     ("fftconv_b200_forward_host", _i, [_p, _p, _sz, _sz, _sz, _sz, _p, _sz, _sz, _sz, _p, C.c_uint]),
     ("fftconv_b200_grad_input_host", _i, [_p, _p, _sz, _sz, _sz, _sz, _p, _sz, _sz, _sz, _p, C.c_uint]),

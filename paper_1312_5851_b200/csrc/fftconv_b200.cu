@@ -1505,31 +1505,40 @@ int fftconv_b200_grad_input_host(fftconv_b200_ws* ws, const float* gy, size_t S,
   });
 }
 
-int fftconv_b200_grad_weight_host(fftconv_b200_ws* ws, const float* gy, size_t S_gy, size_t fo,
-                                  size_t gy_rows, size_t gy_cols, const float* x, size_t S_x,
-                                  size_t f, size_t x_rows, size_t x_cols, float* gw,
-                                  unsigned threads) {
-  (void)threads;
-  if (!ws) return FFTCONV_B200_INVALID_ARGUMENT;
-  return guarded(ws, [&] {
-    DeviceGuard g(ws->device);
+namespace {
+// grad_weight on host buffers (chunked H2D / compute pipeline); with `comm`
+// the finished gw is all-reduced over the ranks before the D2H (the
+// minibatch-sharded host entry point; an empty shard contributes zeros).
+void grad_weight_host_impl(fftconv_b200_ws* ws, const float* gy, size_t S_gy, size_t fo, size_t gy_rows,
+                           size_t gy_cols, const float* x, size_t S_x, size_t f, size_t x_rows, size_t x_cols,
+                           float* gw, void* comm) {
+  DeviceGuard g(ws->device);
+  const bool empty = comm && S_gy == 0 && S_x == 0;
+  if (!empty) {
     require_nonzero(S_gy, fo, gy_rows, gy_cols, "Tensor4");
     require_nonzero(S_x, f, x_rows, x_cols, "Tensor4");
-    if (!(gy_rows == gy_cols && x_rows == x_cols && S_gy == S_x && gy_rows <= x_rows)) {
-      run_grad_weight(ws, nullptr, S_gy, fo, gy_rows, gy_cols, nullptr, S_x, f, x_rows, x_cols,
-                      nullptr, ws->host_stream);
-      return;
-    }
-    const size_t S = S_x, no = gy_rows, n = x_rows, k = n - no + 1;
-    const size_t m = prepare(ws, fftconv_b200_layer{k, n, f, fo, S});
-    const size_t pgy = fo * no * no, px = f * n * n, ngw = fo * f * k * k;
-    grow(ws->st_in0, ws->n_in0, S * pgy);
-    grow(ws->st_in1, ws->n_in1, S * px);
-    grow(ws->st_out, ws->n_out, ngw);
+  } else {
+    require_nonzero(fo, gy_rows, gy_cols, 1, "Tensor4");
+    require_nonzero(f, x_rows, x_cols, 1, "Tensor4");
+  }
+  if (!(gy_rows == gy_cols && x_rows == x_cols && S_gy == S_x && gy_rows <= x_rows)) {
+    run_grad_weight(ws, nullptr, S_gy, fo, gy_rows, gy_cols, nullptr, S_x, f, x_rows, x_cols, nullptr,
+                    ws->host_stream);  // raises the reference's error
+    return;
+  }
+  const size_t S = S_x, no = gy_rows, n = x_rows, k = n - no + 1;
+  const size_t m = empty ? next_pow2(n) : prepare(ws, fftconv_b200_layer{k, n, f, fo, S});
+  const size_t pgy = fo * no * no, px = f * n * n, ngw = fo * f * k * k;
+  grow(ws->st_in0, ws->n_in0, std::max<size_t>(S, 1) * pgy);
+  grow(ws->st_in1, ws->n_in1, std::max<size_t>(S, 1) * px);
+  grow(ws->st_out, ws->n_out, ngw);
+  order_after_last(ws, ws->host_stream);
+  uint64_t saved[3];
+  std::memcpy(saved, ws->ctr, sizeof saved);
+  if (empty) {
+    FCB_CUDA(cudaMemsetAsync(ws->st_out, 0, ngw * sizeof(float), ws->host_stream));
+  } else {
     const int C = host_chunks(S, S * (pgy + px) * sizeof(float), m, 32);
-    order_after_last(ws, ws->host_stream);
-    uint64_t saved[3];
-    std::memcpy(saved, ws->ctr, sizeof saved);
     for (int c = 0; c < C; ++c) {
       const auto [b0, b1] = chunk_range(S, C, c);
       h2d(ws, ws->st_in0 + b0 * pgy, gy + b0 * pgy, (b1 - b0) * pgy);
@@ -1540,17 +1549,44 @@ int fftconv_b200_grad_weight_host(fftconv_b200_ws* ws, const float* gy, size_t S
       const auto [b0, b1] = chunk_range(S, C, c);
       FCB_CUDA(cudaStreamWaitEvent(ws->host_stream, ws->pev[0][c], 0));
       // gw = sum over minibatch chunks (batch decomposability)
-      run_grad_weight(ws, ws->st_in0 + b0 * pgy, b1 - b0, fo, no, no, ws->st_in1 + b0 * px,
-                      b1 - b0, f, n, n, ws->st_out, ws->host_stream, /*accum=*/c > 0);
+      run_grad_weight(ws, ws->st_in0 + b0 * pgy, b1 - b0, fo, no, no, ws->st_in1 + b0 * px, b1 - b0, f, n, n,
+                      ws->st_out, ws->host_stream, /*accum=*/c > 0);
     }
-    FCB_CUDA(cudaMemcpyAsync(gw, ws->st_out, ngw * sizeof(float), cudaMemcpyDeviceToHost,
-                             ws->host_stream));
-    FCB_CUDA(cudaStreamSynchronize(ws->host_stream));
-    ws->has_last = false;
+  }
+  if (comm)
+    FCB_NCCL(nccl_api().all_reduce(ws->st_out, ws->st_out, ngw, ncclFloat32, ncclSum,
+                                   reinterpret_cast<ncclComm_t>(comm), ws->host_stream));
+  FCB_CUDA(cudaMemcpyAsync(gw, ws->st_out, ngw * sizeof(float), cudaMemcpyDeviceToHost, ws->host_stream));
+  FCB_CUDA(cudaStreamSynchronize(ws->host_stream));
+  ws->has_last = false;
+  if (!empty) {
     const uint64_t bins = m * (m / 2 + 1);
     ws->ctr[0] = saved[0] + S * f + S * fo;
     ws->ctr[1] = saved[1] + fo * f;
     ws->ctr[2] = saved[2] + bins * fo * f * S;
+  }
+}
+}  // namespace
+
+int fftconv_b200_grad_weight_host(fftconv_b200_ws* ws, const float* gy, size_t S_gy, size_t fo,
+                                  size_t gy_rows, size_t gy_cols, const float* x, size_t S_x,
+                                  size_t f, size_t x_rows, size_t x_cols, float* gw,
+                                  unsigned threads) {
+  (void)threads;
+  if (!ws) return FFTCONV_B200_INVALID_ARGUMENT;
+  return guarded(ws, [&] {
+    grad_weight_host_impl(ws, gy, S_gy, fo, gy_rows, gy_cols, x, S_x, f, x_rows, x_cols, gw, nullptr);
+  });
+}
+
+int fftconv_b200_grad_weight_sharded_host(fftconv_b200_ws* ws, const float* gy, size_t S_gy, size_t fo,
+                                          size_t gy_rows, size_t gy_cols, const float* x, size_t S_x, size_t f,
+                                          size_t x_rows, size_t x_cols, float* gw, void* comm, unsigned threads) {
+  (void)threads;
+  if (!ws) return FFTCONV_B200_INVALID_ARGUMENT;
+  return guarded(ws, [&] {
+    if (!comm) throw Error(FFTCONV_B200_INVALID_ARGUMENT, "grad_weight_sharded_host: comm is NULL");
+    grad_weight_host_impl(ws, gy, S_gy, fo, gy_rows, gy_cols, x, S_x, f, x_rows, x_cols, gw, comm);
   });
 }
 

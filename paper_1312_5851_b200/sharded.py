@@ -130,6 +130,8 @@ class ShardedConv:
 
         if self.comm is not None and isinstance(gy_local, torch.Tensor) and gy_local.is_cuda:
             return self._grad_weight_nccl(gy_local, x_local)
+        if self.comm is not None and not isinstance(gy_local, torch.Tensor):
+            return self._grad_weight_nccl_host(gy_local, x_local)
         multi = dist.is_initialized() and dist.get_world_size(self.group) > 1
         if int(gy_local.shape[0]) == 0 and int(x_local.shape[0]) == 0:
             # empty shard (world > S): contribute zeros so the other ranks'
@@ -178,6 +180,23 @@ class ShardedConv:
             ws._dev_ptr(gw), self.comm.handle, self.chunks, int(flags),
             C.c_void_p(torch.cuda.current_stream(gy.device).cuda_stream))
         raise_for_status(code, _native.last_error(ws._h))
+        return gw
+
+    def _grad_weight_nccl_host(self, gy, x):
+        """Host-buffer form (fftconv_b200_grad_weight_sharded_host): numpy
+        shards in, the full-batch gradient (numpy) out."""
+        import numpy as np
+
+        gy = np.ascontiguousarray(gy, dtype=np.float32)
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        Sg, fo, gr, gc = gy.shape
+        Sx, f, xr, xc = x.shape
+        k = xr - gr + 1 if gr <= xr else 1
+        gw = np.zeros((fo, f, k, k), dtype=np.float32)
+        code = _native.lib().fftconv_b200_grad_weight_sharded_host(
+            self.ws._h, gy.ctypes.data_as(C.c_void_p), Sg, fo, gr, gc, x.ctypes.data_as(C.c_void_p), Sx, f, xr,
+            xc, gw.ctypes.data_as(C.c_void_p), self.comm.handle, 1)
+        raise_for_status(code, _native.last_error(self.ws._h))
         return gw
 
     def comm_ms(self):

@@ -219,5 +219,18 @@ int main() {
               fftconv::grad_weight_direct(to64(gy), to64(x))) < 1e-5);
   }
   std::printf("dropin_test: %d checks, %d failures\n", g_checks, g_fail);
+  {  // grad_weight_sharded on a one-rank communicator: the shard is the whole
+     // minibatch, so the summed gradient equals grad_weight bit for bit
+     // (conv_direct_test.cpp:186-212 batch decomposability)
+    const LayerConfig c{5, 16, 3, 4, 6};
+    WS ws({c});
+    auto x = random_tensor<float>(6, 3, 16, 80, fftconv::TensorRole::input);
+    auto gy = random_tensor<float>(6, 4, 12, 81, fftconv::TensorRole::grad_output);
+    void* comm = fftconv::b200::nccl_comm_create(fftconv::b200::nccl_unique_id(), 1, 0, 0);
+    auto full = ws.grad_weight(gy, x);
+    auto sh = ws.grad_weight_sharded(gy, x, comm);
+    for (std::size_t i = 0; i < full.size(); ++i) CHECK(full.data()[i] == sh.data()[i]);
+    fftconv::b200::nccl_comm_destroy(comm);
+  }
   return g_fail == 0 ? 0 : 1;
 }

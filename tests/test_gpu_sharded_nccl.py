@@ -110,3 +110,17 @@ def test_run_iteration_through_sharded_accgrad(dev, comm):
     for a, b in zip(dp.conv_weight_grads, plain.conv_weight_grads):
         assert torch.equal(a, b)
     assert torch.equal(dp.fc_weight_grad, plain.fc_weight_grad)
+
+
+def test_sharded_host_buffers(comm):
+    """fftconv_b200_grad_weight_sharded_host (the drop-in's Tensor4 storage):
+    numpy shards in, the all-reduced gradient out; an empty shard gives zeros."""
+    cfg = LayerConfig(7, 32, 24, 20, 10)
+    x, gy = _inputs(cfg, 63)
+    ws = ConvWorkspace([cfg])
+    ref = ws.grad_weight(gy, x)  # host path
+    got = ShardedConv(ws, comm=comm).grad_weight(gy, x)
+    assert isinstance(got, np.ndarray) and np.array_equal(got, ref)
+    ez = ShardedConv(ws, comm=comm).grad_weight(np.zeros((0, 20, 26, 26), np.float32),
+                                                 np.zeros((0, 24, 32, 32), np.float32))
+    assert ez.shape == (20, 24, 7, 7) and not ez.any()
