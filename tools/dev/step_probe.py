@@ -36,8 +36,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="paper")
     ap.add_argument("--reps", type=int, default=30)
+    ap.add_argument("--S", type=int, default=0, help="override the batch (a strong-scaling shard)")
     a = ap.parse_args()
     (k, n, f, fo, S), _ = bench.parse_config(a.config)
+    S = a.S or S
     no = n - k + 1
     dev = torch.device("cuda:0")
     x = torch.from_numpy(fill_uniform((S, f, n, n), 1234, 1)).to(dev)
