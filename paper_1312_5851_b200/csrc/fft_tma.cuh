@@ -496,10 +496,9 @@ struct TC2R {
   static constexpr int THREADS = 32 + NPIPE * (P1W + P2W);
   static constexpr int TW = S * STAGE + 4 * S * 8;  // inverse twiddle table e^(+2 pi i k / M), M float2
   static constexpr int SMEM = TW + M * 8 + 128;
-  // small crops (weight gradients): pass 2 evaluates each output as a direct
-  // Hermitian DFT over u, one (plane, row, column) per item, instead of one
-  // FFT per column (pair) that would leave most pass-2 threads idle
-  static constexpr int DFT_MAX_ITEMS = 4;  // per pass-2 thread
+  // small crops (weight gradients, crop <= M/4): pass 2 evaluates each
+  // output as a direct Hermitian DFT over u, one thread per (plane, column),
+  // instead of one FFT per column (pair) producing mostly discarded rows
   static constexpr uint32_t BOX_BYTES = 2 * G * 4 * M;  // one u row
   static_assert(G * tile_plane_stride(M) * 4 <= STAGE, "a staged output tile must fit a stage");
 };
@@ -516,17 +515,14 @@ __global__ void __launch_bounds__(TC2R<M>::THREADS, 1)
   uint64_t* mid = full + S;
   uint64_t* empty = mid + S;  // pass 2 read the stage (direct-store mode)
   uint64_t* outb = empty + S;  // pass 2 wrote the output tile (bulk mode)
-  float2* twt = reinterpret_cast<float2*>(smem + T::TW);
   const int ngj = (p.J + G - 1) / G;
   const int ngroups = p.R * ngj;
   const int crop = p.crop;
-  const bool dft2 = crop <= M / 4 && G * crop * crop <= T::DFT_MAX_ITEMS * T::P2W;
+  const bool dft2 = crop <= M / 4 && G * crop <= T::P2W;
   // output-tile plane stride (floats): 16-B aligned for the bulk stores and
   // an odd number of 16-B units, so the plane-fastest pass-2 lanes spread
   // over the banks (a 32 x 32 crop at stride 1024 put 16 planes on one bank)
   const int pst = tile_plane_stride(crop);
-  if (threadIdx.x == 32)
-    static_for<0, M>([&](auto K) { twt[decltype(K)::value] = tw128c<true, decltype(K)::value * (128 / M)>(); });
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
@@ -667,39 +663,43 @@ __global__ void __launch_bounds__(TC2R<M>::THREADS, 1)
       if (dft2) {
         // x[y] = Re Z[0] + (-1)^y Re Z[M/2] + 2 sum_{0<u<M/2} Re(Z[u] e^(2 pi i u y / M))
         // (the imaginary parts of Z[0] and Z[M/2] are dropped, as c2r does).
-        // Items (plane, y, c) with the plane fastest: a half-warp reads one
-        // (y, c) of G planes -- distinct banks (odd plane stride PS) -- and
-        // shares y (twiddle-table broadcasts).  Measured: the column-fastest
-        // order hit 3-4-way bank conflicts and bounded accGrad's K4.
-        const int items = G * crop * crop;
-        float res[T::DFT_MAX_ITEMS];
-#pragma unroll
-        for (int q = 0; q < T::DFT_MAX_ITEMS; ++q) {
-          const int it = t + q * T::P2W;
-          res[q] = 0.f;
-          const int jl = it % G, rest = it / G;
-          if (it < items && jl < jv) {
-            const int y = rest / crop, c = rest - y * crop;
-            const float2* col = inter + jl * PS + c;
-            float acc = 0.f;
-            static_for<1, M / 2>([&](auto U) {
-              constexpr int u = decltype(U)::value;
-              const float2 z = col[u * CP];
-              const float2 w = twt[(u * y) & (M - 1)];
-              acc = fmaf(z.x, w.x, fmaf(-z.y, w.y, acc));
-            });
-            const float e = col[0].x + ((y & 1) ? -col[(M / 2) * CP].x : col[(M / 2) * CP].x);
-            res[q] = (e + 2.f * acc) * scale;
-          }
+        // One thread per (plane, output column c), plane fastest (a half-warp
+        // reads one column of G planes: distinct banks at the odd plane
+        // stride): the column's M/2 + 1 values are loaded once and every row
+        // y < crop <= M/4 is a direct Hermitian DFT with the twiddles
+        // e^(2 pi i u y / M) as instruction immediates.  (Per-(plane, y, c)
+        // items re-read the column and a twiddle table for each y: ~3
+        // shared-memory wavefronts per term bounded accGrad's K4, ~3.5k
+        // cycles per 16-plane group.)
+        constexpr int YMAX = M / 4;
+        const int jl = t % G, c = t / G;
+        const bool act = jl < jv && c < crop;
+        float res[YMAX];
+        if (act) {
+          const float2* col = inter + jl * PS + c;
+          float2 z[M / 2 + 1];
+          static_for<0, M / 2 + 1>([&](auto U) { z[decltype(U)::value] = col[decltype(U)::value * CP]; });
+          static_for<0, YMAX>([&](auto Y) {
+            constexpr int y = decltype(Y)::value;
+            if (y < crop) {
+              float acc = 0.f;
+              static_for<1, M / 2>([&](auto U) {
+                constexpr int u = decltype(U)::value;
+                const float2 w = tw128c<true, (u * y * (128 / M)) % 128>();
+                acc = fmaf(z[u].x, w.x, fmaf(-z[u].y, w.y, acc));
+              });
+              const float e = z[0].x + ((y & 1) ? -z[M / 2].x : z[M / 2].x);
+              res[y] = (e + 2.f * acc) * scale;
+            }
+          });
         }
         named_bar_sync(1 + T::NPIPE + pipe, T::P2W);  // stage read: reuse it as the output tile
         float* tile = reinterpret_cast<float*>(smem + s * T::STAGE);
-#pragma unroll
-        for (int q = 0; q < T::DFT_MAX_ITEMS; ++q) {
-          const int it = t + q * T::P2W;
-          const int jl = it % G, rest = it / G;
-          if (it < items && jl < jv) tile[jl * pst + rest] = res[q];
-        }
+        if (act)
+          static_for<0, YMAX>([&](auto Y) {
+            constexpr int y = decltype(Y)::value;
+            if (y < crop) tile[jl * pst + y * crop + c] = res[y];
+          });
         if (p.bulk) {
           fence_proxy_async_smem();
           mbar_arrive(&outb[s]);
