@@ -65,7 +65,10 @@ __device__ long long g_xform_trace[6][64];
 __host__ __device__ constexpr int stores_inflight(int stages) { return stages >= 6 ? 1 : 0; }
 
 #ifndef FCB_R2C_G
-#define FCB_R2C_G 8  // planes per K1 group at m <= 32
+#define FCB_R2C_G 8  // planes per K1 group at m = 32
+#endif
+#ifndef FCB_R2C_G_SMALL
+#define FCB_R2C_G_SMALL 16  // planes per K1 group at m <= 16 (full 128-B lines; n=16 sweep step 122 -> 111 us vs 8)
 #endif
 
 // Independent pass-1/pass-2 pipelines: the largest of 4, 2, 1 that divides
@@ -104,7 +107,7 @@ struct TR2C {
   // planes (K indices) per group: 8 (64-B spectrum segments; a 16-plane
   // group made 72-KB stages, only 3 of which fit, too shallow to hide the
   // ~4.5k-cycle load latency under load), 4 at m = 64
-  static constexpr int G = BIG ? 4 : FCB_R2C_G;
+  static constexpr int G = BIG ? 4 : (M <= 16 ? FCB_R2C_G_SMALL : FCB_R2C_G);
   static constexpr int PC = M / 2 + 1;
   static constexpr int CP = M + 1;        // intermediate row stride (float2)
   static constexpr int BINS = M * PC;
