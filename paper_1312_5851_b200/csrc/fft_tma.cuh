@@ -67,6 +67,15 @@ __host__ __device__ constexpr int stores_inflight(int stages) { return stages >=
 #ifndef FCB_R2C_G
 #define FCB_R2C_G 8  // planes per K1 group at m = 32
 #endif
+#ifndef FCB_R2C_G_BIG
+#define FCB_R2C_G_BIG 4  // planes per K1 group at m = 64
+#endif
+#ifndef FCB_C2R_G_BIG
+#define FCB_C2R_G_BIG 4  // planes per K4 group at m = 64
+#endif
+#ifndef FCB_BIG_NPIPE
+#define FCB_BIG_NPIPE 0  // 1: two pass pipelines at m = 64 when the stage count allows
+#endif
 #ifndef FCB_R2C_G_SMALL
 #define FCB_R2C_G_SMALL 16  // planes per K1 group at m <= 16 (full 128-B lines; n=16 sweep step 122 -> 111 us vs 8)
 #endif
@@ -107,7 +116,7 @@ struct TR2C {
   // planes (K indices) per group: 8 (64-B spectrum segments; a 16-plane
   // group made 72-KB stages, only 3 of which fit, too shallow to hide the
   // ~4.5k-cycle load latency under load), 4 at m = 64
-  static constexpr int G = BIG ? 4 : (M <= 16 ? FCB_R2C_G_SMALL : FCB_R2C_G);
+  static constexpr int G = BIG ? FCB_R2C_G_BIG : (M <= 16 ? FCB_R2C_G_SMALL : FCB_R2C_G);
   static constexpr int PC = M / 2 + 1;
   static constexpr int CP = M + 1;        // intermediate row stride (float2)
   static constexpr int BINS = M * PC;
@@ -126,7 +135,7 @@ struct TR2C {
   // independent pass-1/pass-2 pipelines on alternating groups (an even
   // stage count keeps every stage in one parity class, so no mbarrier
   // phase is ever shared between the pipelines)
-  static constexpr int NPIPE = BIG ? 1 : npipe_for(S, 32, P1W + P2W);
+  static constexpr int NPIPE = (BIG && !FCB_BIG_NPIPE) ? 1 : npipe_for(S, 32, P1W + P2W);
   static constexpr int THREADS = 32 + NPIPE * (P1W + P2W);
   static constexpr int SMEM = S * STAGE + 3 * S * 8 + 128;
   // output tile stores: NBOX boxes of BT bins x G planes
@@ -481,7 +490,7 @@ __device__ __forceinline__ void c2r_store_tile(const float* tile, int pst, int j
 template <int M>
 struct TC2R {
   static constexpr bool BIG = (M == 64);
-  static constexpr int G = BIG ? 4 : FCB_C2R_G;
+  static constexpr int G = BIG ? FCB_C2R_G_BIG : FCB_C2R_G;
   static constexpr int PC = M / 2 + 1;
   static constexpr int CP = M + 1;  // intermediate row stride (float2), >= crop
   static constexpr int PS = BIG ? PC * CP + ((4 - (PC * CP) % 16) + 16) % 16 : ((PC * CP) | 1);
@@ -495,7 +504,7 @@ struct TC2R {
   static constexpr int P1 = BIG ? G * PC * 2 : G * PC;  // (plane, u[, half]) row items
   static constexpr int P2 = BIG ? G * M : G * (M / 2);  // column (pair) items
   static constexpr int P1W = ceil32_i(P1), P2W = ceil32_i(P2);
-  static constexpr int NPIPE = (!BIG && S % 2 == 0) ? 2 : 1;
+  static constexpr int NPIPE = ((!BIG || FCB_BIG_NPIPE) && S % 2 == 0) ? 2 : 1;
   static constexpr int THREADS = 32 + NPIPE * (P1W + P2W);
   static constexpr int TW = S * STAGE + 4 * S * 8;  // inverse twiddle table e^(+2 pi i k / M), M float2
   static constexpr int SMEM = TW + M * 8 + 128;
