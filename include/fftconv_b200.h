@@ -218,6 +218,17 @@ int fftconv_b200_ifft_2d_real_batch(const float* spec, size_t planes_count, size
 int fftconv_b200_set_stage_timing(fftconv_b200_ws* ws, int enable);
 int fftconv_b200_stage_ms(fftconv_b200_ws* ws, float out[4]);
 
+/* Live kernel spans with the programmatic-dependent-launch chain intact (no
+ * events between the kernels): when enabled (synchronises the device and
+ * clears up to 128 operator slots), each operator's K1 / K3 / K4 (TMA
+ * kernels, m in 4..64) record, on the GPU's global timer, the first CTA past
+ * its dependency wait and the last CTA done.  fftconv_b200_span_ms writes
+ * out[3 i + k] (ms; -1 where not recorded) for the first min(ops, max_ops)
+ * operators since enabling and returns that count (negative status on
+ * error). */
+int fftconv_b200_set_span_timing(fftconv_b200_ws* ws, int enable);
+int fftconv_b200_span_ms(fftconv_b200_ws* ws, float* out, int max_ops);
+
 /* Number of kernel launches the last operator call enqueued. */
 int fftconv_b200_last_launch_count(const fftconv_b200_ws* ws);
 

@@ -47,6 +47,8 @@ SIGNATURES = [
     ("fftconv_b200_set_stage_timing", _i, [_p, _i]),
     ("fftconv_b200_stage_ms", _i, [_p, _p]),
     ("fftconv_b200_last_launch_count", _i, [_p]),
+    ("fftconv_b200_set_span_timing", _i, [_p, _i]),
+    ("fftconv_b200_span_ms", _i, [_p, _p, _i]),
     ("fftconv_b200_relu_forward", _i, [_p, _p, _sz, _p]),
     ("fftconv_b200_relu_backward", _i, [_p, _p, _p, _sz, _p]),
     ("fftconv_b200_maxpool_forward", _i, [_p, _sz, _sz, _sz, _p, _p, _p]),

@@ -78,6 +78,7 @@ struct GemmParams {
   // (the 3xTF32 fallback of the same launch pair)
   int select;
   int* path;  // optional: the kernel that runs writes 1 (fp16x3) or 0 (3xTF32)
+  unsigned long long* tspan = nullptr;  // live span slot (ptx.cuh)
 };
 
 // fp16x3 keeps ~2^-20 row-relative accuracy for rows within 2^18 of the
@@ -262,6 +263,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   }
   if (p.path && blockIdx.x == 0 && threadIdx.x == 0) *p.path = F16 ? 1 : 0;
+  span_begin(p.tspan);  // the kernel of an auto pair that runs
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
@@ -551,6 +553,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 
   __syncthreads();
+  span_end(p.tspan);
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, kTmemCols);

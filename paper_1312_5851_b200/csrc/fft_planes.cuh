@@ -301,6 +301,7 @@ struct R2CParams {
 struct R2CPair {
   R2CParams op[2];
   int n;  // 1 or 2 operands
+  unsigned long long* tspan = nullptr;  // live span slot (ptx.cuh span_begin / span_end)
 };
 
 // grid = (kpad/G, R, ceil((M/2+1)/UC)), block = PlaneTraits<M>::THREADS.
@@ -441,6 +442,7 @@ struct C2RParams {
   // while the next chunk transforms).  jbase is a multiple of the group size.
   int jbase = 0;
   int J_all = 0;  // 0: J
+  unsigned long long* tspan = nullptr;  // live span slot (TMA K4 only)
 };
 
 // grid = (ceil(J/G), R, ceil(crop/cc)), block = PlaneTraits<M>::THREADS.

@@ -206,6 +206,7 @@ __global__ void __launch_bounds__(TR2C<M>::THREADS, 1)
   }
   __syncthreads();
   pdl_wait();
+  span_begin(P.tspan);
   pdl_trigger();
 
   if (threadIdx.x < 32) {
@@ -433,6 +434,10 @@ __global__ void __launch_bounds__(TR2C<M>::THREADS, 1)
       }
     }
   }
+  if (P.tspan) {  // uniform: the whole CTA is done
+    __syncthreads();
+    span_end(P.tspan);
+  }
 #ifdef FCB_XFORM_TRACE
   __syncthreads();
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -547,6 +552,7 @@ __global__ void __launch_bounds__(TC2R<M>::THREADS, 1)
   }
   __syncthreads();
   pdl_wait();
+  span_begin(p.tspan);
   pdl_trigger();
 
   if (threadIdx.x < 32) {
@@ -834,6 +840,10 @@ __global__ void __launch_bounds__(TC2R<M>::THREADS, 1)
         }
       }
     }
+  }
+  if (p.tspan) {
+    __syncthreads();
+    span_end(p.tspan);
   }
 #ifdef FCB_XFORM_TRACE
   __syncthreads();

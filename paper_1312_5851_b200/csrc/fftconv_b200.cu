@@ -267,8 +267,9 @@ static void launch_r2c_tma(const R2CPair& P, const DevInfo& di, cudaStream_t st)
 // Both forward transforms of an operator (one launch at m >= 4; operand A's
 // groups first, then B's).  Returns the number of launches.
 static int launch_r2c_both(size_t m, const R2CParams& a, const R2CParams& b, cudaStream_t st,
-                           const DevInfo& di) {
-  const R2CPair P{{a, b}, 2};
+                           const DevInfo& di, unsigned long long* tspan = nullptr) {
+  R2CPair P{{a, b}, 2};
+  P.tspan = tspan;
   switch (m) {
     case 1: launch_r2c_small<1>(a, st); launch_r2c_small<1>(b, st); return 2;
     case 2: launch_r2c_small<2>(a, st); launch_r2c_small<2>(b, st); return 2;
@@ -488,7 +489,7 @@ static GemmRoute gemm_route(int kind, size_t M, size_t N, size_t K) {
 static void launch_gemm_kernel(const float* A, const float* B, float* out, size_t bins, size_t M, size_t N,
                                size_t kpad, float im_sign, OutLayout lay, size_t ldm, const DevInfo& di,
                                cudaStream_t st, bool f16, int select, const unsigned long long* amax_a,
-                               const unsigned long long* amax_b, int* path);
+                               const unsigned long long* amax_b, int* path, unsigned long long* tspan = nullptr);
 
 // Returns the number of launches (2 for an auto pair).  amax_* (K1's per-row
 // words, rows_* rows) are required for the fp16 routes; without them the
@@ -497,22 +498,23 @@ static int launch_gemm(const float* A, const float* B, float* out, size_t bins, 
                        size_t kpad, float im_sign, OutLayout lay, size_t ldm, const DevInfo& di,
                        cudaStream_t st, GemmRoute route = kRouteTf32,
                        const unsigned long long* amax_a = nullptr, const unsigned long long* amax_b = nullptr,
-                       int* path = nullptr) {
+                       int* path = nullptr, unsigned long long* tspan = nullptr) {
   if (!amax_a || !amax_b) route = kRouteTf32;
   if (route == kRouteAuto) {
-    launch_gemm_kernel(A, B, out, bins, M, N, kpad, im_sign, lay, ldm, di, st, true, 1, amax_a, amax_b, path);
-    launch_gemm_kernel(A, B, out, bins, M, N, kpad, im_sign, lay, ldm, di, st, false, 2, amax_a, amax_b, path);
+    launch_gemm_kernel(A, B, out, bins, M, N, kpad, im_sign, lay, ldm, di, st, true, 1, amax_a, amax_b, path, tspan);
+    launch_gemm_kernel(A, B, out, bins, M, N, kpad, im_sign, lay, ldm, di, st, false, 2, amax_a, amax_b, path,
+                       tspan);
     return 2;
   }
   launch_gemm_kernel(A, B, out, bins, M, N, kpad, im_sign, lay, ldm, di, st, route == kRouteF16, 0, amax_a,
-                     amax_b, path);
+                     amax_b, path, tspan);
   return 1;
 }
 
 static void launch_gemm_kernel(const float* A, const float* B, float* out, size_t bins, size_t M, size_t N,
                                size_t kpad, float im_sign, OutLayout lay, size_t ldm, const DevInfo& di,
                                cudaStream_t st, bool f16, int select, const unsigned long long* amax_a,
-                               const unsigned long long* amax_b, int* path) {
+                               const unsigned long long* amax_b, int* path, unsigned long long* tspan) {
   const GemmGeom g = gemm_geom(M, N, di, f16);
   CUtensorMap ta = make_operand_map(A, kpad, M, bins, kTileM);
   CUtensorMap tb = make_operand_map(B, kpad, N, bins, (uint32_t)g.nc);
@@ -533,6 +535,7 @@ static void launch_gemm_kernel(const float* A, const float* B, float* out, size_
   p.rows_b = (int)N;
   p.select = select;
   p.path = path;
+  p.tspan = tspan;
   p.gm_log2 = 4;
   if (lay == kBinMajor) {
     p.s_t = (long long)N * ldm;
@@ -732,6 +735,12 @@ struct fftconv_b200_ws {
   cudaEvent_t comm_ev[3] = {};
   bool comm_ready = false;
   bool comm_timed = false;
+  // live kernel spans (fftconv_b200_set_span_timing): per operator, K1 / K3 /
+  // K4 start and end words (ptx.cuh kSpanSlots operators per batch)
+  unsigned long long* spans = nullptr;
+  int span_on = 0;
+  int span_next = 0;
+  unsigned long long* span_slot(int k) { return span_on ? spans + (size_t)(span_next % kSpanSlots) * 3 + k : nullptr; }
   std::string last_error;
   bool timing = false;
   cudaEvent_t ev[5] = {};
@@ -903,13 +912,15 @@ int r2c_operands(fftconv_b200_ws* ws, size_t m, R2CParams& a, R2CParams& b, cuda
     a.epoch = b.epoch = ++ws->epoch;
   }
   if (m == kL) return launch_r2c_large(a, ws->lscr, ws->lscr_n, st) + launch_r2c_large(b, ws->lscr, ws->lscr_n, st);
-  return launch_r2c_both(m, a, b, st, ws->di);
+  return launch_r2c_both(m, a, b, st, ws->di, ws->span_slot(0));
 }
 
 // K4 for any supported m; returns the number of launches.
 int c2r_run(fftconv_b200_ws* ws, size_t m, const C2RParams& c, cudaStream_t st) {
   if (m == kL) return launch_c2r_large(c, ws->lscr, ws->lscr_n, st);
-  launch_c2r(m, c, st, ws->di);
+  C2RParams cs = c;
+  cs.tspan = ws->span_slot(2);
+  launch_c2r(m, cs, st, ws->di);
   return 1;
 }
 
@@ -941,10 +952,10 @@ void run_forward(fftconv_b200_ws* ws, const float* x, size_t S, size_t f, size_t
   int ng;
   if (!gemm_swap(S, fo)) {  // D[t][o][b]: planes (r = o, j = b)
     ng = launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, S, fo, kp, 1.0f, c2r_layout(m), round_up(S, 2),
-                     ws->di, st, route, a.amax, b.amax, ws->gemm_path);
+                     ws->di, st, route, a.amax, b.amax, ws->gemm_path, ws->span_slot(1));
   } else {  // D^T[t][b][o]: planes (r = b, j = o)
     ng = launch_gemm(ws->bufB, ws->bufA, ws->bufD, bins, fo, S, kp, -1.0f, c2r_layout(m), round_up(fo, 2),
-                     ws->di, st, route, b.amax, a.amax, ws->gemm_path);
+                     ws->di, st, route, b.amax, a.amax, ws->gemm_path, ws->span_slot(1));
     c = C2RParams{ws->bufD, y, (long long)(fo * no * no), (long long)(no * no), (int)S, (int)fo,
                   (int)no, 0, 0, 1.0f / (float)(m * m), (int)round_up(fo, 2)};
   }
@@ -953,6 +964,7 @@ void run_forward(fftconv_b200_ws* ws, const float* x, size_t S, size_t f, size_t
   const int nc = c2r_run(ws, m, c, st);
   record(ws, 4, st);
   ws->last_launches = nl + ng + nc;
+  if (ws->span_on) ++ws->span_next;
   ws->ctr[0] += S * f + fo * f;
   ws->ctr[1] += S * fo;
   ws->ctr[2] += (uint64_t)bins * fo * f * S;
@@ -987,10 +999,10 @@ void run_grad_input(fftconv_b200_ws* ws, const float* gy, size_t S, size_t fo, s
   int ng;
   if (!gemm_swap(S, f)) {  // D[t][f][b]
     ng = launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, S, f, kp, 1.0f, c2r_layout(m), round_up(S, 2),
-                     ws->di, st, route, a.amax, b.amax, ws->gemm_path);
+                     ws->di, st, route, a.amax, b.amax, ws->gemm_path, ws->span_slot(1));
   } else {  // D^T[t][b][f]
     ng = launch_gemm(ws->bufB, ws->bufA, ws->bufD, bins, f, S, kp, -1.0f, c2r_layout(m), round_up(f, 2),
-                     ws->di, st, route, b.amax, a.amax, ws->gemm_path);
+                     ws->di, st, route, b.amax, a.amax, ws->gemm_path, ws->span_slot(1));
     c = C2RParams{ws->bufD, gx, (long long)(f * n * n), (long long)(n * n), (int)S, (int)f, (int)n,
                   0, 0, 1.0f / (float)(m * m), (int)round_up(f, 2)};
   }
@@ -999,6 +1011,7 @@ void run_grad_input(fftconv_b200_ws* ws, const float* gy, size_t S, size_t fo, s
   const int nc = c2r_run(ws, m, c, st);
   record(ws, 4, st);
   ws->last_launches = nl + ng + nc;
+  if (ws->span_on) ++ws->span_next;
   ws->ctr[0] += S * fo + fo * f;
   ws->ctr[1] += S * f;
   ws->ctr[2] += (uint64_t)bins * fo * f * S;
@@ -1039,7 +1052,7 @@ void run_grad_weight(fftconv_b200_ws* ws, const float* gy, size_t Sg, size_t fo,
   record(ws, 1, st);  // both forward transforms
   record(ws, 2, st);
   const int ng = launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, fo, f, kp, -1.0f, c2r_layout(m), round_up(fo, 2),
-                             ws->di, st, route, a.amax, b.amax, ws->gemm_path);
+                             ws->di, st, route, a.amax, b.amax, ws->gemm_path, ws->span_slot(1));
   record(ws, 3, st);
   C2RParams c{ws->bufD, gw, (long long)(k * k), (long long)(f * k * k), (int)f, (int)fo, (int)k,
               0, 0, 1.0f / (float)(m * m), (int)round_up(fo, 2)};
@@ -1068,6 +1081,7 @@ void run_grad_weight(fftconv_b200_ws* ws, const float* gy, size_t Sg, size_t fo,
   }
   record(ws, 4, st);
   ws->last_launches = nl + ng + nc;
+  if (ws->span_on) ++ws->span_next;
   ws->ctr[0] += S * f + S * fo;
   ws->ctr[1] += fo * f;
   ws->ctr[2] += (uint64_t)bins * fo * f * S;
@@ -1156,6 +1170,7 @@ void fftconv_b200_ws_destroy(fftconv_b200_ws* ws) {
     if (ws->ev_ready)
       for (auto& e : ws->ev) cudaEventDestroy(e);
     if (ws->done_ev) cudaEventDestroy(ws->done_ev);
+    if (ws->spans) cudaFree(ws->spans);
     if (ws->comm_ready) {
       cudaStreamDestroy(ws->comm_stream);
       for (auto& e : ws->chunk_ev) cudaEventDestroy(e);
@@ -1604,6 +1619,41 @@ int fftconv_b200_stage_ms(fftconv_b200_ws* ws, float out[4]) {
     FCB_CUDA(cudaEventSynchronize(ws->ev[4]));
     for (int i = 0; i < 4; ++i) FCB_CUDA(cudaEventElapsedTime(&out[i], ws->ev[i], ws->ev[i + 1]));
   });
+}
+
+int fftconv_b200_set_span_timing(fftconv_b200_ws* ws, int enable) {
+  if (!ws) return FFTCONV_B200_INVALID_ARGUMENT;
+  return guarded(ws, [&] {
+    DeviceGuard g(ws->device);
+    ws->span_on = 0;
+    if (!enable) return;
+    const size_t words = 2 * 3 * (size_t)kSpanSlots;
+    if (!ws->spans) FCB_CUDA(cudaMalloc(&ws->spans, words * sizeof(unsigned long long)));
+    FCB_CUDA(cudaDeviceSynchronize());
+    FCB_CUDA(cudaMemset(ws->spans, 0xff, words / 2 * sizeof(unsigned long long)));  // starts: +inf
+    FCB_CUDA(cudaMemset(ws->spans + words / 2, 0, words / 2 * sizeof(unsigned long long)));
+    ws->span_next = 0;
+    ws->span_on = 1;
+  });
+}
+
+int fftconv_b200_span_ms(fftconv_b200_ws* ws, float* out, int max_ops) {
+  if (!ws || !out) return -FFTCONV_B200_INVALID_ARGUMENT;
+  int n = -FFTCONV_B200_INVALID_ARGUMENT;
+  const int code = guarded(ws, [&] {
+    if (!ws->spans) throw Error(FFTCONV_B200_INVALID_ARGUMENT, "span timing never enabled");
+    DeviceGuard g(ws->device);
+    FCB_CUDA(cudaDeviceSynchronize());
+    std::vector<unsigned long long> h(2 * 3 * (size_t)kSpanSlots);
+    FCB_CUDA(cudaMemcpy(h.data(), ws->spans, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    n = std::min({ws->span_next, kSpanSlots, max_ops});
+    for (int i = 0; i < n; ++i)
+      for (int k = 0; k < 3; ++k) {
+        const unsigned long long b = h[(size_t)i * 3 + k], e = h[(size_t)kSpanEndOff + (size_t)i * 3 + k];
+        out[i * 3 + k] = (b == ~0ull || e == 0 || e < b) ? -1.f : (float)((e - b) * 1e-6);
+      }
+  });
+  return code == FFTCONV_B200_OK ? n : -code;
 }
 
 int fftconv_b200_last_launch_count(const fftconv_b200_ws* ws) {

@@ -55,6 +55,23 @@ __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// Live kernel spans with the PDL chain intact (fftconv_b200_set_span_timing):
+// the first CTA past its dependency wait and the last CTA done, on the
+// global timer (ns).  Start words at s[0], end words at s[kSpanEndOff].
+constexpr int kSpanSlots = 128;                 // operators per timing batch
+constexpr int kSpanEndOff = 3 * kSpanSlots;     // start words, then end words
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void span_begin(unsigned long long* s) {
+  if (s && threadIdx.x == 0) atomicMin(s, global_ns());
+}
+__device__ __forceinline__ void span_end(unsigned long long* s) {  // after __syncthreads()
+  if (s && threadIdx.x == 0) atomicMax(s + kSpanEndOff, global_ns());
+}
+
 // Generic-proxy smem writes -> visible to the async proxy (UMMA reads).
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

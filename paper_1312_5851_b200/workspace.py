@@ -130,6 +130,19 @@ class ConvWorkspace:
         raise_for_status(code, _native.last_error(self._h))
         return [float(v) for v in out]
 
+    def set_span_timing(self, enable: bool) -> None:
+        """Live per-kernel spans with the PDL chain intact (include/fftconv_b200.h)."""
+        code = _native.lib().fftconv_b200_set_span_timing(self._h, int(bool(enable)))
+        raise_for_status(code, _native.last_error(self._h))
+
+    def span_ms(self, max_ops: int = 128):
+        """[(k1_ms, gemm_ms, k4_ms)] per operator since set_span_timing(True); None where not recorded."""
+        out = (C.c_float * (3 * max_ops))()
+        n = int(_native.lib().fftconv_b200_span_ms(self._h, out, max_ops))
+        if n < 0:
+            raise_for_status(-n, _native.last_error(self._h))
+        return [tuple(None if out[3 * i + k] < 0 else float(out[3 * i + k]) for k in range(3)) for i in range(n)]
+
     def last_gemm_path(self) -> str | None:
         """Which GEMM kernel ran in the last call: "f16x3", "tf32x3" or None
         (synchronises the device; include/fftconv_b200.h)."""
