@@ -86,3 +86,29 @@ def test_per_workspace_gemm_kind(dev):
     for y in (ya, yb):
         assert oracle.rel_l2_error(y.cpu().numpy(), ref) <= 1e-4
     assert a.set_gemm_kind(None) == "f16x3"
+
+
+def test_live_spans_cover_each_kernel(dev):
+    """fftconv_b200_set_span_timing: every operator's K1 / K3 / K4 span is
+    recorded, positive, and together no longer than the operator's event
+    time (the spans exclude the launch hand-offs)."""
+    import torch
+
+    cfg = LayerConfig(7, 32, 48, 40, 32)
+    ws = ConvWorkspace([cfg])
+    x, w, gy = _inputs(cfg, 44)
+    xd, wd, gyd = (torch.from_numpy(a).to(dev) for a in (x, w, gy))
+    ws.forward(xd, wd)
+    ws.set_span_timing(True)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    ws.forward(xd, wd)
+    ws.grad_input(gyd, wd)
+    ws.grad_weight(gyd, xd)
+    b.record()
+    spans = ws.span_ms()
+    ws.set_span_timing(False)
+    assert len(spans) == 3
+    for sp in spans:
+        assert all(v is not None and v > 0 for v in sp), spans
+    assert sum(sum(sp) for sp in spans) <= a.elapsed_time(b) * 1.05
