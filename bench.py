@@ -626,7 +626,7 @@ def main():
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
-        dist.destroy_process_group()
+        _teardown(sc.comm if sc is not None else None)
 
 
 def run_stack(args):
@@ -719,7 +719,7 @@ def run_stack(args):
     ms = sum(per.values())
     if rank != 0:
         if world > 1:
-            dist.destroy_process_group()
+            _teardown(comm)
         return
     line = dict(base, value=ms, ms_per_step=ms, per_category_ms=per,
                 wall_ms_incl_param_upload=statistics.mean(wall), loss=r.loss, grad_checksum=r.grad_checksum,
@@ -728,7 +728,20 @@ def run_stack(args):
                      "B200 kernels, relu/pool/fit_to on the layer-stack kernels, fc on fp32 cuBLAS")
     print(json.dumps(line), flush=True)
     if world > 1:
-        dist.destroy_process_group()
+        _teardown(comm)
+
+
+def _teardown(comm):
+    """Every rank destroys the library's NCCL communicator while all ranks are
+    still alive, then the process group."""
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.synchronize()
+    if comm is not None:
+        dist.barrier()
+        comm.close()
+    dist.destroy_process_group()
 
 
 def ncu_traffic(kernel, config):
