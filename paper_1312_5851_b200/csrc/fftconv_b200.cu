@@ -32,6 +32,7 @@
 #include "fft_planes.cuh"
 #include "fft_large.cuh"
 #include "fft_tma.cuh"
+#include "fft_small.cuh"
 #include "layers.cuh"
 
 namespace fcb {
@@ -281,6 +282,49 @@ static int launch_r2c_both(size_t m, const R2CParams& a, const R2CParams& b, cud
     default: size_unsupported(m);
   }
   return 0;
+}
+
+// K1 for an operand of small planes (src <= m/4, m in {32, 64}): 16-plane
+// groups, full-line spectrum stores (fft_small.cuh).  FFTCONV_B200_SMALLSRC=0
+// turns it off (A/B, tests).
+static bool small_src_enabled() {
+  const char* e = getenv("FFTCONV_B200_SMALLSRC");
+  return !(e && atoi(e) == 0);
+}
+// m = 64 only: measured W 4.27 -> 3.87 ms and the n = 64 sweep point k = 7
+// 1.045 -> 1.011 ms, but P (m = 32, where K1's 8-plane groups already store
+// 64-B pieces) 265 -> 292 us.
+static bool small_src_ok(size_t m, const R2CParams& p) {
+  return small_src_enabled() && m == 64 && (size_t)p.src * 4 <= m && p.src >= 1;
+}
+template <int M>
+static void launch_r2c_small_src(const R2CParams& p, const DevInfo& di, cudaStream_t st, unsigned long long* tspan) {
+  using T = TSmall<M>;
+  auto kern = r2c_small_kernel<M>;
+  smem_optin(kern, T::SMEM);
+  const int groups = p.R * ((p.kpad + T::G - 1) / T::G);
+  const int grid = std::max(1, std::min(groups, di.sms));
+  const CUtensorMap tm = make_bin_map(p.out, p.kpad, p.R, (size_t)M * (M / 2 + 1), T::G, M);
+  launch_pdl(kern, dim3(grid), dim3(T::THREADS), T::SMEM, st, p, tm, tspan);
+}
+static void launch_r2c_small_any(size_t m, const R2CParams& p, const DevInfo& di, cudaStream_t st,
+                                 unsigned long long* tspan) {
+  if (m == 32) launch_r2c_small_src<32>(p, di, st, tspan);
+  else launch_r2c_small_src<64>(p, di, st, tspan);
+}
+
+static void launch_r2c_one_span(size_t m, const R2CParams& p, cudaStream_t st, const DevInfo& di,
+                                unsigned long long* tspan) {
+  R2CPair P{{p, p}, 1};
+  P.tspan = tspan;
+  switch (m) {
+    case 4: return launch_r2c_tma<4>(P, di, st);
+    case 8: return launch_r2c_tma<8>(P, di, st);
+    case 16: return launch_r2c_tma<16>(P, di, st);
+    case 32: return launch_r2c_tma<32>(P, di, st);
+    case 64: return launch_r2c_tma<64>(P, di, st);
+    default: size_unsupported(m);
+  }
 }
 
 static void launch_r2c_one(size_t m, const R2CParams& p, cudaStream_t st, const DevInfo& di) {
@@ -912,6 +956,15 @@ int r2c_operands(fftconv_b200_ws* ws, size_t m, R2CParams& a, R2CParams& b, cuda
     a.epoch = b.epoch = ++ws->epoch;
   }
   if (m == kL) return launch_r2c_large(a, ws->lscr, ws->lscr_n, st) + launch_r2c_large(b, ws->lscr, ws->lscr_n, st);
+  const bool sa = small_src_ok(m, a), sb = small_src_ok(m, b);
+  if (sa || sb) {  // the small-plane operand(s) through fft_small.cuh, the other through K1
+    unsigned long long* ts = ws->span_slot(0);
+    if (sa) launch_r2c_small_any(m, a, ws->di, st, ts);
+    else launch_r2c_one_span(m, a, st, ws->di, ts);
+    if (sb) launch_r2c_small_any(m, b, ws->di, st, ts);
+    else launch_r2c_one_span(m, b, st, ws->di, ts);
+    return 2;
+  }
   return launch_r2c_both(m, a, b, st, ws->di, ws->span_slot(0));
 }
 

@@ -14,6 +14,7 @@ from paper_1312_5851_b200.rng import fill_uniform  # noqa: E402
 
 cfg, op = sys.argv[1], sys.argv[2]
 (k, n, f, fo, S), _ = bench.parse_config(cfg)
+S = int(os.environ.get("TRACE_S", S))
 no = n - k + 1
 dev = torch.device("cuda:0")
 x = torch.from_numpy(fill_uniform((S, f, n, n), 1234, 1)).to(dev)
