@@ -28,6 +28,7 @@
 #include <cstdint>
 
 #include "fft_planes.cuh"
+#include "fft_tma.cuh"
 #include "ptx.cuh"
 
 namespace fcb {
@@ -201,6 +202,167 @@ __global__ void __launch_bounds__(256, 1)
   if (tspan) {
     __syncthreads();
     span_end(tspan);
+  }
+}
+
+}  // namespace fcb
+
+namespace fcb {
+
+// ---------------------------------------------------------------- K4, small crops
+// The c2r of accGrad's weight gradients (crop <= m/4, e.g. 11 x 11 kernels
+// in 64 x 64 planes) at m in {32, 64}, from the group-major product
+// P[r][J/16][t][16] (the GEMM writes it so for this kernel): every 16-plane
+// group's u row is one contiguous M x 128-B block, so the group streams in
+// as UC-row chunks through a ring of stages (full-line bulk loads, loads in
+// flight across groups), where c2r_tma_kernel at m = 64 holds 4-plane
+// groups and reads 32-B pieces per bin.
+//   pass 1  per chunk, (plane, u, half h): the inverse row FFT over v by one
+//           radix-2 DIF step, x = 2k + h, only the x < crop outputs kept ->
+//           the intermediate [plane][u][x] (crop columns: small)
+//   pass 2  per group, (plane, column x): direct Hermitian DFTs over u for
+//           every row y < crop, twiddles as immediates (as in c2r_tma_kernel)
+//           -> staged tile -> coalesced stores (optionally accumulated)
+template <int M>
+struct TC2RSmall {
+  static constexpr int G = 16;
+  static constexpr int PC = M / 2 + 1, H = M / 2;
+  static constexpr int UC = 8;                           // u rows per chunk
+  static constexpr int NCH = (PC + UC - 1) / UC;
+  static constexpr int STAGE = UC * M * G * 8;           // bytes
+  static constexpr int NST = (M == 64) ? 2 : 4;          // stages
+  static constexpr int CMAX = M / 4;                     // largest crop
+  static constexpr int IS = CMAX + 1;                    // intermediate row stride (float2)
+  static constexpr int IPS = (PC * IS) | 1;              // plane stride (odd)
+  static constexpr int INTER = G * IPS * 8;
+  static constexpr int PST = ((CMAX * CMAX + 3) / 4 % 2 == 0) ? ((CMAX * CMAX + 3) / 4 + 1) * 4
+                                                             : (CMAX * CMAX + 3) / 4 * 4;
+  static constexpr int TILE = G * PST * 4;
+  static constexpr int NC = 256;                         // compute threads
+  static constexpr int THREADS = 32 + NC;                // + the copy warp
+  static constexpr int SMEM = NST * STAGE + INTER + TILE + 2 * NST * 8 + 64;
+  static_assert(G * UC * 2 == NC && G * CMAX <= NC, "c2r_small thread mapping");
+};
+
+// grid = persistent (<= groups), block = THREADS, smem = SMEM.  p.gm must be
+// set (group-major product); groups g = (row r, 16-column group jg).
+template <int M>
+__global__ void __launch_bounds__(TC2RSmall<M>::THREADS, 1) c2r_small_kernel(const __grid_constant__ C2RParams p) {
+  using T = TC2RSmall<M>;
+  constexpr int G = T::G, PC = T::PC, H = T::H, UC = T::UC, NST = T::NST;
+  extern __shared__ __align__(128) uint8_t smem[];
+  float2* inter = reinterpret_cast<float2*>(smem + NST * T::STAGE);
+  float* tile = reinterpret_cast<float*>(smem + NST * T::STAGE + T::INTER);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NST * T::STAGE + T::INTER + T::TILE);
+  uint64_t* empty = full + NST;
+  const int ngj = (p.J + G - 1) / G;
+  const int ngj_all = p.J_all ? (p.J_all + G - 1) / G : ngj;
+  const int ngroups = p.R * ngj;
+  const int crop = p.crop;
+  constexpr long long BLOCK = (long long)M * PC * G;  // complex per group block
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], T::NC);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  pdl_wait();
+  span_begin(p.tspan);
+  pdl_trigger();
+  if (threadIdx.x < 32) {
+    // ------------------------------------------------ copy warp: u-row chunks into the ring
+    if (threadIdx.x == 0) {
+      const uint64_t pol = l2_policy_evict_first();
+      int k = 0;
+      for (int g = blockIdx.x; g < ngroups; g += gridDim.x) {
+        const int r = g / ngj, jg = g - r * ngj;
+        const float2* blk = reinterpret_cast<const float2*>(p.in) +
+                            (long long)(r * ngj_all + p.jbase / G + jg) * BLOCK;
+        for (int ch = 0; ch < T::NCH; ++ch, ++k) {
+          const int s = k % NST;
+          mbar_wait(&empty[s], ((k / NST) & 1) ^ 1);
+          const int rows = min(UC, PC - ch * UC);
+          const uint32_t bytes = (uint32_t)rows * M * G * 8;
+          mbar_arrive_expect_tx(&full[s], bytes);
+          bulk_load(smem + s * T::STAGE, blk + (long long)ch * UC * M * G, bytes, &full[s], pol);
+        }
+      }
+    }
+    return;  // the copy warp takes no part in the compute barriers below
+  }
+  const int t = threadIdx.x - 32;
+  const float scale = p.scale;
+  int k = 0;
+  for (int g = blockIdx.x; g < ngroups; g += gridDim.x) {
+    const int r = g / ngj, j0 = (g - r * ngj) * G;
+    const int jv = min(G, p.J - j0);
+    // ---- pass 1: (plane jl, u, half h): inverse row FFT over v, x = 2k' + h < crop kept
+    for (int ch = 0; ch < T::NCH; ++ch, ++k) {
+      const int s = k % NST;
+      mbar_wait(&full[s], (k / NST) & 1);
+      const int jl = t & 15, h = (t >> 4) & 1, ul = t >> 5, u = ch * UC + ul;
+      const float2* row = reinterpret_cast<const float2*>(smem + s * T::STAGE) + ul * M * G + jl;
+      float2 z[H];
+      if (u < PC) {
+        static_for<0, H>([&](auto Nn) {
+          constexpr int n = decltype(Nn)::value;
+          const float2 a0 = row[n * G], a1 = row[(n + H) * G];
+          if constexpr (n == 0) {
+            z[n] = h ? csub(a0, a1) : cadd(a0, a1);
+          } else {
+            const float2 d = csub(a0, a1);
+            z[n] = h ? cmul(d, tw128c<true, n * (128 / M)>()) : cadd(a0, a1);
+          }
+        });
+      }
+      mbar_arrive(&empty[s]);  // the chunk is in registers: the ring slot may refill
+      if (u < PC && jl < jv) {
+        fft_reg<H, true>(z);
+        float2* dst = inter + jl * T::IPS + u * T::IS + h;
+#pragma unroll
+        for (int kk = 0; kk < H; ++kk)
+          if (2 * kk + h < crop) dst[2 * kk] = z[kk];
+      }
+    }
+    named_bar_sync(1, T::NC);  // intermediate complete
+    // ---- pass 2: (plane jl, column x), direct Hermitian DFTs over u
+    {
+      const int jl = t & 15, x = t >> 4;
+      const bool act = jl < jv && x < crop;
+      float res[T::CMAX];
+      if (act) {
+        const float2* col = inter + jl * T::IPS + x;
+        float2 zz[H + 1];
+        static_for<0, H + 1>([&](auto U) { zz[decltype(U)::value] = col[decltype(U)::value * T::IS]; });
+        static_for<0, T::CMAX>([&](auto Y) {
+          constexpr int y = decltype(Y)::value;
+          if (y < crop) {
+            float acc = 0.f;
+            static_for<1, H>([&](auto U) {
+              constexpr int u = decltype(U)::value;
+              const float2 w = tw128c<true, (u * y * (128 / M)) % 128>();
+              acc = fmaf(zz[u].x, w.x, fmaf(-zz[u].y, w.y, acc));
+            });
+            const float e = zz[0].x + ((y & 1) ? -zz[H].x : zz[H].x);
+            res[y] = (e + 2.f * acc) * scale;
+          }
+        });
+        static_for<0, T::CMAX>([&](auto Y) {
+          constexpr int y = decltype(Y)::value;
+          if (y < crop) tile[jl * T::PST + y * crop + x] = res[y];
+        });
+      }
+    }
+    named_bar_sync(1, T::NC);  // tile complete, intermediate read
+    c2r_store_tile(tile, T::PST, jv, crop * crop, p.out + (long long)r * p.out_sr + (long long)j0 * p.out_sj,
+                   p.out_sj, p.accum, t, T::NC);
+    named_bar_sync(1, T::NC);  // tile read before the next group's pass 2 writes it
+  }
+  if (p.tspan) {  // thread 0 of the CTA is the copy thread (gone): compute thread 0 records
+    named_bar_sync(1, T::NC);
+    if (t == 0) atomicMax(p.tspan + kSpanEndOff, global_ns());
   }
 }
 

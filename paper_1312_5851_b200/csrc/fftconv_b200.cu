@@ -366,7 +366,32 @@ static void launch_c2r_tma(C2RParams p, const DevInfo& di, cudaStream_t st) {
   launch_pdl(kern, dim3(grid), dim3(T::THREADS), T::SMEM, st, tm, p);
 }
 
+// K4 for small crops (accGrad's weight gradients, crop <= m/4) from a
+// group-major product (fft_small.cuh); m = 64 by default,
+// FFTCONV_B200_SMALLCROP=0 off, =2 also at m = 32 (A/B).
+static int small_crop_mode() {
+  const char* e = getenv("FFTCONV_B200_SMALLCROP");
+  return e ? atoi(e) : 1;
+}
+static bool small_crop_ok(size_t m, size_t crop) {
+  const int mode = small_crop_mode();
+  return crop * 4 <= m && crop >= 1 && ((m == 64 && mode >= 1) || (m == 32 && mode >= 2));
+}
+template <int M>
+static void launch_c2r_small(const C2RParams& p, const DevInfo& di, cudaStream_t st) {
+  using T = TC2RSmall<M>;
+  auto kern = c2r_small_kernel<M>;
+  smem_optin(kern, T::SMEM);
+  const int groups = p.R * ((p.J + T::G - 1) / T::G);
+  const int grid = std::max(1, std::min(groups, di.sms));
+  launch_pdl(kern, dim3(grid), dim3(T::THREADS), T::SMEM, st, p);
+}
+
 static void launch_c2r(size_t m, const C2RParams& p, cudaStream_t st, const DevInfo& di) {
+  if (p.gm && small_crop_ok(m, p.crop)) {
+    if (m == 64) return launch_c2r_small<64>(p, di, st);
+    if (m == 32) return launch_c2r_small<32>(p, di, st);
+  }
   switch (m) {
     case 1: return launch_c2r_small<1>(p, st);
     case 2: return launch_c2r_small<2>(p, st);
@@ -1104,12 +1129,14 @@ void run_grad_weight(fftconv_b200_ws* ws, const float* gy, size_t Sg, size_t fo,
   const int nl = r2c_operands(ws, m, a, b, st, route);
   record(ws, 1, st);  // both forward transforms
   record(ws, 2, st);
-  const int ng = launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, fo, f, kp, -1.0f, c2r_layout(m), round_up(fo, 2),
+  // small crops at m = 64 read a group-major product (the small-crop K4)
+  const OutLayout lay = small_crop_ok(m, k) ? kGroupMajor : c2r_layout(m);
+  const int ng = launch_gemm(ws->bufA, ws->bufB, ws->bufD, bins, fo, f, kp, -1.0f, lay, round_up(fo, 2),
                              ws->di, st, route, a.amax, b.amax, ws->gemm_path, ws->span_slot(1));
   record(ws, 3, st);
   C2RParams c{ws->bufD, gw, (long long)(k * k), (long long)(f * k * k), (int)f, (int)fo, (int)k,
               0, 0, 1.0f / (float)(m * m), (int)round_up(fo, 2)};
-  c.gm = c2r_layout(m) == kGroupMajor;
+  c.gm = lay == kGroupMajor;
   c.accum = accum;
   int nc = 0;
   // chunked only where the TMA K4 runs (m in 4..64); chunk edges on 16-plane
