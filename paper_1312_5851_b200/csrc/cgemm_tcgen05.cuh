@@ -101,9 +101,13 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-#define GTRACE(ev, idx)                                                      \
-  do {                                                                       \
-    if (blockIdx.x == 0 && (idx) < 64) g_gemm_trace[ev][idx] = clock64();    \
+#ifndef FCB_GEMM_TRACE_G0
+#define FCB_GEMM_TRACE_G0 0  // first traced chunk (a steady-state window: > 0)
+#endif
+#define GTRACE(ev, idx)                                                                 \
+  do {                                                                                  \
+    const int i_ = (int)(idx) - ((ev) == 5 ? 0 : FCB_GEMM_TRACE_G0);                    \
+    if (blockIdx.x == 0 && i_ >= 0 && i_ < 64) g_gemm_trace[ev][i_] = clock64();        \
   } while (0)
 #else
 #define GTRACE(ev, idx) \
@@ -294,8 +298,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           uint8_t* st = smem + s * rawBytes;
           if constexpr (!F16) {
             mbar_arrive_expect_tx(&rfull[s], kChunkBytesA + rowsB);
+#ifdef FCB_GEMM_LAYOUT_EXP
+            tma_load_3d_hint(st, &tmA, &rfull[s], 0, kc * p.m_valid + mt * kTileM, t, pol_a);
+            tma_load_3d_hint(st + offB, &tmB, &rfull[s], 0, kc * p.n_valid + nt * nc, t, pol_b);
+#else
             tma_load_3d_hint(st, &tmA, &rfull[s], kc * 32, mt * kTileM, t, pol_a);
             tma_load_3d_hint(st + offB, &tmB, &rfull[s], kc * 32, nt * nc, t, pol_b);
+#endif
           } else {  // chunks 2kc, 2kc+1 (the second absent at odd k_chunks: converters zero it)
             const bool two = 2 * kc + 1 < p.k_chunks;
             mbar_arrive_expect_tx(&rfull[s], (two ? 2 : 1) * (kChunkBytesA + rowsB));

@@ -131,8 +131,13 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 static CUtensorMap make_operand_map(const float* base, size_t kpad, size_t rows, size_t bins,
                                     uint32_t box_rows) {
   CUtensorMap m;
+#ifdef FCB_GEMM_LAYOUT_EXP  // timing experiment only: chunk-contiguous reads of the same bytes
+  const cuuint64_t dims[3] = {32, rows * (kpad / 16), bins};
+  const cuuint64_t strides[2] = {128, rows * 2 * kpad * sizeof(float)};
+#else
   const cuuint64_t dims[3] = {2 * kpad, rows, bins};
   const cuuint64_t strides[2] = {2 * kpad * sizeof(float), rows * 2 * kpad * sizeof(float)};
+#endif
   const cuuint32_t box[3] = {32, box_rows, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims,
@@ -505,6 +510,9 @@ struct GemmGeom {
 #ifndef FCB_F16_MAXNC
 #define FCB_F16_MAXNC kMaxNc
 #endif
+#ifndef FCB_GEMM_MAXST
+#define FCB_GEMM_MAXST 8
+#endif
 static GemmGeom gemm_geom(size_t M, size_t N, const DevInfo& di, bool f16) {
   GemmGeom g;
   const size_t n16 = round_up(N, 16);
@@ -516,7 +524,7 @@ static GemmGeom gemm_geom(size_t M, size_t N, const DevInfo& di, bool f16) {
   const int sb = gemm_raw_stage_bytes(g.nc, f16);
   const int fixed = 2 * gemm_bbuf_bytes(g.nc);
   const int budget = di.max_smem_optin - 1024 - 256 - fixed;
-  g.stages = std::min(f16 ? 4 : 8, budget / sb);
+  g.stages = std::min(f16 ? 4 : FCB_GEMM_MAXST, budget / sb);
   if (g.stages < 2) throw Error(FFTCONV_B200_CUDA_ERROR, "gemm tile does not fit shared memory");
   g.smem = (size_t)g.stages * sb + fixed + 1024 + 256;
   return g;
@@ -545,14 +553,33 @@ static std::atomic<int> g_gemm_kind{[] {
 
 enum GemmRoute { kRouteTf32 = 0, kRouteF16 = 1, kRouteAuto = 2 };
 
-// Which GEMM kernel(s) a product of M x N over K needs.  Tensor-bound iff
-// 8 bins M N K / P_tf32x3 > 8 bins (MK + NK + MN) / B_hbm, i.e.
-// MNK / (MK + NK + MN) > 274 TF/s / 6.55 TB/s ~= 42 (MEASURED_PEAKS.json).
-static GemmRoute gemm_route(int kind, size_t M, size_t N, size_t K) {
+// Which GEMM kernel(s) a product of M x N over K on `bins` bins needs, from
+// a time model of the two kernels:
+//   3xTF32  max(tensor, bytes);  fp16x3  max(tensor / 2, bytes) + 8 us
+// (the auto pair's second launch, K1's per-row maxima, the heavier
+// converters).  Per K chunk of 16 complex a tile issues 12 UMMAs (M = 128,
+// N = 2 nc <= 192, K = 8), measured on the box at ~110 cycles each whatever
+// nc (a GEMM trace of W at S = 16, nc = 16: 3xTF32 317 us, fp16x3 197 us;
+// at P, nc = 96, ~105) -- so a small-N tile is tensor-bound long before its
+// FLOPs say so.  Bytes at 6.5 TB/s (MEASURED_PEAKS.json), 148 SMs at
+// 1.9 GHz; the tile shape follows gemm_swap / gemm_geom.  Near a tie at
+// large N (AlexNet's conv2 at S = 128: fp16x3 measured faster, the model
+// says even) round 1's FLOP / byte rule still picks fp16x3:
+// MNK / (MK + NK + MN) > 274 TF/s / 6.55 TB/s ~= 42.
+static GemmRoute gemm_route(int kind, size_t M, size_t N, size_t K, size_t bins) {
   if (kind == FFTCONV_B200_GEMM_TF32X3) return kRouteTf32;
   if (kind == FFTCONV_B200_GEMM_F16X3) return kRouteF16;
-  const double mnk = (double)M * N * K, bytes = (double)M * K + (double)N * K + (double)M * N;
-  return mnk > 42.0 * bytes ? kRouteAuto : kRouteTf32;
+  if ((double)M * N * K > 42.0 * ((double)M * K + (double)N * K + (double)M * N)) return kRouteAuto;
+  auto padded = [](size_t rows, size_t cols) { return ((rows + 127) / 128) * round_up(cols, 16); };
+  if (padded(N, M) < padded(M, N)) std::swap(M, N);  // gemm_swap's orientation
+  const size_t n16 = round_up(N, 16);
+  const size_t n_tiles = (n16 + kMaxNc - 1) / kMaxNc;
+  const size_t m_tiles = (M + kTileM - 1) / kTileM;
+  const double umma = (double)bins * m_tiles * n_tiles * (round_up(K, 16) / 16) * 12.0;
+  const double t_tensor = umma * 110.0 / (148.0 * 1.9e9);
+  const double t_bytes = 8.0 * bins * ((double)M * K + (double)N * K + (double)M * N) / 6.5e12;
+  const double t_tf32 = std::max(t_tensor, t_bytes), t_f16 = std::max(0.5 * t_tensor, t_bytes) + 8e-6;
+  return t_f16 < t_tf32 ? kRouteAuto : kRouteTf32;
 }
 
 static void launch_gemm_kernel(const float* A, const float* B, float* out, size_t bins, size_t M, size_t N,
@@ -1021,7 +1048,7 @@ void run_forward(fftconv_b200_ws* ws, const float* x, size_t S, size_t f, size_t
               (int)n, (int)(n | 1)};
   R2CParams b{w, ws->bufB, (long long)(f * k * k), (long long)(k * k), (int)fo, (int)f, (int)kp,
               (int)k, (int)(k | 1)};
-  const GemmRoute route = gemm_route(ws_gemm_kind(ws), S, fo, f);
+  const GemmRoute route = gemm_route(ws_gemm_kind(ws), S, fo, f, bins);
   const int nl = r2c_operands(ws, m, a, b, st, route);
   record(ws, 1, st);  // both forward transforms
   record(ws, 2, st);
@@ -1068,7 +1095,7 @@ void run_grad_input(fftconv_b200_ws* ws, const float* gy, size_t S, size_t fo, s
               (int)kp, (int)no, (int)(no | 1)};
   R2CParams b{w, ws->bufB, (long long)(k * k), (long long)(f * k * k), (int)f, (int)fo, (int)kp,
               (int)k, (int)(k | 1), /*conj=*/1};  // GX = GY . W = GY . conj(conj W)
-  const GemmRoute route = gemm_route(ws_gemm_kind(ws), S, f, fo);
+  const GemmRoute route = gemm_route(ws_gemm_kind(ws), S, f, fo, bins);
   const int nl = r2c_operands(ws, m, a, b, st, route);
   record(ws, 1, st);  // both forward transforms
   record(ws, 2, st);
@@ -1125,7 +1152,7 @@ void run_grad_weight(fftconv_b200_ws* ws, const float* gy, size_t Sg, size_t fo,
               (int)kp, (int)no, (int)(no | 1)};
   R2CParams b{x, ws->bufB, (long long)(n * n), (long long)(f * n * n), (int)f, (int)S, (int)kp,
               (int)n, (int)(n | 1)};
-  const GemmRoute route = gemm_route(ws_gemm_kind(ws), fo, f, S);
+  const GemmRoute route = gemm_route(ws_gemm_kind(ws), fo, f, S, bins);
   const int nl = r2c_operands(ws, m, a, b, st, route);
   record(ws, 1, st);  // both forward transforms
   record(ws, 2, st);
