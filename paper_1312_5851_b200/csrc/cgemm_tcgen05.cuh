@@ -115,6 +115,26 @@ __device__ __forceinline__ unsigned long long gtimer() {
   } while (0)
 #endif
 
+// Tile order.  One tile per bin (P, the narrow first layers; RANGES, a
+// template flag so the loops keep a constant stride): contiguous bin ranges
+// per CTA (P step 265 -> 260 us: each CTA's product and operand pieces are
+// adjacent).  Several tiles per bin (W): round-robin, bins
+// outermost -- the tiles of one bin share its operand rows in L2 (contiguous
+// ranges measured 1.67 -> 1.72 ms at W, S = 16).
+template <bool RANGES>
+__device__ __forceinline__ void decode_tile(int tile, const GemmParams& p, int& t, int& mt, int& nt) {
+  if (RANGES) {  // one tile per bin
+    t = tile;
+    mt = nt = 0;
+    return;
+  }
+  const int tpb = p.m_tiles * p.n_tiles;
+  t = tile / tpb;
+  const int rem = tile - t * tpb;
+  mt = rem / p.n_tiles;
+  nt = rem - mt * p.n_tiles;
+}
+
 // One raw stage holds one K chunk (tf32 mode) or two (fp16 mode: a 128-B
 // fp16 row covers 32 complex).
 __host__ __device__ inline int gemm_raw_stage_bytes(int nc, bool f16 = false) {
@@ -158,7 +178,7 @@ __host__ __device__ inline int gemm_bbuf_bytes(int nc) {
 // F16 = false: 3xTF32 (hi = raw fp32, lo = x - tf32(x)); true: 3xFP16 on
 // per-operand power-of-two scaled values, kind::f16 MMAs (twice the K per
 // instruction), hi.hi + hi.mid + mid.hi.
-template <bool F16>
+template <bool F16, bool RANGES>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     cgemm_bins_tcgen05(const __grid_constant__ CUtensorMap tmA,
                        const __grid_constant__ CUtensorMap tmB, const GemmParams p) {
@@ -224,6 +244,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   const int tiles_per_bin = p.m_tiles * p.n_tiles;
   const int total_tiles = p.bins * tiles_per_bin;
+  // RANGES (the launcher's choice: one tile per bin): contiguous tile ranges
+  const int per = (total_tiles + gridDim.x - 1) / gridDim.x;
+  const int tile_b = RANGES ? blockIdx.x * per : blockIdx.x;
+  const int tile_e = RANGES ? min(total_tiles, tile_b + per) : total_tiles;
+  const int tile_s = RANGES ? 1 : gridDim.x;
   // pipeline steps per tile: K chunks (tf32) or chunk pairs (fp16)
   const int kc_n = F16 ? (p.k_chunks + 1) >> 1 : p.k_chunks;
   int ea = 14, eb = 14;  // fp16 operand scale exponents
@@ -287,10 +312,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint64_t pol_first = l2_policy_evict_first(), pol_norm = l2_policy_evict_normal();
       const uint64_t pol_a = (FCB_GEMM_EVF && p.n_tiles == 1) ? pol_first : pol_norm;
       const uint64_t pol_b = (FCB_GEMM_EVF && p.m_tiles == 1) ? pol_first : pol_norm;
-      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-        const int t = tile / tiles_per_bin;
-        const int rem = tile - t * tiles_per_bin;
-        const int mt = rem / p.n_tiles, nt = rem - mt * p.n_tiles;
+      for (int tile = tile_b; tile < tile_e; tile += tile_s) {
+        int t, mt, nt;
+        decode_tile<RANGES>(tile, p, t, mt, nt);
         for (int kc = 0; kc < kc_n; ++kc) {
           mbar_wait(&rempty[s], ph ^ 1);
           GTRACE(0, gi);
@@ -324,7 +348,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const uint32_t idesc = F16 ? umma_idesc_f16(kTileM, 2 * nc) : umma_idesc_tf32(kTileM, 2 * nc);
     uint32_t g = 0;  // global chunk counter (TMEM A buffer / B buffer = g & 1)
     int local = 0;
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++local) {
+    for (int tile = tile_b; tile < tile_e; tile += tile_s, ++local) {
       const int a = local & 1;
       mbar_wait(&tempty[a], ((local >> 1) & 1) ^ 1);
       tc_fence_after();
@@ -369,7 +393,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     int s = 0;
     uint32_t ph = 0;
     uint32_t g = 0;
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+    for (int tile = tile_b; tile < tile_e; tile += tile_s) {
       for (int kc = 0; kc < kc_n; ++kc, ++g) {
         mbar_wait(&rfull[s], ph);
         if (threadIdx.x == 128) GTRACE(1, g);
@@ -433,7 +457,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     int s = 0;
     uint32_t ph = 0;
     uint32_t g = 0;
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+    for (int tile = tile_b; tile < tile_e; tile += tile_s) {
       for (int kc = 0; kc < kc_n; ++kc, ++g) {
         mbar_wait(&rfull[s], ph);
         const float4* braw = reinterpret_cast<const float4*>(smem + s * rawBytes + offB);
@@ -520,10 +544,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const float im_sign = p.im_sign;
     const float oscale = F16 ? ldexpf(1.f, ea - 14) * ldexpf(1.f, eb - 14) : 1.f;
     int local = 0;
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x, ++local) {
-      const int t = tile / tiles_per_bin;
-      const int rem = tile - t * tiles_per_bin;
-      const int mt = rem / p.n_tiles, nt = rem - mt * p.n_tiles;
+    for (int tile = tile_b; tile < tile_e; tile += tile_s, ++local) {
+      int t, mt, nt;
+      decode_tile<RANGES>(tile, p, t, mt, nt);
       const int a = local & 1;
       mbar_wait(&tfull[a], (local >> 1) & 1);
       tc_fence_after();

@@ -644,7 +644,9 @@ static void launch_gemm_kernel(const float* A, const float* B, float* out, size_
     p.s_mg = (long long)bins * G;
     p.s_n = (long long)((M + G - 1) / G) * (long long)bins * G;
   }
-  auto kern = f16 ? cgemm_bins_tcgen05<true> : cgemm_bins_tcgen05<false>;
+  const bool ranges = g.m_tiles * g.n_tiles == 1;
+  auto kern = f16 ? (ranges ? cgemm_bins_tcgen05<true, true> : cgemm_bins_tcgen05<true, false>)
+                  : (ranges ? cgemm_bins_tcgen05<false, true> : cgemm_bins_tcgen05<false, false>);
   smem_optin(kern, (int)g.smem);
   const long long tiles = (long long)bins * g.m_tiles * g.n_tiles;
   const int grid = (int)std::min<long long>(tiles, di.sms);
