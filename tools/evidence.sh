@@ -13,6 +13,10 @@ FFTCONV_B200_GEMM=tf32 timeout 400 python bench.py --config wide --no-cpu-baseli
 timeout 600 python bench.py --config alex1 > $O/bench_alex1.json 2> $O/bench_alex1.err
 timeout 400 python bench.py --config stack > $O/bench_stack.json 2> $O/bench_stack.err
 timeout 400 python bench.py --config stack:alexnet-128 --steps 5 --warmup 3 > $O/bench_stack_alexnet.json 2> $O/bench_stack_alexnet.err
+for S in 16 32 64; do  # strong-scaling shards: per-rank step at S/N samples
+  timeout 200 python tools/dev/step_probe.py --config wide --S $S --reps 20 > $O/probe_wide_S$S.txt 2>&1
+  timeout 200 python tools/dev/step_probe.py --config paper --S $S --reps 20 > $O/probe_paper_S$S.txt 2>&1
+done
 timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $O/launches_paper.csv \
   python tools/profile_step.py --reps 3 > /dev/null 2>&1
 python tools/launch_sum.py $O/launches_paper.csv > $O/launch_sum_paper.txt 2>&1
