@@ -55,6 +55,47 @@ __device__ __forceinline__ void class_twiddle(float2 (&z)[32]) {
   });
 }
 
+// Runtime-class forms of rot_i / class_twiddle (FCB_LARGE_RT, default on):
+// the four decimation classes then share one instruction stream instead of
+// four unrolled copies -- each class's 32-point FFT is ~1.4k instructions,
+// and four of them in one kernel made instruction fetch ("no_instructions")
+// the top ncu stall of K1a / K4b.  Twiddles from a constant-memory table
+// (the class is warp-uniform: broadcast reads); same values as tw128c, so
+// the results are bit-identical.
+#ifndef FCB_LARGE_RT
+#define FCB_LARGE_RT 1
+#endif
+struct Tw128Tab {
+  float re[128], im[128];
+};
+__host__ __device__ constexpr Tw128Tab make_tw128_tab() {
+  Tw128Tab t{};
+  for (int k = 0; k < 128; ++k) {
+    t.re[k] = tw128_re(k);
+    t.im[k] = tw128_im(k);
+  }
+  return t;
+}
+__constant__ Tw128Tab c_tw128 = make_tw128_tab();
+
+template <bool INV>
+__device__ __forceinline__ float2 rot_i_rt(float2 a, int e) {  // a * (-+i)^e
+  float2 r = a;
+  if (e & 1) r = INV ? make_float2(-a.y, a.x) : make_float2(a.y, -a.x);
+  if (e & 2) r = make_float2(-r.x, -r.y);
+  return r;
+}
+template <bool INV>
+__device__ __forceinline__ void class_twiddle_rt(float2 (&z)[32], int c) {
+  if (c == 0) return;
+  static_for<1, 32>([&](auto N) {
+    constexpr int n = decltype(N)::value;
+    const int k = (c * n) & (kL - 1);
+    const float im = c_tw128.im[k];
+    z[n] = cmul(z[n], make_float2(c_tw128.re[k], INV ? -im : im));
+  });
+}
+
 // ---------------------------------------------------------------- r2c K1a
 // Two real columns per complex FFT: the column pair (2p, 2p + 1) is
 // transformed as a + i b; K1b separates A[u] = (Z[u] + conj(Z[-u])) / 2 and
@@ -86,6 +127,37 @@ __device__ __forceinline__ void r2c128_colpair_class(const float2* col, int cs, 
   });
 }
 
+__device__ __forceinline__ void r2c128_colpair_rt(const float2* col, int cs, float2* o, int src, int np, int c) {
+  float2 z[32];
+  static_for<0, 32>([&](auto Y) {
+    constexpr int y0 = decltype(Y)::value;
+    z[y0] = y0 < src ? col[y0 * cs] : make_float2(0.f, 0.f);
+  });
+  static_for<1, 4>([&](auto Q) {
+    constexpr int q = decltype(Q)::value;
+    if (32 * q < src)
+      static_for<0, 32>([&](auto Y) {
+        constexpr int y0 = decltype(Y)::value;
+        if (y0 + 32 * q < src) z[y0] = cadd(z[y0], rot_i_rt<false>(col[(y0 + 32 * q) * cs], c * q));
+      });
+  });
+  class_twiddle_rt<false>(z, c);
+  fft_reg<32, false>(z);
+  static_for<0, 32>([&](auto K) { o[(long long)(4 * decltype(K)::value + c) * np] = z[decltype(K)::value]; });
+}
+__device__ __forceinline__ void r2c128_colpair(const float2* col, int cs, float2* o, int src, int np, int c) {
+#if FCB_LARGE_RT
+  r2c128_colpair_rt(col, cs, o, src, np, c);
+#else
+  switch (c) {
+    case 0: r2c128_colpair_class<0>(col, cs, o, src, np); break;
+    case 1: r2c128_colpair_class<1>(col, cs, o, src, np); break;
+    case 2: r2c128_colpair_class<2>(col, cs, o, src, np); break;
+    default: r2c128_colpair_class<3>(col, cs, o, src, np); break;
+  }
+#endif
+}
+
 constexpr int kLColPad = kL + 1;  // odd float2 stride of a staged column pair
 
 // grid = rows * J (one plane per CTA), block = 256 = (column pair p, class
@@ -114,13 +186,7 @@ __global__ void __launch_bounds__(256, 2) r2c128_cols_kernel(const R2CParams p, 
   const int pp = threadIdx.x & 63, c = threadIdx.x >> 6;
   if (pp >= np) return;
   float2* o = scr + (long long)ql * kL * np + pp;
-  const float2* col = pair_s + pp * kLColPad;
-  switch (c) {
-    case 0: r2c128_colpair_class<0>(col, 1, o, src, np); break;
-    case 1: r2c128_colpair_class<1>(col, 1, o, src, np); break;
-    case 2: r2c128_colpair_class<2>(col, 1, o, src, np); break;
-    default: r2c128_colpair_class<3>(col, 1, o, src, np); break;
-  }
+  r2c128_colpair(pair_s + pp * kLColPad, 1, o, src, np, c);
 }
 
 // K1a with the planes streamed by 1-D bulk copies (TMA) through a 2-stage
@@ -166,13 +232,7 @@ __global__ void __launch_bounds__(256, 2) r2c128_cols_bulk_kernel(const R2CParam
     const float2* stage = reinterpret_cast<const float2*>(lsm + 16 + s * sbytes);
     if (pp < np) {
       float2* o = scr + (long long)ql * kL * np + pp;
-      const float2* col = stage + pp;
-      switch (c) {
-        case 0: r2c128_colpair_class<0>(col, np, o, src, np); break;
-        case 1: r2c128_colpair_class<1>(col, np, o, src, np); break;
-        case 2: r2c128_colpair_class<2>(col, np, o, src, np); break;
-        default: r2c128_colpair_class<3>(col, np, o, src, np); break;
-      }
+      r2c128_colpair(stage + pp, np, o, src, np, c);
     }
     __syncthreads();  // stage s read by every thread
     if (threadIdx.x == 0 && ql + 2 * G < nplanes) {
@@ -209,6 +269,39 @@ __device__ __forceinline__ void r2c128_row_class(const float2* row, float2 (&z)[
   });
   class_twiddle<false, H>(z);
   fft_reg<32, false>(z);
+}
+
+__device__ __forceinline__ void r2c128_row(const float2* row, float2 (&z)[32], int src, int h) {
+#if FCB_LARGE_RT
+  const float4* row4 = reinterpret_cast<const float4*>(row);
+  static_for<0, 16>([&](auto X2) {
+    constexpr int x0 = 2 * decltype(X2)::value;
+    const float4 v = x0 < src ? row4[x0 / 2] : make_float4(0.f, 0.f, 0.f, 0.f);
+    z[x0] = make_float2(v.x, v.y);
+    z[x0 + 1] = make_float2(v.z, v.w);
+  });
+  static_for<1, 4>([&](auto Q) {
+    constexpr int q = decltype(Q)::value;
+    if (32 * q < src)
+      static_for<0, 16>([&](auto X2) {
+        constexpr int x0 = 2 * decltype(X2)::value;
+        if (x0 + 32 * q < src) {
+          const float4 v = row4[(x0 + 32 * q) / 2];
+          z[x0] = cadd(z[x0], rot_i_rt<false>(make_float2(v.x, v.y), h * q));
+          z[x0 + 1] = cadd(z[x0 + 1], rot_i_rt<false>(make_float2(v.z, v.w), h * q));
+        }
+      });
+  });
+  class_twiddle_rt<false>(z, h);
+  fft_reg<32, false>(z);
+#else
+  switch (h) {
+    case 0: r2c128_row_class<0>(row, z, src); break;
+    case 1: r2c128_row_class<1>(row, z, src); break;
+    case 2: r2c128_row_class<2>(row, z, src); break;
+    default: r2c128_row_class<3>(row, z, src); break;
+  }
+#endif
 }
 
 constexpr int kLRowPad = kL + 1;                 // odd float2 stride of K4a's output rows
@@ -259,13 +352,7 @@ __global__ void __launch_bounds__(128, 6) r2c128_rows_kernel(const R2CParams p, 
   float2 z[32];
   const bool act = cu < kLRows && jl < jv;
   if (act) {
-    const float2* row = buf + cul * kLRowBuf + jl * kLRowPadF;
-    switch (h) {
-      case 0: r2c128_row_class<0>(row, z, src); break;
-      case 1: r2c128_row_class<1>(row, z, src); break;
-      case 2: r2c128_row_class<2>(row, z, src); break;
-      default: r2c128_row_class<3>(row, z, src); break;
-    }
+    r2c128_row(buf + cul * kLRowBuf + jl * kLRowPadF, z, src, h);
   }
   __syncthreads();  // rows read: reuse as the tile
   float2* tile = buf + cul * kLRowBuf;  // [v][16]
@@ -321,6 +408,29 @@ __device__ __forceinline__ void c2r128_row_class(const float2* tile, int jl, flo
   });
   class_twiddle<true, H>(z);
   fft_reg<32, true>(z);
+}
+
+template <int TS>
+__device__ __forceinline__ void c2r128_row(const float2* tile, int jl, float2 (&z)[32], int h) {
+#if FCB_LARGE_RT
+  static_for<0, 32>([&](auto V) { z[decltype(V)::value] = tile[decltype(V)::value * TS + jl]; });
+  static_for<1, 4>([&](auto Q) {
+    constexpr int q = decltype(Q)::value;
+    static_for<0, 32>([&](auto V) {
+      constexpr int v0 = decltype(V)::value;
+      z[v0] = cadd(z[v0], rot_i_rt<true>(tile[(v0 + 32 * q) * TS + jl], h * q));
+    });
+  });
+  class_twiddle_rt<true>(z, h);
+  fft_reg<32, true>(z);
+#else
+  switch (h) {
+    case 0: c2r128_row_class<0, TS>(tile, jl, z); break;
+    case 1: c2r128_row_class<1, TS>(tile, jl, z); break;
+    case 2: c2r128_row_class<2, TS>(tile, jl, z); break;
+    default: c2r128_row_class<3, TS>(tile, jl, z); break;
+  }
+#endif
 }
 
 constexpr int kLTile = kL * 17;  // [v][16 planes] with an odd stride (>= kLRowBuf)
@@ -390,18 +500,8 @@ __global__ void __launch_bounds__(128, 6) c2r128_rows_kernel(const C2RParams p, 
     float2* ctile = buf + cul * kLTile;
     float2 z[32];
     if (act) {
-      if (bulk) switch (h) {
-          case 0: c2r128_row_class<0, 16>(ctile, jl, z); break;
-          case 1: c2r128_row_class<1, 16>(ctile, jl, z); break;
-          case 2: c2r128_row_class<2, 16>(ctile, jl, z); break;
-          default: c2r128_row_class<3, 16>(ctile, jl, z); break;
-        }
-      else switch (h) {
-          case 0: c2r128_row_class<0, 17>(ctile, jl, z); break;
-          case 1: c2r128_row_class<1, 17>(ctile, jl, z); break;
-          case 2: c2r128_row_class<2, 17>(ctile, jl, z); break;
-          default: c2r128_row_class<3, 17>(ctile, jl, z); break;
-        }
+      if (bulk) c2r128_row<16>(ctile, jl, z, h);
+      else c2r128_row<17>(ctile, jl, z, h);
     }
     __syncthreads();  // tile read: reuse it for the output rows [plane][x']
     if (act) {
@@ -456,6 +556,59 @@ __device__ __forceinline__ void c2r128_col_class(const C2RParams& p, const float
   }
 }
 
+__device__ __forceinline__ void c2r128_col_rt(const C2RParams& p, const float2* col, int cs, float* o, int crop,
+                                              int c) {
+  float2 z[32];
+  static_for<0, 32>([&](auto U) { z[decltype(U)::value] = col[decltype(U)::value * cs]; });
+  static_for<1, 4>([&](auto Q) {
+    constexpr int q = decltype(Q)::value;
+    static_for<0, 32>([&](auto U) {
+      constexpr int u0 = decltype(U)::value;
+      constexpr int u = u0 + 32 * q;
+      const float2 v = u < kLRows ? col[u * cs] : cconj(col[(kL - u) * cs]);
+      z[u0] = cadd(z[u0], rot_i_rt<true>(v, c * q));
+    });
+  });
+  class_twiddle_rt<true>(z, c);
+  fft_reg<32, true>(z);
+  const float scale = p.scale;
+  const long long step = 4LL * crop;
+  float* d = o + (long long)c * crop;  // walks rows y = 4k + c
+  if (p.accum) {  // branch outside the stores: no speculative loads of *d
+    static_for<0, 32>([&](auto K) {
+      if (4 * decltype(K)::value + c < crop) *d += scale * z[decltype(K)::value].x;
+      d += step;
+    });
+  } else {
+    static_for<0, 32>([&](auto K) {
+      if (4 * decltype(K)::value + c < crop) *d = scale * z[decltype(K)::value].x;
+      d += step;
+    });
+  }
+}
+// thread (x', g) runs classes g and g + 2
+__device__ __forceinline__ void c2r128_col_pair(const C2RParams& p, const float2* col, int cs, float* o, int crop,
+                                                int g) {
+#if FCB_LARGE_RT
+#pragma unroll 1
+  for (int c = g; c < 4; c += 2) {
+    c2r128_col_rt(p, col, cs, o, crop, c);
+    __syncwarp();
+  }
+#else
+  // __syncwarp between the classes keeps their register live ranges apart
+  if (g == 0) {
+    c2r128_col_class<0>(p, col, cs, o, crop);
+    __syncwarp();
+    c2r128_col_class<2>(p, col, cs, o, crop);
+  } else {
+    c2r128_col_class<1>(p, col, cs, o, crop);
+    __syncwarp();
+    c2r128_col_class<3>(p, col, cs, o, crop);
+  }
+#endif
+}
+
 // grid = rows * J (one plane per CTA), block = 256 = (column x', class
 // pair): the plane's 65 x crop scratch rows are staged transposed in smem
 // ([x'][u], stride 65: conflict-free 64-bit accesses per half-warp) with
@@ -477,17 +630,7 @@ __global__ void __launch_bounds__(256, 2) c2r128_cols_kernel(const C2RParams p, 
   __syncthreads();
   if (x >= crop) return;
   float* o = p.out + (long long)r * p.out_sr + (long long)j * p.out_sj + x;
-  const float2* col = zs + x * kLRows;
-  // __syncwarp between the classes keeps their register live ranges apart
-  if (g == 0) {
-    c2r128_col_class<0>(p, col, 1, o, crop);
-    __syncwarp();
-    c2r128_col_class<2>(p, col, 1, o, crop);
-  } else {
-    c2r128_col_class<1>(p, col, 1, o, crop);
-    __syncwarp();
-    c2r128_col_class<3>(p, col, 1, o, crop);
-  }
+  c2r128_col_pair(p, zs + x * kLRows, 1, o, crop, g);
 }
 
 
@@ -518,16 +661,7 @@ __global__ void __launch_bounds__(256, 2) c2r128_cols_flat_kernel(const C2RParam
   mbar_wait(bar, 0);
   if (x >= crop) return;
   float* o = p.out + (long long)r * p.out_sr + (long long)j * p.out_sj + x;
-  const float2* col = zs + x;
-  if (g == 0) {
-    c2r128_col_class<0>(p, col, crop, o, crop);
-    __syncwarp();
-    c2r128_col_class<2>(p, col, crop, o, crop);
-  } else {
-    c2r128_col_class<1>(p, col, crop, o, crop);
-    __syncwarp();
-    c2r128_col_class<3>(p, col, crop, o, crop);
-  }
+  c2r128_col_pair(p, zs + x, crop, o, crop, g);
 }
 
 }  // namespace fcb
