@@ -586,10 +586,16 @@ __device__ __forceinline__ void c2r128_col_rt(const C2RParams& p, const float2* 
     });
   }
 }
-// thread (x', g) runs classes g and g + 2
+// thread (x', g) runs classes g and g + 2.  K4b keeps the unrolled class
+// copies (FCB_LARGE_RT_K4B=0): with runtime twiddles it turned issue-bound
+// (ncu issue 81 %, 295 -> 325 us at alex1) -- its two classes per thread
+// already halve the instruction footprint.
+#ifndef FCB_LARGE_RT_K4B
+#define FCB_LARGE_RT_K4B 0
+#endif
 __device__ __forceinline__ void c2r128_col_pair(const C2RParams& p, const float2* col, int cs, float* o, int crop,
                                                 int g) {
-#if FCB_LARGE_RT
+#if FCB_LARGE_RT_K4B
 #pragma unroll 1
   for (int c = g; c < 4; c += 2) {
     c2r128_col_rt(p, col, cs, o, crop, c);
