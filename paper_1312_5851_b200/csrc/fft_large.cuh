@@ -103,7 +103,7 @@ __device__ __forceinline__ void class_twiddle_rt(float2 (&z)[32], int c) {
 // all 128 rows u of the packed Z (half the column-pass work of a transform
 // per column).
 template <int C>
-__device__ __forceinline__ void r2c128_colpair_class(const float2* col, int cs, float2* o, int src, int np) {
+__device__ __forceinline__ void r2c128_colpair_class(const float2* col, int cs, float2* o, int src, long long np) {
   // q-outer accumulation keeps one input live at a time (z + 1 load)
   float2 z[32];
   static_for<0, 32>([&](auto Y) {
@@ -127,7 +127,8 @@ __device__ __forceinline__ void r2c128_colpair_class(const float2* col, int cs, 
   });
 }
 
-__device__ __forceinline__ void r2c128_colpair_rt(const float2* col, int cs, float2* o, int src, int np, int c) {
+__device__ __forceinline__ void r2c128_colpair_rt(const float2* col, int cs, float2* o, int src, long long np,
+                                                  int c) {
   float2 z[32];
   static_for<0, 32>([&](auto Y) {
     constexpr int y0 = decltype(Y)::value;
@@ -145,7 +146,8 @@ __device__ __forceinline__ void r2c128_colpair_rt(const float2* col, int cs, flo
   fft_reg<32, false>(z);
   static_for<0, 32>([&](auto K) { o[(long long)(4 * decltype(K)::value + c) * np] = z[decltype(K)::value]; });
 }
-__device__ __forceinline__ void r2c128_colpair(const float2* col, int cs, float2* o, int src, int np, int c) {
+// np: the scratch u stride (float2)
+__device__ __forceinline__ void r2c128_colpair(const float2* col, int cs, float2* o, int src, long long np, int c) {
 #if FCB_LARGE_RT
   r2c128_colpair_rt(col, cs, o, src, np, c);
 #else
@@ -155,6 +157,28 @@ __device__ __forceinline__ void r2c128_colpair(const float2* col, int cs, float2
     case 2: r2c128_colpair_class<2>(col, cs, o, src, np); break;
     default: r2c128_colpair_class<3>(col, cs, o, src, np); break;
   }
+#endif
+}
+
+// K1a -> K1b scratch layout: S[plane][u][np] (default), or with
+// FCB_LARGE_GLAYOUT=1 grouped, S[row][16-plane group][u][plane][npad]
+// (npad = column pairs rounded up to even), so the 16 planes of one u row
+// that a K1b CTA reads are one contiguous block -- measured slower (alex1
+// bprop 0.89 -> 0.98 ms): K1a's per-plane writes then scatter over 1 MB
+// instead of one 60 KB plane.
+#ifndef FCB_LARGE_GLAYOUT
+#define FCB_LARGE_GLAYOUT 0
+#endif
+__host__ __device__ inline int large_npad(int np) { return FCB_LARGE_GLAYOUT ? (np + 1) & ~1 : np; }
+// scratch of plane (row rl, column j): base pointer (u = 0) and u stride
+__device__ __forceinline__ float2* large_scr_plane(float2* scr, int rl, int j, int J, int np, long long& ustride) {
+#if FCB_LARGE_GLAYOUT
+  const int npad = large_npad(np), ngj = (J + 15) >> 4;
+  ustride = 16LL * npad;
+  return scr + (((long long)(rl * ngj + (j >> 4)) * kL) * 16 + (j & 15)) * npad;
+#else
+  ustride = np;
+  return scr + (long long)(rl * J + j) * kL * np;
 #endif
 }
 
@@ -185,8 +209,9 @@ __global__ void __launch_bounds__(256, 2) r2c128_cols_kernel(const R2CParams p, 
   __syncthreads();
   const int pp = threadIdx.x & 63, c = threadIdx.x >> 6;
   if (pp >= np) return;
-  float2* o = scr + (long long)ql * kL * np + pp;
-  r2c128_colpair(pair_s + pp * kLColPad, 1, o, src, np, c);
+  long long us;
+  float2* o = large_scr_plane(scr, ql / p.J, j, p.J, np, us) + pp;
+  r2c128_colpair(pair_s + pp * kLColPad, 1, o, src, us, c);
 }
 
 // K1a with the planes streamed by 1-D bulk copies (TMA) through a 2-stage
@@ -231,8 +256,9 @@ __global__ void __launch_bounds__(256, 2) r2c128_cols_bulk_kernel(const R2CParam
     mbar_wait(bar + s, (it >> 1) & 1);
     const float2* stage = reinterpret_cast<const float2*>(lsm + 16 + s * sbytes);
     if (pp < np) {
-      float2* o = scr + (long long)ql * kL * np + pp;
-      r2c128_colpair(stage + pp, np, o, src, np, c);
+      long long us;
+      float2* o = large_scr_plane(scr, ql / p.J, ql % p.J, p.J, np, us) + pp;
+      r2c128_colpair(stage + pp, np, o, src, us, c);
     }
     __syncthreads();  // stage s read by every thread
     if (threadIdx.x == 0 && ql + 2 * G < nplanes) {
@@ -310,6 +336,18 @@ constexpr int kLRowPad = kL + 1;                 // odd float2 stride of K4a's o
 constexpr int kLRowPadF = kL + 2;
 constexpr int kLRowBuf = 16 * kLRowPadF;         // float2 per staged u row (>= 128 x 16 tile)
 constexpr int kLUPerCta = 2;                     // u rows per K1b / K4a CTA
+constexpr int kLUPairs = (kLRows + kLUPerCta - 1) / kLUPerCta;
+// K1b / K4a grid order: u pairs fastest (FCB_LARGE_UFAST, default on), so
+// CTAs resident together read adjacent scratch / product rows of the same
+// planes; else sample rows fastest.
+#ifndef FCB_LARGE_UFAST
+#define FCB_LARGE_UFAST 1
+#endif
+__device__ __forceinline__ int large_bu() { return FCB_LARGE_UFAST ? blockIdx.x : blockIdx.z; }
+__device__ __forceinline__ int large_br() { return FCB_LARGE_UFAST ? blockIdx.z : blockIdx.x; }
+__host__ inline dim3 large_row_grid(int rows, int groups) {
+  return FCB_LARGE_UFAST ? dim3(kLUPairs, groups, rows) : dim3(rows, groups, kLUPairs);
+}
 
 // grid = (rows, kpad / 16, ceil(65 / 2)), block = 128 = (u row, plane jl,
 // v class h).  The 16 staged scratch rows of a u row are overwritten by
@@ -318,23 +356,29 @@ __global__ void __launch_bounds__(128, 6) r2c128_rows_kernel(const R2CParams p, 
   __shared__ __align__(16) float2 buf[kLUPerCta * kLRowBuf];
   pdl_wait();
   pdl_trigger();
-  const int rl = blockIdx.x, r = r0 + rl;
+  const int rl = large_br(), r = r0 + rl;
   const int j0 = blockIdx.y * 16;
   const int jv = max(0, min(16, p.J - j0));
   const int src = p.src;
-  const int ul = threadIdx.x >> 6, u = blockIdx.z * kLUPerCta + ul;
+  const int ul = threadIdx.x >> 6, u = large_bu() * kLUPerCta + ul;
   const int t = threadIdx.x & 63;
   float2* rows_s = buf + ul * kLRowBuf;
   const int np = (src + 1) >> 1;
   if (u < kLRows && t < np) {  // separate the packed column pairs (K1a): A = (Z[u] + conj Z[-u]) / 2,
-    const float2* zp = scr + (long long)(rl * p.J + j0) * kL * np + t;  // B = (Z[u] - conj Z[-u]) / 2i
-    const long long ou = (long long)u * np, onu = (long long)((kL - u) & (kL - 1)) * np;
+    long long us;                                                     // B = (Z[u] - conj Z[-u]) / 2i
+    const float2* zp = large_scr_plane(const_cast<float2*>(scr), rl, j0, p.J, np, us) + t;
+#if FCB_LARGE_GLAYOUT
+    const long long js = large_npad(np);  // plane stride inside a u row block
+#else
+    const long long js = (long long)kL * np;
+#endif
+    const long long ou = (long long)u * us, onu = (long long)((kL - u) & (kL - 1)) * us;
     float2 za[16], zb[16];
 #pragma unroll
     for (int jl = 0; jl < 16; ++jl)  // all 32 loads in flight before the first use
       if (jl < jv) {
-        za[jl] = zp[(long long)jl * kL * np + ou];
-        zb[jl] = zp[(long long)jl * kL * np + onu];
+        za[jl] = zp[jl * js + ou];
+        zb[jl] = zp[jl * js + onu];
       }
 #pragma unroll
     for (int jl = 0; jl < 16; ++jl)
@@ -348,7 +392,7 @@ __global__ void __launch_bounds__(128, 6) r2c128_rows_kernel(const R2CParams p, 
   __syncthreads();
   // FFT phase: warp = class h (warp-uniform switch), lanes = (u row, plane)
   const int h = threadIdx.x >> 5, cul = (threadIdx.x >> 4) & 1, jl = threadIdx.x & 15;
-  const int cu = blockIdx.z * kLUPerCta + cul;
+  const int cu = large_bu() * kLUPerCta + cul;
   float2 z[32];
   const bool act = cu < kLRows && jl < jv;
   if (act) {
@@ -452,17 +496,17 @@ __global__ void __launch_bounds__(128, 6) c2r128_rows_kernel(const C2RParams p, 
   __syncthreads();
   pdl_wait();
   pdl_trigger();
-  const int rl = blockIdx.x, r = r0 + rl;
+  const int rl = large_br(), r = r0 + rl;
   const int jg = blockIdx.y, j0 = jg * 16;
   const int jv = min(16, p.J - j0);
   const int crop = p.crop;
-  const int ul = threadIdx.x >> 6, u = blockIdx.z * kLUPerCta + ul;
+  const int ul = threadIdx.x >> 6, u = large_bu() * kLUPerCta + ul;
   const int t = threadIdx.x & 63;
   float2* tile = buf + ul * kLTile;
   const float2* in = reinterpret_cast<const float2*>(p.in);
   if (bulk) {
     if (threadIdx.x == 0) {
-      const int ngj = (p.J + 15) >> 4, u0 = blockIdx.z * kLUPerCta;
+      const int ngj = (p.J + 15) >> 4, u0 = large_bu() * kLUPerCta;
       const int nr = min(kLUPerCta, kLRows - u0);
       const uint64_t pol = l2_policy_evict_first();
       mbar_arrive_expect_tx(&bar, (uint32_t)nr * kL * 16 * 8);
@@ -496,7 +540,7 @@ __global__ void __launch_bounds__(128, 6) c2r128_rows_kernel(const C2RParams p, 
   __syncthreads();
   {  // FFT phase: warp = class h (warp-uniform switch), lanes = (u row, plane)
     const int h = threadIdx.x >> 5, cul = (threadIdx.x >> 4) & 1, jl = threadIdx.x & 15;
-    const bool act = blockIdx.z * kLUPerCta + cul < kLRows && jl < jv;
+    const bool act = large_bu() * kLUPerCta + cul < kLRows && jl < jv;
     float2* ctile = buf + cul * kLTile;
     float2 z[32];
     if (act) {

@@ -425,8 +425,8 @@ static size_t large_scratch_budget() {  // FFTCONV_B200_LSCRATCH_MB overrides (t
 // float2 elements: every plane of the largest role up to the budget, at
 // least one operand row (maxJ planes)
 static size_t large_scratch_elems(size_t maxJ, size_t planes) {
-  const size_t per_plane = (size_t)kLRows * kL;
-  return std::max(maxJ * per_plane, std::min(large_scratch_budget() / sizeof(float2), planes * per_plane));
+  const size_t per_plane = (size_t)kLRows * kL;  // >= K1a's 128 x 64 (grouped: rows of 16-plane groups)
+  return std::max(round_up(maxJ, 16) * per_plane, std::min(large_scratch_budget() / sizeof(float2), planes * per_plane));
 }
 
 // per_plane = scratch float2 per plane (r2c: 128 rows x column pairs; c2r:
@@ -434,7 +434,8 @@ static size_t large_scratch_elems(size_t maxJ, size_t planes) {
 static int large_rows_per_chunk(size_t J, size_t per_plane, size_t scratch_elems) {
   const size_t per_row = J * per_plane;
   const size_t cap = std::min(scratch_elems, large_scratch_budget() / sizeof(float2));
-  return (int)std::max<size_t>(1, cap / std::max<size_t>(per_row, 1));
+  // <= 65535: the row kernels put rows on gridDim.z
+  return (int)std::min<size_t>(65535, std::max<size_t>(1, cap / std::max<size_t>(per_row, 1)));
 }
 
 // Persistent grid: as many CTAs as fit on all SMs at once (capped by the work).
@@ -459,7 +460,8 @@ static bool large_bulk_enabled() {
 // Returns the number of launches.
 static int launch_r2c_large(const R2CParams& p, float2* scr, size_t scr_n, cudaStream_t st) {
   const int np = (p.src + 1) / 2;  // column pairs (K1a packs two real columns per FFT)
-  const int rpc = large_rows_per_chunk(p.J, (size_t)kL * np, scr_n);
+  const int rpc = FCB_LARGE_GLAYOUT ? large_rows_per_chunk(round_up(p.J, 16), (size_t)kL * large_npad(np), scr_n)
+                                    : large_rows_per_chunk(p.J, (size_t)kL * np, scr_n);
   int nl = 0;
   for (int r0 = 0; r0 < p.R; r0 += rpc) {
     const int rows = std::min(rpc, p.R - r0);
@@ -476,8 +478,8 @@ static int launch_r2c_large(const R2CParams& p, float2* scr, size_t scr_n, cudaS
       smem_optin(r2c128_cols_kernel, smem);
       launch_pdl(r2c128_cols_kernel, dim3(rows * p.J), dim3(256), smem, st, p, r0, scr);
     }
-    launch_pdl(r2c128_rows_kernel, dim3(rows, (p.kpad + 15) / 16, (kLRows + kLUPerCta - 1) / kLUPerCta), dim3(128), 0,
-               st, p, r0, (const float2*)scr);
+    launch_pdl(r2c128_rows_kernel, large_row_grid(rows, (p.kpad + 15) / 16), dim3(128), 0, st, p, r0,
+               (const float2*)scr);
     nl += 2;
   }
   return nl;
@@ -488,8 +490,7 @@ static int launch_c2r_large(const C2RParams& p, float2* scr, size_t scr_n, cudaS
   int nl = 0;
   for (int r0 = 0; r0 < p.R; r0 += rpc) {
     const int rows = std::min(rpc, p.R - r0);
-    launch_pdl(c2r128_rows_kernel, dim3(rows, (p.J + 15) / 16, (kLRows + kLUPerCta - 1) / kLUPerCta),
-               dim3(128), 0, st, p, r0, scr);
+    launch_pdl(c2r128_rows_kernel, large_row_grid(rows, (p.J + 15) / 16), dim3(128), 0, st, p, r0, scr);
     const int smem = kLRows * p.crop * (int)sizeof(float2);
     if (large_bulk_enabled() && p.crop % 2 == 0) {
       smem_optin(c2r128_cols_flat_kernel, 16 + smem);
@@ -1950,6 +1951,9 @@ namespace {
 int ew_grid(long long n) {
   return (int)std::max<long long>(1, std::min<long long>((n + 255) / 256, 148LL * 16));
 }
+// plane-walking layer kernels (layers.cuh): one 256-thread block per plane,
+// at most 8 resident blocks per SM
+int plane_grid(long long planes) { return (int)std::max<long long>(1, std::min<long long>(planes, 148LL * 8)); }
 }  // namespace
 
 int fftconv_b200_relu_forward(const float* x, float* y, size_t n, void* stream) {
@@ -1984,7 +1988,7 @@ int fftconv_b200_maxpool_forward(const float* x, size_t planes, size_t rows, siz
       throw Error(FFTCONV_B200_SIZE_ERROR, "maxpool: rows and cols must be even");
     const long long total = (long long)planes * (rows / 2) * (cols / 2);
     if (total)
-      maxpool_fwd_kernel<<<ew_grid(total), 256, 0, (cudaStream_t)stream>>>(
+      maxpool_fwd_kernel<<<plane_grid((long long)planes), 256, 0, (cudaStream_t)stream>>>(
           x, y, argmax, (long long)planes, (int)rows, (int)cols);
     FCB_CUDA(cudaGetLastError());
   });
@@ -1997,7 +2001,7 @@ int fftconv_b200_maxpool_backward(const float* gy, const uint32_t* argmax, size_
       throw Error(FFTCONV_B200_SIZE_ERROR, "maxpool: rows and cols must be even");
     const long long total = (long long)planes * (rows / 2) * (cols / 2);
     if (total)
-      maxpool_bwd_kernel<<<ew_grid(total), 256, 0, (cudaStream_t)stream>>>(
+      maxpool_bwd_kernel<<<plane_grid((long long)planes), 256, 0, (cudaStream_t)stream>>>(
           gy, argmax, gx, (long long)planes, (int)rows, (int)cols);
     FCB_CUDA(cudaGetLastError());
   });
@@ -2008,7 +2012,7 @@ int fftconv_b200_fit_to(const float* x, size_t planes, size_t rows, size_t cols,
   return guarded(nullptr, [&] {
     const long long total = (long long)planes * size * size;
     if (total)
-      fit_to_kernel<<<ew_grid(total), 256, 0, (cudaStream_t)stream>>>(
+      fit_to_kernel<<<plane_grid((long long)planes), 256, 0, (cudaStream_t)stream>>>(
           x, y, (long long)planes, (int)rows, (int)cols, (int)size);
     FCB_CUDA(cudaGetLastError());
   });

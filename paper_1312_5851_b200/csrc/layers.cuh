@@ -3,8 +3,8 @@
 //   relu forward / backward, 2x2 stride-2 max pooling forward (with the
 //   winning flat index per window) / backward, and fit_to (top-left pad or
 //   crop of every plane).
-// All are single-pass HBM-bound kernels: grid-stride loops over output
-// elements, 16-B vector accesses where the layout allows.
+// All are single-pass HBM-bound kernels: relu as grid-stride float4 loops,
+// pooling and fit_to as plane-walking blocks (below).
 #pragma once
 #include <cstdint>
 
@@ -41,33 +41,59 @@ __global__ void relu_bwd_tail(const float* gy, const float* x, float* gx, long l
   if (i < n) gx[i] = x[i] > 0.f ? gy[i] : 0.f;
 }
 
+// Pooling and fit_to: blocks walk whole planes (grid-stride over planes),
+// the block's threads tile a plane's output rows -- thread (i0, j) with
+// j = t % C, i0 = t / C handles rows i0, i0 + 256 / C, ... -- so the index
+// arithmetic is one 32-bit division per thread, not a 64-bit div / mod per
+// element (round 1's flat loops spent ~1.3 ms of an AlexNet-128 iteration on
+// fit_to's index math; one block per (plane, row) or a warp per row were
+// slower still, §4 of DESIGN.md).
+struct PlaneTiler {
+  int j, i0, rpi;  // column, first row, rows per pass (0: thread idle when C <= 256)
+  __device__ PlaneTiler(int C) {
+    const int t = threadIdx.x, nt = blockDim.x;
+    if (C <= nt) {
+      rpi = nt / C;
+      j = t % C;
+      i0 = t / C;
+      if (i0 >= rpi) rpi = 0;
+    } else {  // wide rows: every thread walks columns j, j + nt, ... of each row
+      rpi = 1;
+      j = t;
+      i0 = 0;
+    }
+  }
+};
+
 // layers.hpp:34-66: 2x2 windows, stride 2; ties go to the earliest element in
 // row-major order; argmax = flat index of the winner inside its input plane.
 __global__ void maxpool_fwd_kernel(const float* __restrict__ x, float* __restrict__ y,
                                    uint32_t* __restrict__ arg, long long planes, int rows, int cols) {
   const int orow = rows / 2, ocol = cols / 2;
-  const long long total = planes * orow * ocol;
-  for (long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x; o < total;
-       o += (long long)gridDim.x * blockDim.x) {
-    const long long pl = o / (orow * ocol);
-    const int rem = (int)(o - pl * orow * ocol);
-    const int i = rem / ocol, j = rem - i * ocol;
+  const PlaneTiler tl(ocol);
+  if (!tl.rpi) return;
+  for (long long pl = blockIdx.x; pl < planes; pl += gridDim.x) {
     const float* in = x + pl * rows * cols;
-    int best = 2 * i * cols + 2 * j;
-    float bv = in[best];
+    float* yo = y + pl * orow * ocol;
+    uint32_t* ao = arg + pl * orow * ocol;
+    for (int i = tl.i0; i < orow; i += tl.rpi)
+      for (int j = tl.j; j < ocol; j += blockDim.x) {
+        int best = 2 * i * cols + 2 * j;
+        float bv = in[best];
 #pragma unroll
-    for (int di = 0; di < 2; ++di)
+        for (int di = 0; di < 2; ++di)
 #pragma unroll
-      for (int dj = 0; dj < 2; ++dj) {
-        const int q = (2 * i + di) * cols + 2 * j + dj;
-        const float v = in[q];
-        if (v > bv) {
-          bv = v;
-          best = q;
-        }
+          for (int dj = 0; dj < 2; ++dj) {
+            const int q = (2 * i + di) * cols + 2 * j + dj;
+            const float v = in[q];
+            if (v > bv) {
+              bv = v;
+              best = q;
+            }
+          }
+        yo[i * ocol + j] = bv;
+        ao[i * ocol + j] = (uint32_t)best;
       }
-    y[o] = bv;
-    arg[o] = (uint32_t)best;
   }
 }
 
@@ -76,21 +102,21 @@ __global__ void maxpool_fwd_kernel(const float* __restrict__ x, float* __restric
 __global__ void maxpool_bwd_kernel(const float* __restrict__ gy, const uint32_t* __restrict__ arg,
                                    float* __restrict__ gx, long long planes, int rows, int cols) {
   const int orow = rows / 2, ocol = cols / 2;
-  const long long total = planes * orow * ocol;
-  for (long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x; o < total;
-       o += (long long)gridDim.x * blockDim.x) {
-    const long long pl = o / (orow * ocol);
-    const int rem = (int)(o - pl * orow * ocol);
-    const int i = rem / ocol, j = rem - i * ocol;
+  const PlaneTiler tl(ocol);
+  if (!tl.rpi) return;
+  for (long long pl = blockIdx.x; pl < planes; pl += gridDim.x) {
     float* out = gx + pl * rows * cols;
-    const float g = gy[o];
-    const int win = (int)arg[o];
+    const float* g0 = gy + pl * orow * ocol;
+    const uint32_t* a0 = arg + pl * orow * ocol;
+    for (int i = tl.i0; i < orow; i += tl.rpi)
+      for (int j = tl.j; j < ocol; j += blockDim.x) {
+        const float g = g0[i * ocol + j];
+        const int win = (int)a0[i * ocol + j];
 #pragma unroll
-    for (int di = 0; di < 2; ++di)
-#pragma unroll
-      for (int dj = 0; dj < 2; ++dj) {
-        const int q = (2 * i + di) * cols + 2 * j + dj;
-        out[q] = (q == win) ? g : 0.f;
+        for (int di = 0; di < 2; ++di) {
+          const int q = (2 * i + di) * cols + 2 * j;
+          *reinterpret_cast<float2*>(out + q) = make_float2(q == win ? g : 0.f, q + 1 == win ? g : 0.f);
+        }
       }
   }
 }
@@ -99,13 +125,14 @@ __global__ void maxpool_bwd_kernel(const float* __restrict__ gy, const uint32_t*
 // to size x size.
 __global__ void fit_to_kernel(const float* __restrict__ x, float* __restrict__ y, long long planes,
                               int rows, int cols, int size) {
-  const long long total = planes * size * size;
-  for (long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x; o < total;
-       o += (long long)gridDim.x * blockDim.x) {
-    const long long pl = o / ((long long)size * size);
-    const int rem = (int)(o - pl * size * size);
-    const int i = rem / size, j = rem - i * size;
-    y[o] = (i < rows && j < cols) ? x[pl * rows * cols + (long long)i * cols + j] : 0.f;
+  const PlaneTiler tl(size);
+  if (!tl.rpi) return;
+  for (long long pl = blockIdx.x; pl < planes; pl += gridDim.x) {
+    const float* in = x + pl * rows * cols;
+    float* o = y + pl * size * size;
+    for (int i = tl.i0; i < size; i += tl.rpi)
+      for (int j = tl.j; j < size; j += blockDim.x)
+        o[i * size + j] = (i < rows && j < cols) ? in[i * cols + j] : 0.f;
   }
 }
 
