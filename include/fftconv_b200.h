@@ -120,6 +120,14 @@ int fftconv_b200_forward(fftconv_b200_ws* ws, const float* x, size_t S, size_t f
                          size_t x_cols, const float* w, size_t w_out, size_t w_in, size_t k,
                          float* y, void* stream);
 
+/* forward followed by the layer stack's relu (layers.hpp:88-97), fused into
+ * the inverse transform's stores: y = max(forward(x, w), 0) with the
+ * reference's x > 0 ? x : 0.  Same arguments and errors as
+ * fftconv_b200_forward; the stack's relu backward can use y as its mask. */
+int fftconv_b200_forward_relu(fftconv_b200_ws* ws, const float* x, size_t S, size_t f, size_t x_rows,
+                              size_t x_cols, const float* w, size_t w_out, size_t w_in, size_t k,
+                              float* y, void* stream);
+
 /* ConvWorkspace<float>::grad_input(gy, w)  conv_fft.hpp:115-152.
  * gy: [S][fo][gy_rows][gy_cols]; gx: [S][w_in][n][n], n = gy_rows + k - 1. */
 int fftconv_b200_grad_input(fftconv_b200_ws* ws, const float* gy, size_t S, size_t fo,

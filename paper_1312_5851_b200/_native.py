@@ -27,6 +27,7 @@ SIGNATURES = [
     ("fftconv_b200_counters", _i, [_p, _p]),
     ("fftconv_b200_reset_counters", _i, [_p]),
     ("fftconv_b200_forward", _i, [_p, _p, _sz, _sz, _sz, _sz, _p, _sz, _sz, _sz, _p, _p]),
+    ("fftconv_b200_forward_relu", _i, [_p, _p, _sz, _sz, _sz, _sz, _p, _sz, _sz, _sz, _p, _p]),
     ("fftconv_b200_grad_input", _i, [_p, _p, _sz, _sz, _sz, _sz, _p, _sz, _sz, _sz, _p, _p]),
     ("fftconv_b200_grad_weight", _i, [_p, _p, _sz, _sz, _sz, _sz, _p, _sz, _sz, _sz, _sz, _p, _p]),
     ("fftconv_b200_nccl_get_unique_id", _i, [_p]),

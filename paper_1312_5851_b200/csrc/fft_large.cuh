@@ -594,7 +594,7 @@ __device__ __forceinline__ void c2r128_col_class(const C2RParams& p, const float
   } else {
     static_for<0, 32>([&](auto K) {
       constexpr int k = decltype(K)::value;
-      if (4 * k + C < crop) *d = scale * z[k].x;
+      if (4 * k + C < crop) *d = c2r_out(scale * z[k].x, p.relu);
       d += step;
     });
   }
@@ -625,7 +625,7 @@ __device__ __forceinline__ void c2r128_col_rt(const C2RParams& p, const float2* 
     });
   } else {
     static_for<0, 32>([&](auto K) {
-      if (4 * decltype(K)::value + c < crop) *d = scale * z[decltype(K)::value].x;
+      if (4 * decltype(K)::value + c < crop) *d = c2r_out(scale * z[decltype(K)::value].x, p.relu);
       d += step;
     });
   }

@@ -443,7 +443,13 @@ struct C2RParams {
   int jbase = 0;
   int J_all = 0;  // 0: J
   unsigned long long* tspan = nullptr;  // live span slot (TMA K4 only)
+  // 1: the stack's relu fused into the store, y = max(conv, 0) as
+  // layers.hpp:88-97 writes it (x > 0 ? x : 0); never with accum
+  int relu = 0;
 };
+
+// The output value of a K4 store: scaled, optionally through the fused relu.
+__device__ __forceinline__ float c2r_out(float v, int relu) { return relu ? (v > 0.f ? v : 0.f) : v; }
 
 // grid = (ceil(J/G), R, ceil(crop/cc)), block = PlaneTraits<M>::THREADS.
 // smem = G * (M/2+1) * ccpad * sizeof(float2).
@@ -531,8 +537,8 @@ __global__ void __launch_bounds__(PlaneTraits<M>::THREADS, PlaneTraits<M>::MIN_C
 #pragma unroll
       for (int i = 0; i < M; ++i) {
         if (i < p.crop) {
-          dst[(long long)i * p.crop] = z[i].x * scale;
-          if (has_b) dst[(long long)i * p.crop + 1] = z[i].y * scale;
+          dst[(long long)i * p.crop] = c2r_out(z[i].x * scale, p.relu);
+          if (has_b) dst[(long long)i * p.crop + 1] = c2r_out(z[i].y * scale, p.relu);
         }
       }
     }
@@ -549,7 +555,7 @@ __global__ void __launch_bounds__(PlaneTraits<M>::THREADS, PlaneTraits<M>::MIN_C
       float* dst = p.out + (long long)r * p.out_sr + (long long)(j0 + jl) * p.out_sj + c0 + cl;
 #pragma unroll
       for (int i = 0; i < M; ++i)
-        if (i < p.crop) dst[(long long)i * p.crop] = x[i] * scale;
+        if (i < p.crop) dst[(long long)i * p.crop] = c2r_out(x[i] * scale, p.relu);
     }
   }
 }

@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(TC2RSmall<M>::THREADS, 1) c2r_small_kernel(con
               acc = fmaf(zz[u].x, w.x, fmaf(-zz[u].y, w.y, acc));
             });
             const float e = zz[0].x + ((y & 1) ? -zz[H].x : zz[H].x);
-            res[y] = (e + 2.f * acc) * scale;
+            res[y] = c2r_out((e + 2.f * acc) * scale, p.relu);
           }
         });
         static_for<0, T::CMAX>([&](auto Y) {

@@ -707,7 +707,7 @@ __global__ void __launch_bounds__(TC2R<M>::THREADS, 1)
                 acc = fmaf(z[u].x, w.x, fmaf(-z[u].y, w.y, acc));
               });
               const float e = z[0].x + ((y & 1) ? -z[M / 2].x : z[M / 2].x);
-              res[y] = (e + 2.f * acc) * scale;
+              res[y] = c2r_out((e + 2.f * acc) * scale, p.relu);
             }
           });
         }
@@ -763,8 +763,8 @@ __global__ void __launch_bounds__(TC2R<M>::THREADS, 1)
 #pragma unroll
           for (int row = 0; row < M; ++row) {
             if (row < crop) {
-              tile[0] = zz[row].x * scale;
-              if (hb) tile[H] = zz[row].y * scale;
+              tile[0] = c2r_out(zz[row].x * scale, p.relu);
+              if (hb) tile[H] = c2r_out(zz[row].y * scale, p.relu);
             }
             tile += crop;
           }
@@ -813,8 +813,8 @@ __global__ void __launch_bounds__(TC2R<M>::THREADS, 1)
             float* tile = reinterpret_cast<float*>(smem + s * T::STAGE) + jl * pst + c;
 #pragma unroll
             for (int i2 = 0; i2 < H; ++i2) {
-              if (2 * i2 < crop) tile[(2 * i2) * crop] = z[i2].x * scale;
-              if (2 * i2 + 1 < crop) tile[(2 * i2 + 1) * crop] = z[i2].y * scale;
+              if (2 * i2 < crop) tile[(2 * i2) * crop] = c2r_out(z[i2].x * scale, p.relu);
+              if (2 * i2 + 1 < crop) tile[(2 * i2 + 1) * crop] = c2r_out(z[i2].y * scale, p.relu);
             }
           }
           fence_proxy_async_smem();
@@ -832,8 +832,8 @@ __global__ void __launch_bounds__(TC2R<M>::THREADS, 1)
                 if (2 * i2 < crop) *d0 += z[i2].x * scale;
                 if (2 * i2 + 1 < crop) *d1 += z[i2].y * scale;
               } else {
-                if (2 * i2 < crop) *d0 = z[i2].x * scale;
-                if (2 * i2 + 1 < crop) *d1 = z[i2].y * scale;
+                if (2 * i2 < crop) *d0 = c2r_out(z[i2].x * scale, p.relu);
+                if (2 * i2 + 1 < crop) *d1 = c2r_out(z[i2].y * scale, p.relu);
               }
             }
           }

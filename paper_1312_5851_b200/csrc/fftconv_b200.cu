@@ -1033,7 +1033,7 @@ int c2r_run(fftconv_b200_ws* ws, size_t m, const C2RParams& c, cudaStream_t st) 
 }
 
 void run_forward(fftconv_b200_ws* ws, const float* x, size_t S, size_t f, size_t xr, size_t xc,
-                 const float* w, size_t wo, size_t wi, size_t k, float* y, cudaStream_t st) {
+                 const float* w, size_t wo, size_t wi, size_t k, float* y, cudaStream_t st, bool relu = false) {
   require_nonzero(S, f, xr, xc, "Tensor4");
   require_nonzero(wo, wi, k, 1, "Weights4");
   if (xr != xc) throw Error(FFTCONV_B200_SIZE_ERROR, "forward_fft: planes must be square");
@@ -1069,6 +1069,7 @@ void run_forward(fftconv_b200_ws* ws, const float* x, size_t S, size_t f, size_t
   }
   record(ws, 3, st);
   c.gm = c2r_layout(m) == kGroupMajor;
+  c.relu = relu ? 1 : 0;
   const int nc = c2r_run(ws, m, c, st);
   record(ws, 4, st);
   ws->last_launches = nl + ng + nc;
@@ -1350,6 +1351,18 @@ int fftconv_b200_forward(fftconv_b200_ws* ws, const float* x, size_t S, size_t f
     DeviceGuard g(ws->device);
     order_after_last(ws, (cudaStream_t)stream);
     run_forward(ws, x, S, f, x_rows, x_cols, w, w_out, w_in, k, y, (cudaStream_t)stream);
+    mark_done(ws, (cudaStream_t)stream);
+  });
+}
+
+int fftconv_b200_forward_relu(fftconv_b200_ws* ws, const float* x, size_t S, size_t f, size_t x_rows,
+                              size_t x_cols, const float* w, size_t w_out, size_t w_in, size_t k,
+                              float* y, void* stream) {
+  if (!ws) return FFTCONV_B200_INVALID_ARGUMENT;
+  return guarded(ws, [&] {
+    DeviceGuard g(ws->device);
+    order_after_last(ws, (cudaStream_t)stream);
+    run_forward(ws, x, S, f, x_rows, x_cols, w, w_out, w_in, k, y, (cudaStream_t)stream, true);
     mark_done(ws, (cudaStream_t)stream);
   });
 }

@@ -252,7 +252,9 @@ class _CountingWorkspace:
         _launched(self.ws.last_launch_count())
         return r
 
-    def forward(self, x, w):
+    def forward(self, x, w, relu=False):
+        if relu:
+            return self._run(lambda a, b: self.ws.forward(a, b, relu=True), x, w)
         return self._run(self.ws.forward, x, w)
 
     def grad_input(self, gy, w):
@@ -394,16 +396,22 @@ def run_iteration(spec: NetworkSpec, params: NetworkParams, batch, ws: ConvWorks
 
         def forward_all():
             ci = 0
-            for st in spec.stages:
+            fused = False  # the last conv already applied this relu (fftconv_b200_forward_relu)
+            for si, st in enumerate(spec.stages):
                 cur = state["cur"]
                 if st.kind == StageKind.conv:
                     fin = fit_to(cur, st.conv.image)
                     conv_rec.append((fin, cur.shape[2]))
-                    state["cur"] = ws.forward(fin, w_dev[ci])
+                    fused = si + 1 < len(spec.stages) and spec.stages[si + 1].kind == StageKind.relu
+                    state["cur"] = ws.forward(fin, w_dev[ci], relu=fused)
                     ci += 1
                 elif st.kind == StageKind.relu:
+                    # relu backward masks by x > 0, and relu(x) > 0 exactly where x > 0,
+                    # so the fused output serves as the record
                     relu_rec.append(cur)
-                    state["cur"] = relu_forward(cur)
+                    if not fused:
+                        state["cur"] = relu_forward(cur)
+                    fused = False
                 elif st.kind == StageKind.pool:
                     rec = maxpool_forward(cur)
                     pool_rec.append(rec)

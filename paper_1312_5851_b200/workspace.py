@@ -193,8 +193,10 @@ class ConvWorkspace:
             raise ValueError(f"out must be a C-contiguous float32 array of shape {tuple(shape)}")
         return out
 
-    def forward(self, x, w, threads: int = 1, out=None):
-        """conv_fft.hpp:74-113: y = valid cross-correlation of x by w."""
+    def forward(self, x, w, threads: int = 1, out=None, relu: bool = False):
+        """conv_fft.hpp:74-113: y = valid cross-correlation of x by w.
+        relu=True (device operands): the layer stack's following relu
+        (layers.hpp:88-97) fused into the inverse transform's stores."""
         S, f, xr, xc = _shape4(x)
         wo, wi, k = _weights_shape(w)
         no = xr - k + 1 if k <= xr else 1
@@ -203,10 +205,13 @@ class ConvWorkspace:
             import torch
 
             y = torch.empty((S, wo, max(no, 1), max(no, 1)), dtype=torch.float32, device=x.device)
-            code = L.fftconv_b200_forward(self._h, self._dev_ptr(x), S, f, xr, xc, self._dev_ptr(w), wo, wi, k,
-                                          self._dev_ptr(y), self._stream(x))
+            fn = L.fftconv_b200_forward_relu if relu else L.fftconv_b200_forward
+            code = fn(self._h, self._dev_ptr(x), S, f, xr, xc, self._dev_ptr(w), wo, wi, k, self._dev_ptr(y),
+                      self._stream(x))
             self._check(code)
             return y
+        if relu:
+            raise ValueError("forward(relu=True) takes device operands")
         xa, xp = self._host(x)
         wa, wp = self._host(w)
         y = self._host_out(out, (S, wo, max(no, 1), max(no, 1)))

@@ -27,6 +27,29 @@ def test_relu(dev):
     assert np.array_equal(layers.relu_backward(_t(gy, dev), xd).cpu().numpy(), np.where(x > 0, gy, 0))
 
 
+@pytest.mark.parametrize("S,f,fo,n,k", [
+    (4, 3, 8, 16, 5),     # m = 16
+    (4, 6, 10, 30, 3),    # m = 32
+    (3, 5, 7, 16, 13),    # small output crop (direct-DFT K4 path)
+    (2, 4, 6, 60, 5),     # m = 64
+    (2, 3, 4, 118, 11),   # m = 128 (two-pass K4)
+    (2, 2, 3, 2, 1),      # m = 2 plane kernels
+])
+def test_forward_relu_fused_equals_relu_of_forward(dev, S, f, fo, n, k):
+    """fftconv_b200_forward_relu: the stack's relu fused into K4's stores
+    is bit-identical to forward followed by the relu kernel."""
+    from paper_1312_5851_b200 import ConvWorkspace, LayerConfig
+
+    rng = np.random.default_rng(S * 1000 + n)
+    x = _t(rng.standard_normal((S, f, n, n)).astype(np.float32), dev)
+    w = _t(rng.standard_normal((fo, f, k, k)).astype(np.float32), dev)
+    ws = ConvWorkspace([LayerConfig(k, n, f, fo, S)], device=0)
+    y = ws.forward(x, w)
+    yr = ws.forward(x, w, relu=True)
+    assert (y > 0).any() and (y < 0).any()
+    assert np.array_equal(yr.cpu().numpy(), layers.relu_forward(y).cpu().numpy())
+
+
 def _pool_ref(x):
     S, M, R, Cc = x.shape
     y = np.zeros((S, M, R // 2, Cc // 2), np.float32)
