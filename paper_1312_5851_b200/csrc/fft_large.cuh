@@ -349,40 +349,68 @@ __host__ inline dim3 large_row_grid(int rows, int groups) {
   return FCB_LARGE_UFAST ? dim3(kLUPairs, groups, rows) : dim3(rows, groups, kLUPairs);
 }
 
-// grid = (rows, kpad / 16, ceil(65 / 2)), block = 128 = (u row, plane jl,
-// v class h).  The 16 staged scratch rows of a u row are overwritten by
-// its [v][plane] output tile once every thread holds its FFT.
-__global__ void __launch_bounds__(128, 6) r2c128_rows_kernel(const R2CParams p, int r0, const float2* scr) {
+// grid = large_row_grid(ceil(rows / rpc), kpad / 16 or 1), block = 128 =
+// (u row, slot jl, v class h).  The 16 staged scratch rows of a u row are
+// overwritten by its [v][slot] output tile once every thread holds its FFT.
+// A slot is one plane of the operand row: with kpad >= 16 the CTA's 16 slots
+// are planes j0 .. j0 + 15 of row r; with a narrow kpad of 4 / 8 (a
+// first-layer f = 3) they are rpc = 16 / kpad consecutive rows x kpad planes
+// -- the same 16 consecutive complex of every bin row of F[t][R][kpad], so
+// the output is still one full 128-B line per bin (the first cut left 12 of
+// 16 slots idle and wrote 32-B pieces).  Rows >= r1 (the chunk end) are
+// neither read nor written.
+template <bool NARROW>
+__global__ void __launch_bounds__(128, 6) r2c128_rows_kernel(const R2CParams p, int r0, int r1, const float2* scr) {
   __shared__ __align__(16) float2 buf[kLUPerCta * kLRowBuf];
   pdl_wait();
   pdl_trigger();
-  const int rl = large_br(), r = r0 + rl;
-  const int j0 = blockIdx.y * 16;
-  const int jv = max(0, min(16, p.J - j0));
+  const int kp = p.kpad;
+  constexpr bool narrow = NARROW;  // the launcher's choice: kpad < 16
+  const int rpc = narrow ? 16 / kp : 1;
+  const int rl0 = large_br() * rpc;  // first row of the CTA (relative to r0)
+  const int j0 = narrow ? 0 : blockIdx.y * 16;
+  const int nrows = min(rpc, r1 - (r0 + rl0));  // rows of this CTA inside the chunk
+  // slot jl -> (row rl0 + sub, plane j)
+  auto slot_row = [&](int jl) { return narrow ? jl / kp : 0; };
+  auto slot_j = [&](int jl) { return narrow ? jl % kp : j0 + jl; };
+  auto slot_ok = [&](int jl) { return slot_row(jl) < nrows && slot_j(jl) < p.J; };
   const int src = p.src;
   const int ul = threadIdx.x >> 6, u = large_bu() * kLUPerCta + ul;
   const int t = threadIdx.x & 63;
   float2* rows_s = buf + ul * kLRowBuf;
   const int np = (src + 1) >> 1;
   if (u < kLRows && t < np) {  // separate the packed column pairs (K1a): A = (Z[u] + conj Z[-u]) / 2,
-    long long us;                                                     // B = (Z[u] - conj Z[-u]) / 2i
-    const float2* zp = large_scr_plane(const_cast<float2*>(scr), rl, j0, p.J, np, us) + t;
+    float2 za[16], zb[16];     //                                          B = (Z[u] - conj Z[-u]) / 2i
+    if constexpr (!narrow) {  // 16 planes of one row: one base pointer, plane stride js
+      long long us;
+      const float2* zp = large_scr_plane(const_cast<float2*>(scr), rl0, j0, p.J, np, us) + t;
 #if FCB_LARGE_GLAYOUT
-    const long long js = large_npad(np);  // plane stride inside a u row block
+      const long long js = large_npad(np);
 #else
-    const long long js = (long long)kL * np;
+      const long long js = (long long)kL * np;
 #endif
-    const long long ou = (long long)u * us, onu = (long long)((kL - u) & (kL - 1)) * us;
-    float2 za[16], zb[16];
+      const long long ou = (long long)u * us, onu = (long long)((kL - u) & (kL - 1)) * us;
+      const int jv = max(0, min(16, p.J - j0));
 #pragma unroll
-    for (int jl = 0; jl < 16; ++jl)  // all 32 loads in flight before the first use
-      if (jl < jv) {
-        za[jl] = zp[jl * js + ou];
-        zb[jl] = zp[jl * js + onu];
-      }
+      for (int jl = 0; jl < 16; ++jl)  // all 32 loads in flight before the first use
+        if (jl < jv) {
+          za[jl] = zp[jl * js + ou];
+          zb[jl] = zp[jl * js + onu];
+        }
+    } else {
+#pragma unroll
+      for (int jl = 0; jl < 16; ++jl)
+        if (slot_ok(jl)) {
+          long long us;
+          const float2* zp =
+              large_scr_plane(const_cast<float2*>(scr), rl0 + slot_row(jl), slot_j(jl), p.J, np, us) + t;
+          za[jl] = zp[(long long)u * us];
+          zb[jl] = zp[(long long)((kL - u) & (kL - 1)) * us];
+        }
+    }
 #pragma unroll
     for (int jl = 0; jl < 16; ++jl)
-      if (jl < jv) {  // pair (2t, 2t + 1); a column at x = src (odd src) is zero
+      if (slot_ok(jl)) {  // pair (2t, 2t + 1); a column at x = src (odd src) is zero
         const bool two = 2 * t + 1 < src;
         *reinterpret_cast<float4*>(rows_s + jl * kLRowPadF + 2 * t) =
             make_float4(0.5f * (za[jl].x + zb[jl].x), 0.5f * (za[jl].y - zb[jl].y),
@@ -390,11 +418,11 @@ __global__ void __launch_bounds__(128, 6) r2c128_rows_kernel(const R2CParams p, 
       }
   }
   __syncthreads();
-  // FFT phase: warp = class h (warp-uniform switch), lanes = (u row, plane)
+  // FFT phase: warp = class h (warp-uniform), lanes = (u row, slot)
   const int h = threadIdx.x >> 5, cul = (threadIdx.x >> 4) & 1, jl = threadIdx.x & 15;
   const int cu = large_bu() * kLUPerCta + cul;
   float2 z[32];
-  const bool act = cu < kLRows && jl < jv;
+  const bool act = cu < kLRows && slot_ok(jl);
   if (act) {
     r2c128_row(buf + cul * kLRowBuf + jl * kLRowPadF, z, src, h);
   }
@@ -411,13 +439,14 @@ __global__ void __launch_bounds__(128, 6) r2c128_rows_kernel(const R2CParams p, 
     }
   }
   __syncthreads();
-  // 128 bins x 16 planes per u row: one 128-B line per bin (a narrow kpad
-  // of 4 / 8 -- first-layer f = 3 -- writes only its 32 / 64 B)
-  const long long bstride = (long long)p.R * p.kpad;  // float2 per bin
+  // 128 bins x 16 slots per u row: one 128-B line per bin (fewer bytes only
+  // where the chunk ends inside the CTA's rows, or kpad < 16 on one row)
+  const long long bstride = (long long)p.R * kp;  // float2 per bin
   if (u < kLRows) {
     const float2* tile = rows_s;
-    float2* out = reinterpret_cast<float2*>(p.out) + (long long)u * kL * bstride + (long long)r * p.kpad + j0;
-    if (p.kpad - j0 >= 16) {
+    float2* out = reinterpret_cast<float2*>(p.out) + (long long)u * kL * bstride + (long long)(r0 + rl0) * kp + j0;
+    const int width = narrow ? nrows * kp : min(16, kp - j0);  // complex per bin (even)
+    if (width == 16) {
 #pragma unroll 8
       for (int i = t; i < kL * 8; i += 64) {
         const int v = i >> 3, part = i & 7;
@@ -425,7 +454,7 @@ __global__ void __launch_bounds__(128, 6) r2c128_rows_kernel(const R2CParams p, 
             *reinterpret_cast<const float4*>(tile + v * 16 + 2 * part);
       }
     } else {
-      const int hp = (p.kpad - j0) >> 1;  // float4 parts per bin (kpad is 4 or 8 here)
+      const int hp = width >> 1;  // float4 parts per bin
       for (int i = t; i < kL * hp; i += 64) {
         const int v = i / hp, part = i - v * hp;
         *reinterpret_cast<float4*>(out + v * bstride + 2 * part) =
@@ -433,9 +462,16 @@ __global__ void __launch_bounds__(128, 6) r2c128_rows_kernel(const R2CParams p, 
       }
     }
   }
-  if (p.amax) {  // row r's maximum
-    amx = __reduce_max_sync(0xffffffffu, amx);
-    if ((threadIdx.x & 31) == 0) atomicMax(p.amax + r, ((unsigned long long)p.epoch << 32) | amx);
+  if (p.amax) {  // each row's maximum: reduce over the lanes of the same row
+    if constexpr (narrow) {
+      for (int m = 1; m < kp; m <<= 1) amx = max(amx, __shfl_xor_sync(0xffffffffu, amx, m));
+      amx = max(amx, __shfl_xor_sync(0xffffffffu, amx, 16));  // both u rows
+      if ((jl % kp) == 0 && cul == 0 && slot_row(jl) < nrows)
+        atomicMax(p.amax + r0 + rl0 + slot_row(jl), ((unsigned long long)p.epoch << 32) | amx);
+    } else {
+      amx = __reduce_max_sync(0xffffffffu, amx);
+      if ((threadIdx.x & 31) == 0) atomicMax(p.amax + r0 + rl0, ((unsigned long long)p.epoch << 32) | amx);
+    }
   }
 }
 

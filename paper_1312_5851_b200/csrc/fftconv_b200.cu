@@ -478,8 +478,10 @@ static int launch_r2c_large(const R2CParams& p, float2* scr, size_t scr_n, cudaS
       smem_optin(r2c128_cols_kernel, smem);
       launch_pdl(r2c128_cols_kernel, dim3(rows * p.J), dim3(256), smem, st, p, r0, scr);
     }
-    launch_pdl(r2c128_rows_kernel, large_row_grid(rows, (p.kpad + 15) / 16), dim3(128), 0, st, p, r0,
-               (const float2*)scr);
+    const int rpc16 = p.kpad < 16 ? 16 / p.kpad : 1;  // narrow kpad: rows per K1b CTA
+    launch_pdl(p.kpad < 16 ? r2c128_rows_kernel<true> : r2c128_rows_kernel<false>,
+               large_row_grid((rows + rpc16 - 1) / rpc16, p.kpad < 16 ? 1 : p.kpad / 16), dim3(128), 0, st, p, r0,
+               r0 + rows, (const float2*)scr);
     nl += 2;
   }
   return nl;
