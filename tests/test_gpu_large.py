@@ -146,6 +146,16 @@ def test_ops_m128_chunked_scratch(dev, monkeypatch):
     _check_ops(LayerConfig(7, 128, 16, 8, 4), 4100, dev)
 
 
+@pytest.mark.parametrize("cfg", [(11, 128, 3, 5, 7), (9, 120, 6, 4, 5)])
+def test_ops_m128_narrow_kpad_chunked_rows(dev, monkeypatch, cfg):
+    """A narrow kpad (f <= 8: 4 or 8) packs 16 / kpad operand rows into one
+    K1b CTA; with 1 MiB of scratch the chunks hold a few rows each, so CTAs
+    straddle chunk ends (rows past the chunk must be neither read nor
+    written) and the batch is not a multiple of the rows per CTA."""
+    monkeypatch.setenv("FFTCONV_B200_LSCRATCH_MB", "1")
+    _check_ops(LayerConfig(*cfg), 4300 + sum(cfg), dev)
+
+
 def test_ops_m128_reused_workspace_with_smaller_layers(dev):
     """One workspace serving m = 128 and m = 32 layers (conv_fft_test.cpp:191-209)."""
     big, small = LayerConfig(11, 128, 3, 8, 2), LayerConfig(5, 32, 4, 4, 2)
