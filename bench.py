@@ -80,6 +80,13 @@ class ClockSampler:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
                  "-lms", "50", "-f", self.path], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+            # nvidia-smi's start-up (NVML init) stalls the driver for a moment:
+            # let it finish before the timed region (it landed inside the first
+            # timed step of host-driven workloads, e.g. the layer stack)
+            t_end = time.time() + 3.0
+            while time.time() < t_end and os.path.getsize(self.path) == 0 and self.proc.poll() is None:
+                time.sleep(0.02)
+            time.sleep(0.1)
         except Exception:
             self.proc = None
 

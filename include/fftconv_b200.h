@@ -256,6 +256,13 @@ int fftconv_b200_maxpool_forward(const float* x, size_t planes, size_t rows, siz
  * to each window's winner, zero elsewhere. */
 int fftconv_b200_maxpool_backward(const float* gy, const uint32_t* argmax, size_t planes,
                                   size_t rows, size_t cols, float* gx, void* stream);
+/* maxpool_backward followed by the relu_backward of the relu the pool
+ * consumed (layers.hpp:68-83 then :99-109), in one pass: gx = gy routed to
+ * each window's winner where the pooled value y > 0 (the winner's relu
+ * output, so relu(x) > 0 exactly where x > 0), zero elsewhere -- what the two
+ * kernels produce, bit for bit.  y is maxpool_forward's output. */
+int fftconv_b200_maxpool_relu_backward(const float* gy, const uint32_t* argmax, const float* y, size_t planes,
+                                       size_t rows, size_t cols, float* gx, void* stream);
 /* fit_to  layers.hpp:393-407: every plane padded with zeros or cropped at
  * the top-left corner to size x size. */
 int fftconv_b200_fit_to(const float* x, size_t planes, size_t rows, size_t cols, float* y,

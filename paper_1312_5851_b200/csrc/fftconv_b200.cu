@@ -2022,6 +2022,20 @@ int fftconv_b200_maxpool_backward(const float* gy, const uint32_t* argmax, size_
   });
 }
 
+int fftconv_b200_maxpool_relu_backward(const float* gy, const uint32_t* argmax, const float* y, size_t planes,
+                                       size_t rows, size_t cols, float* gx, void* stream) {
+  return guarded(nullptr, [&] {
+    if (rows % 2 || cols % 2)
+      throw Error(FFTCONV_B200_SIZE_ERROR, "maxpool: rows and cols must be even");
+    if (!y) throw Error(FFTCONV_B200_INVALID_ARGUMENT, "maxpool_relu_backward: pooled output required");
+    const long long total = (long long)planes * (rows / 2) * (cols / 2);
+    if (total)
+      maxpool_bwd_kernel<<<plane_grid((long long)planes), 256, 0, (cudaStream_t)stream>>>(
+          gy, argmax, gx, (long long)planes, (int)rows, (int)cols, y);
+    FCB_CUDA(cudaGetLastError());
+  });
+}
+
 int fftconv_b200_fit_to(const float* x, size_t planes, size_t rows, size_t cols, float* y,
                         size_t size, void* stream) {
   return guarded(nullptr, [&] {

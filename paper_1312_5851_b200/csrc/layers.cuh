@@ -99,18 +99,22 @@ __global__ void maxpool_fwd_kernel(const float* __restrict__ x, float* __restric
 
 // layers.hpp:68-83: the windows tile the plane, so every input element is
 // written exactly once: the window's gradient where it won, zero elsewhere.
+// ypool != nullptr: the following relu backward fused in (gradient kept
+// only where the pooled value, the winner's relu output, is > 0)
 __global__ void maxpool_bwd_kernel(const float* __restrict__ gy, const uint32_t* __restrict__ arg,
-                                   float* __restrict__ gx, long long planes, int rows, int cols) {
+                                   float* __restrict__ gx, long long planes, int rows, int cols,
+                                   const float* __restrict__ ypool = nullptr) {
   const int orow = rows / 2, ocol = cols / 2;
   const PlaneTiler tl(ocol);
   if (!tl.rpi) return;
   for (long long pl = blockIdx.x; pl < planes; pl += gridDim.x) {
     float* out = gx + pl * rows * cols;
     const float* g0 = gy + pl * orow * ocol;
+    const float* y0 = ypool ? ypool + pl * orow * ocol : nullptr;
     const uint32_t* a0 = arg + pl * orow * ocol;
     for (int i = tl.i0; i < orow; i += tl.rpi)
       for (int j = tl.j; j < ocol; j += blockDim.x) {
-        const float g = g0[i * ocol + j];
+        const float g = (!y0 || y0[i * ocol + j] > 0.f) ? g0[i * ocol + j] : 0.f;
         const int win = (int)a0[i * ocol + j];
 #pragma unroll
         for (int di = 0; di < 2; ++di) {

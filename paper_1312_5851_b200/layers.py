@@ -18,6 +18,7 @@ torch.  Times are CUDA-event device times per reference category
 from __future__ import annotations
 
 import ctypes as C
+import os
 import enum
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
@@ -336,6 +337,24 @@ def maxpool_backward(gy, rec):
     return gx
 
 
+def maxpool_relu_backward(gy, rec):
+    """maxpool_backward then the backward of the relu that fed the pool, in
+    one pass (fftconv_b200_maxpool_relu_backward): the relu mask at a
+    window's winner is the pooled value > 0."""
+    import torch
+
+    y, arg, shape = rec
+    if tuple(gy.shape) != tuple(y.shape):
+        raise ShapeError("maxpool backward: gradient shape mismatch")
+    S, M, R, Cc = shape
+    gx = torch.empty(shape, dtype=torch.float32, device=gy.device)
+    raise_for_status(_native.lib().fftconv_b200_maxpool_relu_backward(_ptr(gy), _ptr(arg), _ptr(y), S * M, R, Cc,
+                                                                       _ptr(gx), _stream_ptr(torch)),
+                     _native.last_error(None))
+    _launched()
+    return gx
+
+
 def run_iteration(spec: NetworkSpec, params: NetworkParams, batch, ws: ConvWorkspace | None = None,
                   device: int = 0, group=None, comm=None, chunks: int = 4) -> IterationResult:
     """One training iteration (layers.hpp:441-609) on the GPU.  `batch` is a
@@ -441,7 +460,10 @@ def run_iteration(spec: NetworkSpec, params: NetworkParams, batch, ws: ConvWorks
 
         ci = sh.conv_count
         ri, pi = len(relu_rec), len(pool_rec)
-        for st in reversed(spec.stages):
+        rstages = list(reversed(spec.stages))
+        fuse_pool_relu = os.environ.get("FFTCONV_B200_POOL_RELU_FUSE", "1") != "0"
+        relu_done = False  # the pool backward already applied this relu's mask
+        for si, st in enumerate(rstages):
             if st.kind == StageKind.conv:
                 ci -= 1
                 fin, pre = conv_rec[ci]
@@ -462,10 +484,19 @@ def run_iteration(spec: NetworkSpec, params: NetworkParams, batch, ws: ConvWorks
                     break
             elif st.kind == StageKind.relu:
                 ri -= 1
+                if relu_done:
+                    relu_done = False
+                    continue
                 grad = timed("update_grad_input_ms", lambda g=grad, r=relu_rec[ri]: relu_backward(g, r))
             elif st.kind == StageKind.pool:
                 pi -= 1
-                grad = timed("update_grad_input_ms", lambda g=grad, r=pool_rec[pi]: maxpool_backward(g, r))
+                if fuse_pool_relu and si + 1 < len(rstages) and rstages[si + 1].kind == StageKind.relu:
+                    # relu -> pool in the forward order: the relu's backward fused in
+                    grad = timed("update_grad_input_ms",
+                                 lambda g=grad, r=pool_rec[pi]: maxpool_relu_backward(g, r))
+                    relu_done = True
+                else:
+                    grad = timed("update_grad_input_ms", lambda g=grad, r=pool_rec[pi]: maxpool_backward(g, r))
 
         if multi:
             def reduce_all():

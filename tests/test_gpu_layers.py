@@ -50,6 +50,23 @@ def test_forward_relu_fused_equals_relu_of_forward(dev, S, f, fo, n, k):
     assert np.array_equal(yr.cpu().numpy(), layers.relu_forward(y).cpu().numpy())
 
 
+def test_maxpool_relu_backward_fused_equals_two_kernels(dev):
+    """fftconv_b200_maxpool_relu_backward == relu_backward(maxpool_backward(g), x)
+    for a pool fed by relu(x): windows of all zeros (relu'd negatives) and
+    ties included."""
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal((3, 4, 10, 12)).astype(np.float32)
+    x[0, 0, :4, :4] = -1.0        # an all-negative region: pooled value 0
+    x[1, 1, 2:4, 2:4] = 0.5       # a tie
+    xd = _t(x, dev)
+    r = layers.relu_forward(xd)
+    rec = layers.maxpool_forward(r)
+    g = _t(rng.standard_normal(tuple(rec[0].shape)).astype(np.float32), dev)
+    two = layers.relu_backward(layers.maxpool_backward(g, rec), xd).cpu().numpy()
+    one = layers.maxpool_relu_backward(g, rec).cpu().numpy()
+    assert np.array_equal(one, two)
+
+
 def _pool_ref(x):
     S, M, R, Cc = x.shape
     y = np.zeros((S, M, R // 2, Cc // 2), np.float32)

@@ -16,8 +16,11 @@ S = spec.default_batch
 params = layers.init_params(spec, 1234)
 batch = torch.from_numpy(layers.make_batch(spec, S, 1234)).cuda()
 ws = ConvWorkspace(spec.conv_configs(S), device=0)
-for i in range(6):
+for i in range(int(os.environ.get('ITERS', 6))):
     t0 = time.perf_counter()
     r = layers.run_iteration(spec, params, batch, ws=ws)
     t1 = time.perf_counter()
-    print(i, round((t1 - t0) * 1e3, 2), "ms wall", r.times, torch.cuda.memory_allocated() >> 20, "MiB", flush=True)
+    ms = torch.cuda.memory_stats()
+    print(i, round((t1 - t0) * 1e3, 2), "ms wall", r.times, torch.cuda.memory_allocated() >> 20, "MiB",
+          "retries", ms.get("num_alloc_retries"), "device allocs", ms.get("num_device_alloc"),
+          "frees", ms.get("num_device_free"), flush=True)
