@@ -62,58 +62,83 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled in the background."""
+    """nvidia-smi clocks / throttle reasons sampled in the background.
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap,utilization.gpu")
+    Two sampler processes: SM clock and utilization every 50 ms, the
+    throttle reasons every 250 ms.  The reasons query stalls the driver
+    briefly (measured: with it at 50 ms, host-driven layer-stack iterations
+    took multi-ms outliers in the timed region; clocks alone never did,
+    tools/dev/smi_probe.sh), so it runs 5x less often."""
+
+    QF = "clocks.sm,clocks.max.sm,utilization.gpu"
+    QR = ("clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
         self.index = index
-        self.proc = None
-        self.path = None
+        self.procs = []
+        self.paths = []
+
+    def _spawn(self, q, lms):
+        fd, path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        proc = subprocess.Popen(
+            ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+             "-lms", str(lms), "-f", path], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        self.procs.append(proc)
+        self.paths.append(path)
 
     def start(self):
+        if os.environ.get("FFTCONV_BENCH_NO_SMI") == "1":  # diagnostics: no sampler process
+            return
         try:
-            fd, self.path = tempfile.mkstemp(suffix=".csv")
-            os.close(fd)
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "50", "-f", self.path], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+            self._spawn(self.QF, 50)
+            self._spawn(self.QR, 250)
             # nvidia-smi's start-up (NVML init) stalls the driver for a moment:
-            # let it finish before the timed region (it landed inside the first
-            # timed step of host-driven workloads, e.g. the layer stack)
+            # let both finish it before the timed region
             t_end = time.time() + 3.0
-            while time.time() < t_end and os.path.getsize(self.path) == 0 and self.proc.poll() is None:
+            while time.time() < t_end and any(os.path.getsize(p) == 0 and pr.poll() is None
+                                               for p, pr in zip(self.paths, self.procs)):
                 time.sleep(0.02)
             time.sleep(0.1)
         except Exception:
-            self.proc = None
+            self.procs, self.paths = [], []
+
+    @staticmethod
+    def _rows(path, width):
+        rows = []
+        try:
+            with open(path) as fh:
+                for line in fh:
+                    parts = [p.strip() for p in line.split(",")]
+                    if len(parts) >= width:
+                        rows.append(parts)
+            os.unlink(path)
+        except OSError:
+            pass
+        return rows
 
     def stop(self):
-        if not self.proc:
+        if len(self.procs) != 2:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        rows = []
-        with open(self.path) as fh:
-            for line in fh:
-                parts = [p.strip() for p in line.split(",")]
-                if len(parts) >= 8:
-                    rows.append(parts)
-        os.unlink(self.path)
+        for proc in self.procs:
+            proc.terminate()
+            try:
+                proc.wait(timeout=5)
+            except Exception:
+                proc.kill()
+        rows = self._rows(self.paths[0], 3)
+        rrows = self._rows(self.paths[1], 4)
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        loaded = [r for r in rows if r[7] not in ("0", "[N/A]")] or rows
+        loaded = [r for r in rows if r[2] not in ("0", "[N/A]")] or rows
         sm = [float(r[0]) for r in loaded if r[0].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in loaded for i in range(4) if r[3 + i] == "Active"})
+        reasons = sorted({names[i] for r in rrows for i in range(4) if r[i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
-                "reasons": reasons, "samples": len(rows), "samples_under_load": len(loaded)}
+                "reasons": reasons, "samples": len(rows), "samples_under_load": len(loaded),
+                "reason_samples": len(rrows)}
 
 
 # ---------------------------------------------------------------- reference arm
@@ -702,6 +727,12 @@ def run_stack(args):
     wall, launches = [], []
     sampler = ClockSampler(local)
     sampler.start()
+    # the categories are CUDA-event spans around host-issued calls: a Python
+    # garbage-collection pause inside one (the iteration allocates thousands
+    # of objects) idles the GPU and lands in the span, so collect up front
+    import gc
+    gc.collect()
+    gc.disable()
     for i in range(args.steps):
         flush.fill_(float(i))
         torch.cuda.synchronize()
@@ -713,6 +744,7 @@ def run_stack(args):
         launches.append(r.gpu_launches)
         for k in cats:
             cats[k].append(getattr(r.times, k))
+    gc.enable()
     clocks = sampler.stop()
     per = {k: statistics.mean(v) for k, v in cats.items()}
     if world > 1:  # device times, max over ranks

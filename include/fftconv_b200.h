@@ -128,6 +128,27 @@ int fftconv_b200_forward_relu(fftconv_b200_ws* ws, const float* x, size_t S, siz
                               size_t x_cols, const float* w, size_t w_out, size_t w_in, size_t k,
                               float* y, void* stream);
 
+/* The layer stack's fit_to (layers.hpp:393-407) folded into the operators.
+ * forward_fit: x holds the top-left x_rows x x_cols of a layer image of
+ * image x image (zeros elsewhere; x_rows <= image), y is the layer's
+ * (image - k + 1)^2 output -- the same as fit_to(x, image) then forward,
+ * without materialising the padded input.  flags: FFTCONV_B200_FIT_RELU
+ * fuses the following relu (as fftconv_b200_forward_relu).
+ * grad_input_fit: only the top-left gx_size x gx_size of each input-gradient
+ * plane (gx: [S][w_in][gx_size][gx_size], gx_size <= gy_rows + k - 1), i.e.
+ * grad_input then fit_to(gx, gx_size) for a crop.
+ * grad_weight_fit: x as in forward_fit (k = image - gy_rows + 1). */
+#define FFTCONV_B200_FIT_RELU 1u
+int fftconv_b200_forward_fit(fftconv_b200_ws* ws, const float* x, size_t S, size_t f, size_t x_rows,
+                             size_t x_cols, size_t image, const float* w, size_t w_out, size_t w_in, size_t k,
+                             float* y, unsigned flags, void* stream);
+int fftconv_b200_grad_input_fit(fftconv_b200_ws* ws, const float* gy, size_t S, size_t fo, size_t gy_rows,
+                                size_t gy_cols, const float* w, size_t w_out, size_t w_in, size_t k, float* gx,
+                                size_t gx_size, void* stream);
+int fftconv_b200_grad_weight_fit(fftconv_b200_ws* ws, const float* gy, size_t Sg, size_t fo, size_t gy_rows,
+                                 size_t gy_cols, const float* x, size_t Sx, size_t f, size_t x_rows, size_t x_cols,
+                                 size_t image, float* gw, void* stream);
+
 /* ConvWorkspace<float>::grad_input(gy, w)  conv_fft.hpp:115-152.
  * gy: [S][fo][gy_rows][gy_cols]; gx: [S][w_in][n][n], n = gy_rows + k - 1. */
 int fftconv_b200_grad_input(fftconv_b200_ws* ws, const float* gy, size_t S, size_t fo,

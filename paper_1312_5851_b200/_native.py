@@ -30,6 +30,9 @@ SIGNATURES = [
     ("fftconv_b200_forward_relu", _i, [_p, _p, _sz, _sz, _sz, _sz, _p, _sz, _sz, _sz, _p, _p]),
     ("fftconv_b200_grad_input", _i, [_p, _p, _sz, _sz, _sz, _sz, _p, _sz, _sz, _sz, _p, _p]),
     ("fftconv_b200_grad_weight", _i, [_p, _p, _sz, _sz, _sz, _sz, _p, _sz, _sz, _sz, _sz, _p, _p]),
+    ("fftconv_b200_forward_fit", _i, [_p, _p, _sz, _sz, _sz, _sz, _sz, _p, _sz, _sz, _sz, _p, C.c_uint, _p]),
+    ("fftconv_b200_grad_input_fit", _i, [_p, _p, _sz, _sz, _sz, _sz, _p, _sz, _sz, _sz, _p, _sz, _p]),
+    ("fftconv_b200_grad_weight_fit", _i, [_p, _p, _sz, _sz, _sz, _sz, _p, _sz, _sz, _sz, _sz, _sz, _p, _p]),
     ("fftconv_b200_nccl_get_unique_id", _i, [_p]),
     ("fftconv_b200_nccl_comm_create", _i, [_p, _i, _i, _i, C.POINTER(_p)]),
     ("fftconv_b200_nccl_comm_destroy", _i, [_p]),

@@ -1034,14 +1034,20 @@ int c2r_run(fftconv_b200_ws* ws, size_t m, const C2RParams& c, cudaStream_t st) 
   return 1;
 }
 
+// n_logical > xr: the input planes are the top-left xr x xr of the layer's
+// n x n image, zero elsewhere (the layer stack's fit_to pad, layers.hpp:393-407,
+// folded in: K1 zero-fills beyond the source edge anyway).
 void run_forward(fftconv_b200_ws* ws, const float* x, size_t S, size_t f, size_t xr, size_t xc,
-                 const float* w, size_t wo, size_t wi, size_t k, float* y, cudaStream_t st, bool relu = false) {
+                 const float* w, size_t wo, size_t wi, size_t k, float* y, cudaStream_t st, bool relu = false,
+                 size_t n_logical = 0) {
   require_nonzero(S, f, xr, xc, "Tensor4");
   require_nonzero(wo, wi, k, 1, "Weights4");
   if (xr != xc) throw Error(FFTCONV_B200_SIZE_ERROR, "forward_fft: planes must be square");
   if (wi != f) throw Error(FFTCONV_B200_SHAPE_ERROR, "forward_fft: weight in_maps != input maps");
-  if (k > xr) throw Error(FFTCONV_B200_SIZE_ERROR, "forward_fft: kernel larger than image");
-  const size_t n = xr, no = n - k + 1, fo = wo;
+  const size_t n = n_logical ? n_logical : xr;
+  if (xr > n) throw Error(FFTCONV_B200_SIZE_ERROR, "forward_fft: input larger than the layer image");
+  if (k > n) throw Error(FFTCONV_B200_SIZE_ERROR, "forward_fft: kernel larger than image");
+  const size_t no = n - k + 1, fo = wo;
   const fftconv_b200_layer cfg{k, n, f, fo, S};
   const size_t m = prepare(ws, cfg);
   const size_t bins = m * (m / 2 + 1);
@@ -1049,8 +1055,8 @@ void run_forward(fftconv_b200_ws* ws, const float* x, size_t S, size_t f, size_t
   const size_t kp = kpad_for(f, m);
 
   record(ws, 0, st);
-  R2CParams a{x, ws->bufA, (long long)(f * n * n), (long long)(n * n), (int)S, (int)f, (int)kp,
-              (int)n, (int)(n | 1)};
+  R2CParams a{x, ws->bufA, (long long)(f * xr * xr), (long long)(xr * xr), (int)S, (int)f, (int)kp,
+              (int)xr, (int)(xr | 1)};
   R2CParams b{w, ws->bufB, (long long)(f * k * k), (long long)(k * k), (int)fo, (int)f, (int)kp,
               (int)k, (int)(k | 1)};
   const GemmRoute route = gemm_route(ws_gemm_kind(ws), S, fo, f, bins);
@@ -1081,9 +1087,12 @@ void run_forward(fftconv_b200_ws* ws, const float* x, size_t S, size_t f, size_t
   ws->ctr[2] += (uint64_t)bins * fo * f * S;
 }
 
+// gx_size < n: only the top-left gx_size x gx_size of every input-gradient
+// plane is written (the stack's fit_to crop back to the pre-pad size folded
+// into K4's crop).
 void run_grad_input(fftconv_b200_ws* ws, const float* gy, size_t S, size_t fo, size_t gr,
                     size_t gc, const float* w, size_t wo, size_t wi, size_t k, float* gx,
-                    cudaStream_t st) {
+                    cudaStream_t st, size_t gx_size = 0) {
   require_nonzero(S, fo, gr, gc, "Tensor4");
   require_nonzero(wo, wi, k, 1, "Weights4");
   if (gr != gc) throw Error(FFTCONV_B200_SIZE_ERROR, "grad_input_fft: planes must be square");
@@ -1105,7 +1114,9 @@ void run_grad_input(fftconv_b200_ws* ws, const float* gy, size_t S, size_t fo, s
   const int nl = r2c_operands(ws, m, a, b, st, route);
   record(ws, 1, st);  // both forward transforms
   record(ws, 2, st);
-  C2RParams c{ws->bufD, gx, (long long)(n * n), (long long)(f * n * n), (int)f, (int)S, (int)n,
+  const size_t ge = gx_size ? gx_size : n;  // output plane edge
+  if (ge > n) throw Error(FFTCONV_B200_SIZE_ERROR, "grad_input_fft: output larger than the layer image");
+  C2RParams c{ws->bufD, gx, (long long)(ge * ge), (long long)(f * ge * ge), (int)f, (int)S, (int)ge,
               0, 0, 1.0f / (float)(m * m), (int)round_up(S, 2)};
   int ng;
   if (!gemm_swap(S, f)) {  // D[t][f][b]
@@ -1114,7 +1125,7 @@ void run_grad_input(fftconv_b200_ws* ws, const float* gy, size_t S, size_t fo, s
   } else {  // D^T[t][b][f]
     ng = launch_gemm(ws->bufB, ws->bufA, ws->bufD, bins, f, S, kp, -1.0f, c2r_layout(m), round_up(f, 2),
                      ws->di, st, route, b.amax, a.amax, ws->gemm_path, ws->span_slot(1));
-    c = C2RParams{ws->bufD, gx, (long long)(f * n * n), (long long)(n * n), (int)S, (int)f, (int)n,
+    c = C2RParams{ws->bufD, gx, (long long)(f * ge * ge), (long long)(ge * ge), (int)S, (int)f, (int)ge,
                   0, 0, 1.0f / (float)(m * m), (int)round_up(f, 2)};
   }
   record(ws, 3, st);
@@ -1138,13 +1149,15 @@ struct ChunkHook {
 
 void run_grad_weight(fftconv_b200_ws* ws, const float* gy, size_t Sg, size_t fo, size_t gr,
                      size_t gc, const float* x, size_t Sx, size_t f, size_t xr, size_t xc,
-                     float* gw, cudaStream_t st, bool accum = false, const ChunkHook* hook = nullptr) {
+                     float* gw, cudaStream_t st, bool accum = false, const ChunkHook* hook = nullptr,
+                     size_t n_logical = 0) {
   require_nonzero(Sg, fo, gr, gc, "Tensor4");
   require_nonzero(Sx, f, xr, xc, "Tensor4");
   if (gr != gc) throw Error(FFTCONV_B200_SIZE_ERROR, "grad_weight_fft: planes must be square");
   if (xr != xc) throw Error(FFTCONV_B200_SIZE_ERROR, "grad_weight_fft: planes must be square");
   if (Sg != Sx) throw Error(FFTCONV_B200_SHAPE_ERROR, "grad_weight_fft: batch mismatch");
-  const size_t no = gr, n = xr;
+  const size_t no = gr, n = n_logical ? n_logical : xr;  // n_logical: as run_forward
+  if (xr > n) throw Error(FFTCONV_B200_SIZE_ERROR, "grad_weight_fft: input larger than the layer image");
   if (no > n) throw Error(FFTCONV_B200_SIZE_ERROR, "grad_weight_fft: gradient larger than input");
   const size_t k = n - no + 1, S = Sx;
   const fftconv_b200_layer cfg{k, n, f, fo, S};
@@ -1156,8 +1169,8 @@ void run_grad_weight(fftconv_b200_ws* ws, const float* gy, size_t Sg, size_t fo,
   record(ws, 0, st);
   R2CParams a{gy, ws->bufA, (long long)(no * no), (long long)(fo * no * no), (int)fo, (int)S,
               (int)kp, (int)no, (int)(no | 1)};
-  R2CParams b{x, ws->bufB, (long long)(n * n), (long long)(f * n * n), (int)f, (int)S, (int)kp,
-              (int)n, (int)(n | 1)};
+  R2CParams b{x, ws->bufB, (long long)(xr * xr), (long long)(f * xr * xr), (int)f, (int)S, (int)kp,
+              (int)xr, (int)(xr | 1)};
   const GemmRoute route = gemm_route(ws_gemm_kind(ws), fo, f, S, bins);
   const int nl = r2c_operands(ws, m, a, b, st, route);
   record(ws, 1, st);  // both forward transforms
@@ -1365,6 +1378,44 @@ int fftconv_b200_forward_relu(fftconv_b200_ws* ws, const float* x, size_t S, siz
     DeviceGuard g(ws->device);
     order_after_last(ws, (cudaStream_t)stream);
     run_forward(ws, x, S, f, x_rows, x_cols, w, w_out, w_in, k, y, (cudaStream_t)stream, true);
+    mark_done(ws, (cudaStream_t)stream);
+  });
+}
+
+int fftconv_b200_forward_fit(fftconv_b200_ws* ws, const float* x, size_t S, size_t f, size_t x_rows,
+                             size_t x_cols, size_t image, const float* w, size_t w_out, size_t w_in, size_t k,
+                             float* y, unsigned flags, void* stream) {
+  if (!ws) return FFTCONV_B200_INVALID_ARGUMENT;
+  return guarded(ws, [&] {
+    DeviceGuard g(ws->device);
+    order_after_last(ws, (cudaStream_t)stream);
+    run_forward(ws, x, S, f, x_rows, x_cols, w, w_out, w_in, k, y, (cudaStream_t)stream,
+                (flags & FFTCONV_B200_FIT_RELU) != 0, image);
+    mark_done(ws, (cudaStream_t)stream);
+  });
+}
+
+int fftconv_b200_grad_input_fit(fftconv_b200_ws* ws, const float* gy, size_t S, size_t fo, size_t gy_rows,
+                                size_t gy_cols, const float* w, size_t w_out, size_t w_in, size_t k, float* gx,
+                                size_t gx_size, void* stream) {
+  if (!ws) return FFTCONV_B200_INVALID_ARGUMENT;
+  return guarded(ws, [&] {
+    DeviceGuard g(ws->device);
+    order_after_last(ws, (cudaStream_t)stream);
+    run_grad_input(ws, gy, S, fo, gy_rows, gy_cols, w, w_out, w_in, k, gx, (cudaStream_t)stream, gx_size);
+    mark_done(ws, (cudaStream_t)stream);
+  });
+}
+
+int fftconv_b200_grad_weight_fit(fftconv_b200_ws* ws, const float* gy, size_t Sg, size_t fo, size_t gy_rows,
+                                 size_t gy_cols, const float* x, size_t Sx, size_t f, size_t x_rows, size_t x_cols,
+                                 size_t image, float* gw, void* stream) {
+  if (!ws) return FFTCONV_B200_INVALID_ARGUMENT;
+  return guarded(ws, [&] {
+    DeviceGuard g(ws->device);
+    order_after_last(ws, (cudaStream_t)stream);
+    run_grad_weight(ws, gy, Sg, fo, gy_rows, gy_cols, x, Sx, f, x_rows, x_cols, gw, (cudaStream_t)stream, false,
+                    nullptr, image);
     mark_done(ws, (cudaStream_t)stream);
   });
 }

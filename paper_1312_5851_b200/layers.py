@@ -253,15 +253,19 @@ class _CountingWorkspace:
         _launched(self.ws.last_launch_count())
         return r
 
-    def forward(self, x, w, relu=False):
-        if relu:
-            return self._run(lambda a, b: self.ws.forward(a, b, relu=True), x, w)
+    def forward(self, x, w, relu=False, image=None):
+        if relu or image:
+            return self._run(lambda a, b: self.ws.forward(a, b, relu=relu, image=image), x, w)
         return self._run(self.ws.forward, x, w)
 
-    def grad_input(self, gy, w):
+    def grad_input(self, gy, w, size=None):
+        if size:
+            return self._run(lambda a, b: self.ws.grad_input(a, b, size=size), gy, w)
         return self._run(self.ws.grad_input, gy, w)
 
-    def grad_weight(self, gy, x):
+    def grad_weight(self, gy, x, image=None):
+        if image:
+            return self._run(lambda a, b: self.ws.grad_weight(a, b, image=image), gy, x)
         return self._run(self.ws.grad_weight, gy, x)
 
 
@@ -411,6 +415,15 @@ def run_iteration(spec: NetworkSpec, params: NetworkParams, batch, ws: ConvWorks
 
     try:
         conv_rec, relu_rec, pool_rec = [], [], []
+        # the backward's fit_to crops folded into grad_input's K4 crop
+        # (fftconv_b200_grad_input_fit: the same values, fewer written).  The
+        # forward pad stays explicit: folding it too (forward_fit on the
+        # unpadded planes) is exact in real arithmetic, but K1's zero-pruned
+        # transforms round differently, and outputs whose receptive field is
+        # all padding (exactly 0) then come out as different +-1e-7 noise --
+        # relu / max-pool decisions on that noise flip and the gradients move
+        # by ~1e-4 relative (measured on reference-net-small).
+        fold_fit = os.environ.get("FFTCONV_B200_FOLD_FIT", "1") != "0"
         state = {"cur": x, "fc_in": None, "scores": None}
 
         def forward_all():
@@ -419,9 +432,10 @@ def run_iteration(spec: NetworkSpec, params: NetworkParams, batch, ws: ConvWorks
             for si, st in enumerate(spec.stages):
                 cur = state["cur"]
                 if st.kind == StageKind.conv:
-                    fin = fit_to(cur, st.conv.image)
-                    conv_rec.append((fin, cur.shape[2]))
                     fused = si + 1 < len(spec.stages) and spec.stages[si + 1].kind == StageKind.relu
+                    fin = fit_to(cur, st.conv.image)
+                    # a padded input's gradient is cropped back inside K4 (below)
+                    conv_rec.append((fin, cur.shape[2], fold_fit and cur.shape[2] < st.conv.image))
                     state["cur"] = ws.forward(fin, w_dev[ci], relu=fused)
                     ci += 1
                 elif st.kind == StageKind.relu:
@@ -466,7 +480,7 @@ def run_iteration(spec: NetworkSpec, params: NetworkParams, batch, ws: ConvWorks
         for si, st in enumerate(rstages):
             if st.kind == StageKind.conv:
                 ci -= 1
-                fin, pre = conv_rec[ci]
+                fin, pre, crop_in_k4 = conv_rec[ci]
                 g = grad
                 if sharded is not None:  # all-reduce overlaps the remaining backward layers
                     def acc(g=g, fin=fin):
@@ -477,8 +491,12 @@ def run_iteration(spec: NetworkSpec, params: NetworkParams, batch, ws: ConvWorks
                 else:
                     conv_grads[ci] = timed("acc_grad_ms", lambda g=g, fin=fin: ws.grad_weight(g, fin))
                 if ci > 0:
-                    grad = timed("update_grad_input_ms",
-                                 lambda g=g, c=ci, pre=pre: fit_to(ws.grad_input(g, w_dev[c]), pre))
+                    if crop_in_k4:  # fftconv_b200_grad_input_fit: fit_to's crop inside K4
+                        grad = timed("update_grad_input_ms",
+                                     lambda g=g, c=ci, pre=pre: ws.grad_input(g, w_dev[c], size=pre))
+                    else:
+                        grad = timed("update_grad_input_ms",
+                                     lambda g=g, c=ci, pre=pre: fit_to(ws.grad_input(g, w_dev[c]), pre))
                     grad_input_calls += 1
                 else:
                     break

@@ -193,25 +193,33 @@ class ConvWorkspace:
             raise ValueError(f"out must be a C-contiguous float32 array of shape {tuple(shape)}")
         return out
 
-    def forward(self, x, w, threads: int = 1, out=None, relu: bool = False):
+    def forward(self, x, w, threads: int = 1, out=None, relu: bool = False, image: int | None = None):
         """conv_fft.hpp:74-113: y = valid cross-correlation of x by w.
-        relu=True (device operands): the layer stack's following relu
-        (layers.hpp:88-97) fused into the inverse transform's stores."""
+        Device-operand extensions for the layer stack: relu=True fuses the
+        following relu (layers.hpp:88-97) into the inverse transform's
+        stores; image > x's planes treats x as the top-left of an image x
+        image layer input, zeros elsewhere (fit_to's pad, folded in)."""
         S, f, xr, xc = _shape4(x)
         wo, wi, k = _weights_shape(w)
-        no = xr - k + 1 if k <= xr else 1
+        n = image if image else xr
+        no = n - k + 1 if k <= n else 1
         L = _native.lib()
         if _is_torch(x):
             import torch
 
             y = torch.empty((S, wo, max(no, 1), max(no, 1)), dtype=torch.float32, device=x.device)
-            fn = L.fftconv_b200_forward_relu if relu else L.fftconv_b200_forward
-            code = fn(self._h, self._dev_ptr(x), S, f, xr, xc, self._dev_ptr(w), wo, wi, k, self._dev_ptr(y),
-                      self._stream(x))
+            if image and image != xr:
+                code = L.fftconv_b200_forward_fit(self._h, self._dev_ptr(x), S, f, xr, xc, int(image),
+                                                  self._dev_ptr(w), wo, wi, k, self._dev_ptr(y), 1 if relu else 0,
+                                                  self._stream(x))
+            else:
+                fn = L.fftconv_b200_forward_relu if relu else L.fftconv_b200_forward
+                code = fn(self._h, self._dev_ptr(x), S, f, xr, xc, self._dev_ptr(w), wo, wi, k, self._dev_ptr(y),
+                          self._stream(x))
             self._check(code)
             return y
-        if relu:
-            raise ValueError("forward(relu=True) takes device operands")
+        if relu or image:
+            raise ValueError("forward(relu=..., image=...) take device operands")
         xa, xp = self._host(x)
         wa, wp = self._host(w)
         y = self._host_out(out, (S, wo, max(no, 1), max(no, 1)))
@@ -220,8 +228,10 @@ class ConvWorkspace:
         self._check(code)
         return y
 
-    def grad_input(self, gy, w, threads: int = 1, out=None):
-        """conv_fft.hpp:115-152: gx = full convolution of gy by w."""
+    def grad_input(self, gy, w, threads: int = 1, out=None, size: int | None = None):
+        """conv_fft.hpp:115-152: gx = full convolution of gy by w.  size
+        (device operands): only the top-left size x size of each plane
+        (fit_to's crop back to a pre-pad input, folded in)."""
         S, fo, gr, gc = _shape4(gy)
         wo, wi, k = _weights_shape(w)
         n = gr + k - 1
@@ -229,11 +239,18 @@ class ConvWorkspace:
         if _is_torch(gy):
             import torch
 
-            gx = torch.empty((S, wi, n, n), dtype=torch.float32, device=gy.device)
-            code = L.fftconv_b200_grad_input(self._h, self._dev_ptr(gy), S, fo, gr, gc, self._dev_ptr(w), wo, wi,
-                                             k, self._dev_ptr(gx), self._stream(gy))
+            if size and size != n:
+                gx = torch.empty((S, wi, size, size), dtype=torch.float32, device=gy.device)
+                code = L.fftconv_b200_grad_input_fit(self._h, self._dev_ptr(gy), S, fo, gr, gc, self._dev_ptr(w),
+                                                     wo, wi, k, self._dev_ptr(gx), int(size), self._stream(gy))
+            else:
+                gx = torch.empty((S, wi, n, n), dtype=torch.float32, device=gy.device)
+                code = L.fftconv_b200_grad_input(self._h, self._dev_ptr(gy), S, fo, gr, gc, self._dev_ptr(w), wo,
+                                                 wi, k, self._dev_ptr(gx), self._stream(gy))
             self._check(code)
             return gx
+        if size:
+            raise ValueError("grad_input(size=...) takes device operands")
         ga, gp = self._host(gy)
         wa, wp = self._host(w)
         gx = self._host_out(out, (S, wi, n, n))
@@ -242,20 +259,29 @@ class ConvWorkspace:
         self._check(code)
         return gx
 
-    def grad_weight(self, gy, x, threads: int = 1, out=None):
-        """conv_fft.hpp:154-206: gw = batch-summed valid correlation of x by gy."""
+    def grad_weight(self, gy, x, threads: int = 1, out=None, image: int | None = None):
+        """conv_fft.hpp:154-206: gw = batch-summed valid correlation of x by gy.
+        image (device operands): x as in forward(image=...)."""
         Sg, fo, gr, gc = _shape4(gy)
         Sx, f, xr, xc = _shape4(x)
-        k = xr - gr + 1 if gr <= xr else 1
+        n = image if image else xr
+        k = n - gr + 1 if gr <= n else 1
         L = _native.lib()
         if _is_torch(gy):
             import torch
 
             gw = torch.empty((fo, f, k, k), dtype=torch.float32, device=gy.device)
-            code = L.fftconv_b200_grad_weight(self._h, self._dev_ptr(gy), Sg, fo, gr, gc, self._dev_ptr(x), Sx,
-                                              f, xr, xc, self._dev_ptr(gw), self._stream(gy))
+            if image and image != xr:
+                code = L.fftconv_b200_grad_weight_fit(self._h, self._dev_ptr(gy), Sg, fo, gr, gc, self._dev_ptr(x),
+                                                      Sx, f, xr, xc, int(image), self._dev_ptr(gw),
+                                                      self._stream(gy))
+            else:
+                code = L.fftconv_b200_grad_weight(self._h, self._dev_ptr(gy), Sg, fo, gr, gc, self._dev_ptr(x), Sx,
+                                                  f, xr, xc, self._dev_ptr(gw), self._stream(gy))
             self._check(code)
             return gw
+        if image:
+            raise ValueError("grad_weight(image=...) takes device operands")
         ga, gp = self._host(gy)
         xa, xp = self._host(x)
         gw = self._host_out(out, (fo, f, k, k))

@@ -50,6 +50,40 @@ def test_forward_relu_fused_equals_relu_of_forward(dev, S, f, fo, n, k):
     assert np.array_equal(yr.cpu().numpy(), layers.relu_forward(y).cpu().numpy())
 
 
+@pytest.mark.parametrize("S,f,fo,pre,n,k", [
+    (4, 5, 6, 13, 16, 3),     # m = 16
+    (4, 6, 8, 30, 32, 3),     # m = 32 (AlexNet conv3-5)
+    (2, 4, 6, 59, 64, 5),     # m = 64 (AlexNet conv2)
+    (2, 3, 4, 100, 128, 11),  # m = 128
+])
+def test_fit_folded_operators_equal_fit_to_then_operator(dev, S, f, fo, pre, n, k):
+    """forward_fit / grad_weight_fit on the pre x pre planes with the layer
+    image n == the operators on fit_to(x, n); grad_input_fit(size=pre) ==
+    fit_to(grad_input, pre)."""
+    import torch
+
+    from paper_1312_5851_b200 import ConvWorkspace, LayerConfig
+
+    rng = np.random.default_rng(pre * 7 + n)
+    x = _t(rng.standard_normal((S, f, pre, pre)).astype(np.float32), dev)
+    w = _t(rng.standard_normal((fo, f, k, k)).astype(np.float32), dev)
+    no = n - k + 1
+    gy = _t(rng.standard_normal((S, fo, no, no)).astype(np.float32), dev)
+    ws = ConvWorkspace([LayerConfig(k, n, f, fo, S)], device=0)
+    xp = layers.fit_to(x, n)
+    pairs = [
+        (ws.forward(x, w, image=n), ws.forward(xp, w)),
+        (ws.forward(x, w, image=n, relu=True), layers.relu_forward(ws.forward(xp, w))),
+        (ws.grad_input(gy, w, size=pre), layers.fit_to(ws.grad_input(gy, w), pre)),
+        (ws.grad_weight(gy, x, image=n), ws.grad_weight(gy, xp)),
+    ]
+    torch.cuda.synchronize()
+    for got, want in pairs:
+        g, r = got.cpu().numpy(), want.cpu().numpy()
+        assert g.shape == r.shape
+        assert oracle.rel_l2_error(g, r) <= 1e-6
+
+
 def test_maxpool_relu_backward_fused_equals_two_kernels(dev):
     """fftconv_b200_maxpool_relu_backward == relu_backward(maxpool_backward(g), x)
     for a pool fed by relu(x): windows of all zeros (relu'd negatives) and
