@@ -64,13 +64,15 @@ def load_peaks():
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled in the background.
 
-    Two sampler processes: SM clock and utilization every 50 ms, the
-    throttle reasons every 250 ms.  The reasons query stalls the driver
-    briefly (measured: with it at 50 ms, host-driven layer-stack iterations
-    took multi-ms outliers in the timed region; clocks alone never did,
-    tools/dev/smi_probe.sh), so it runs 5x less often."""
+    Two sampler processes: the SM clock every 50 ms, the throttle reasons
+    every 250 ms.  The reasons and utilization queries stall the host driver
+    calls briefly (measured: with them at 50 ms, host-driven layer-stack
+    iterations took 10-150 ms outliers in the timed region; clocks alone
+    never did, tools/dev/smi_probe.sh, tools/dev/stack_rep.sh), so the
+    reasons run 5x less often and utilization is not sampled (the samplers
+    run only around the timed steps, so every sample is under load)."""
 
-    QF = "clocks.sm,clocks.max.sm,utilization.gpu"
+    QF = "clocks.sm,clocks.max.sm"
     QR = ("clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
           "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -127,11 +129,11 @@ class ClockSampler:
                 proc.wait(timeout=5)
             except Exception:
                 proc.kill()
-        rows = self._rows(self.paths[0], 3)
+        rows = self._rows(self.paths[0], 2)
         rrows = self._rows(self.paths[1], 4)
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        loaded = [r for r in rows if r[2] not in ("0", "[N/A]")] or rows
+        loaded = rows  # the samplers run only around the timed steps
         sm = [float(r[0]) for r in loaded if r[0].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in rrows for i in range(4) if r[i] == "Active"})

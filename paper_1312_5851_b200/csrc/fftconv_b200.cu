@@ -299,8 +299,20 @@ static bool small_src_enabled() {
 // m = 64 only: measured W 4.27 -> 3.87 ms and the n = 64 sweep point k = 7
 // 1.045 -> 1.011 ms, but P (m = 32, where K1's 8-plane groups already store
 // 64-B pieces) 265 -> 292 us.
+// m = 32 only when FFTCONV_B200_SMALLSRC32_MIN (planes) is set and the
+// operand has at least that many planes (tests force it): even AlexNet's
+// 3 x 3 conv3-5 weights (98k-147k planes) ran slower through it (iteration
+// 10.75 -> 11.70 ms; the extra launch and the 16-point row FFTs cost more
+// than the full-line stores save at m = 32).
+static size_t small_src32_min() {
+  const char* e = getenv("FFTCONV_B200_SMALLSRC32_MIN");
+  return (e && atoll(e) > 0) ? (size_t)atoll(e) : 0;
+}
 static bool small_src_ok(size_t m, const R2CParams& p) {
-  return small_src_enabled() && m == 64 && (size_t)p.src * 4 <= m && p.src >= 1;
+  if (!small_src_enabled() || p.src < 1 || (size_t)p.src * 4 > m) return false;
+  if (m == 64) return true;
+  const size_t mn = small_src32_min();
+  return m == 32 && mn && (size_t)p.R * p.kpad >= mn;
 }
 template <int M>
 static void launch_r2c_small_src(const R2CParams& p, const DevInfo& di, cudaStream_t st, unsigned long long* tspan) {

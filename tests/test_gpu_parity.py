@@ -71,6 +71,18 @@ def test_matches_direct_mixed_configs(dev, cfg, seed):
     _assert_close(got, ref, (1e-4, 1e-4, 1e-4))
 
 
+@pytest.mark.parametrize("cfg", [(3, 32, 24, 20, 3), (7, 30, 17, 33, 2), (8, 32, 5, 6, 4)])
+def test_small_src_k1_at_m32_vs_direct(dev, monkeypatch, cfg):
+    """The small-plane K1 (fft_small.cuh) at m = 32 (off by default, measured
+    slower there; FFTCONV_B200_SMALLSRC32_MIN enables it), forced on for
+    every small-plane operand here."""
+    monkeypatch.setenv("FFTCONV_B200_SMALLSRC32_MIN", "1")
+    cfg = LayerConfig(*cfg)
+    x, w, gy = _inputs(cfg, 4400 + cfg.kernel)
+    got = _run_all(ConvWorkspace([cfg]), x, w, gy, dev)
+    _assert_close(got, _direct64(x, w, gy))
+
+
 # ------------------------------------------------- BASELINE configs[0]
 def test_small_cpu_config_vs_direct_oracle(dev):
     cfg = LayerConfig(kernel=5, image=32, in_maps=16, out_maps=16, batch=8)
