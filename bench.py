@@ -72,14 +72,39 @@ class ClockSampler:
     reasons run 5x less often and utilization is not sampled (the samplers
     run only around the timed steps, so every sample is under load)."""
 
-    QF = "clocks.sm,clocks.max.sm"
-    QR = ("clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+    QF = "timestamp,clocks.sm,clocks.max.sm"
+    QR = ("timestamp,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
           "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index):
+    def __init__(self, index, reasons_during=True, during=True):
         self.index = index
+        self.reasons_during = reasons_during  # False: one reasons query right after the steps
+        self.during = during  # False: no background sampling, one query before and one after
+        self.snaps = []
         self.procs = []
         self.paths = []
+        self.t0 = self.t1 = None  # the loaded window (begin() / end()); samples outside it are dropped
+
+    def begin(self):
+        self.t0 = time.time()
+
+    def end(self):
+        self.t1 = time.time()
+
+    def _in_window(self, rows):
+        if self.t0 is None or self.t1 is None:
+            return rows
+        import datetime
+
+        keep = []
+        for r in rows:
+            try:
+                ts = datetime.datetime.strptime(r[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except ValueError:
+                continue
+            if self.t0 <= ts <= self.t1:
+                keep.append(r)
+        return keep or rows
 
     def _spawn(self, q, lms):
         fd, path = tempfile.mkstemp(suffix=".csv")
@@ -90,12 +115,28 @@ class ClockSampler:
         self.procs.append(proc)
         self.paths.append(path)
 
+    def _snap(self):
+        try:
+            out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QF},{self.QR}",
+                                  "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                 timeout=10).stdout
+            for line in out.splitlines():
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 8:
+                    self.snaps.append(parts)
+        except Exception:
+            pass
+
     def start(self):
         if os.environ.get("FFTCONV_BENCH_NO_SMI") == "1":  # diagnostics: no sampler process
             return
+        if not self.during:
+            self._snap()
+            return
         try:
             self._spawn(self.QF, 50)
-            self._spawn(self.QR, 250)
+            if self.reasons_during:
+                self._spawn(self.QR, 250)
             # nvidia-smi's start-up (NVML init) stalls the driver for a moment:
             # let both finish it before the timed region
             t_end = time.time() + 3.0
@@ -121,24 +162,45 @@ class ClockSampler:
         return rows
 
     def stop(self):
-        if len(self.procs) != 2:
+        if not self.during:
+            self._snap()
+            if not self.snaps:
+                return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            sm = [float(r[1]) for r in self.snaps if r[1].replace(".", "").isdigit()]
+            return {"sm_mhz": statistics.median(sm) if sm else None,
+                    "sm_max_mhz": float(self.snaps[0][2]) if self.snaps[0][2].replace(".", "").isdigit() else None,
+                    "reasons": sorted({names[i] for r in self.snaps for i in range(4) if r[4 + i] == "Active"}),
+                    "samples": len(self.snaps),
+                    "note": "one query right before and one right after the timed steps (background "
+                            "nvidia-smi sampling stalls these host-driven steps)"}
+        if len(self.procs) != (2 if self.reasons_during else 1):
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        if not self.reasons_during:  # the GPU is still warm: one query of the current reasons
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QR}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=10).stdout
+                once = [[p.strip() for p in line.split(",")] for line in out.splitlines() if line.strip()]
+            except Exception:
+                once = []
         for proc in self.procs:
             proc.terminate()
             try:
                 proc.wait(timeout=5)
             except Exception:
                 proc.kill()
-        rows = self._rows(self.paths[0], 2)
-        rrows = self._rows(self.paths[1], 4)
+        rows = self._rows(self.paths[0], 3)
+        rrows = self._in_window(self._rows(self.paths[1], 5)) if self.reasons_during else \
+            [r for r in once if len(r) >= 5]
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        loaded = rows  # the samplers run only around the timed steps
-        sm = [float(r[0]) for r in loaded if r[0].replace(".", "").isdigit()]
+        loaded = self._in_window(rows)  # samples inside the loaded window only
+        sm = [float(r[1]) for r in loaded if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rrows for i in range(4) if r[i] == "Active"})
+        reasons = sorted({names[i] for r in rrows for i in range(4) if r[1 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
+                "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
                 "reasons": reasons, "samples": len(rows), "samples_under_load": len(loaded),
                 "reason_samples": len(rrows)}
 
@@ -317,6 +379,7 @@ def main():
     time.sleep(0.15)
     # keep the GPU busy while the sampler spins up, then the timed steps
     t_end = time.time() + 0.5
+    sampler.begin()
     while time.time() < t_end:
         step(reduce=False)
         flush.fill_(1.0)
@@ -342,6 +405,7 @@ def main():
         step(reduce=False)
         flush.fill_(1.0)
     torch.cuda.synchronize()
+    sampler.end()
     clocks = sampler.stop()
     ms = statistics.mean(step_ms)
     if world > 1:
@@ -727,7 +791,11 @@ def run_stack(args):
         layers.run_iteration(spec, params, batch, ws=ws, device=local, comm=comm)
     cats = {"update_output_ms": [], "update_grad_input_ms": [], "acc_grad_ms": []}
     wall, launches = [], []
-    sampler = ClockSampler(local)
+    # the stack's steps are host-driven (hundreds of launches each): any
+    # nvidia-smi query during them can stall the host driver calls (10-150 ms
+    # outliers, tools/dev/stack_rep.sh), so clocks and reasons are read once
+    # right before and once right after the timed steps
+    sampler = ClockSampler(local, during=False)
     sampler.start()
     # the categories are CUDA-event spans around host-issued calls: a Python
     # garbage-collection pause inside one (the iteration allocates thousands
@@ -735,6 +803,7 @@ def run_stack(args):
     import gc
     gc.collect()
     gc.disable()
+    sampler.begin()
     for i in range(args.steps):
         flush.fill_(float(i))
         torch.cuda.synchronize()
@@ -746,6 +815,7 @@ def run_stack(args):
         launches.append(r.gpu_launches)
         for k in cats:
             cats[k].append(getattr(r.times, k))
+    sampler.end()
     gc.enable()
     clocks = sampler.stop()
     per = {k: statistics.mean(v) for k, v in cats.items()}
